@@ -1,0 +1,188 @@
+/*
+ * include/ihs.h -- C ABI of the B200-native Iterative Hessian Sketch hot path
+ * (arXiv 1910.14166, /root/reference/PAPER.md).  Implemented by
+ * paper_1910_14166_b200/libihs.so (hand-written sm_100a CUDA).
+ *
+ * Conventions (apply to every call unless its comment says otherwise)
+ *  - Arrays are fp64 / int row-major, DEVICE pointers on the ctx's device, owned
+ *    by the caller.  The library owns only the scratch inside an ihs_ctx.
+ *  - Every call is stream-ordered on the ctx stream and returns as soon as its
+ *    kernels are enqueued.  Argument errors are returned synchronously and
+ *    nothing is enqueued.  Asynchronous CUDA faults and device-side statuses
+ *    (a non-positive Cholesky pivot, an inner solver hitting its cap) surface
+ *    at the next ihs_ctx_synchronize().  The library never aborts or prints.
+ *  - "Global row": rank k of P holds rows [row_offset, row_offset+n_rows) of
+ *    the global A; the sketch hash always uses the global row index, so the
+ *    per-rank partial sketches sum to S A exactly (linearity).
+ *  - Hash (reading R1; BASELINE.json north_star): with
+ *    SM(x) = splitmix64 finaliser of x + 0x9E3779B97F4A7C15,
+ *    k_t = SM(SM(seed) ^ t), w = SM(k_t ^ (i*s + j)) for global row i and
+ *    SJLT block j, M = m/s, bucket = j*M + ((w>>32)*M >> 32),
+ *    sign = (w & 1) ? -1 : +1.
+ *  - Sign of the gradient (reading R21): g = +A^T (b - A x) = -grad f.
+ */
+#ifndef IHS_H
+#define IHS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IHS_ABI_VERSION 1
+
+typedef enum {
+    IHS_OK = 0,
+    IHS_ERR_INVALID_ARGUMENT = 1,   /* null pointer, negative size, bad spec */
+    IHS_ERR_DIMENSION_MISMATCH = 2, /* e.g. m not divisible by s */
+    IHS_ERR_NOT_SPD = 3,            /* Cholesky pivot <= 0 (reading R13) */
+    IHS_ERR_NOT_CONVERGED = 4,      /* inner PG hit max_inner; best iterate written */
+    IHS_ERR_CUDA = 5,               /* CUDA runtime / launch / async fault */
+    IHS_ERR_COMM = 6,               /* NCCL failure or communicator missing */
+    IHS_ERR_OUT_OF_MEMORY = 7,      /* scratch allocation failed */
+    IHS_ERR_UNSUPPORTED = 8         /* shape outside the kernels' limits */
+} ihs_status;
+
+/* Sketch families (section 2). */
+typedef enum { IHS_COUNTSKETCH = 0, IHS_SJLT = 1 } ihs_family;
+
+typedef struct {
+    int32_t family; /* ihs_family */
+    int32_t s;      /* nonzeros per column of S: 1 for CountSketch; SJLT: 1 <= s <= m, s | m */
+    int64_t m;      /* sketch rows, m >= 1 (m > n is legal) */
+    uint64_t seed;  /* hash seed */
+} ihs_sketch_spec;
+
+typedef enum { IHS_DENSE_ROW_MAJOR = 0, IHS_CSR = 1 } ihs_layout;
+
+/* A local row block of A.  Dense: values[n_rows*n_cols], row-major, 16-byte
+ * aligned.  CSR: row_ptr[n_rows+1] with row_ptr[0] = 0 (rebased per shard),
+ * col_idx[nnz] strictly increasing within a row and < n_cols, values[nnz]. */
+typedef struct {
+    int32_t layout;       /* ihs_layout */
+    int32_t reserved;     /* must be 0 */
+    int64_t n_rows;       /* local rows, 0 <= n_rows < 2^31 */
+    int64_t n_cols;       /* d >= 1 */
+    int64_t row_offset;   /* global index of local row 0 */
+    const double *values;
+    const int64_t *row_ptr;
+    const int32_t *col_idx;
+    int64_t nnz;
+} ihs_matrix;
+
+/* Inner projected-gradient configuration (reading R10). */
+typedef struct {
+    int32_t max_inner;    /* cap on PG steps per outer iteration (default 20000) */
+    int32_t power_iters;  /* power iterations for lambda_max(H) (default 50) */
+    double inner_tol;     /* stop when ||y+ - y|| <= tol * max(1, ||y||) (default 1e-14) */
+    double lip_safety;    /* step 1/(safety * lambda_max) (default 1.05) */
+} ihs_inner_cfg;
+
+/* Per-iteration record written by the solve calls (host memory). Times in ms
+ * from CUDA events on the ctx stream; filled only when trace != NULL. */
+typedef struct {
+    double t_sketch_grad; /* hash/sort + sketch + gradient (a1, a2, a5) */
+    double t_comm;        /* allreduce of [SA | g] (a3), 0 at P = 1 */
+    double t_gram;        /* (SA)^T SA (a4) */
+    double t_solve;       /* inner QP (a6) */
+    int32_t inner_iters;  /* PG steps (l1 ball) or 0 */
+    int32_t status;       /* ihs_status of this iteration's inner solve */
+} ihs_iter_record;
+
+typedef struct ihs_ctx_s *ihs_ctx;
+
+int ihs_abi_version(void);
+const char *ihs_status_string(ihs_status st);
+
+/* Create a context on `device` bound to `stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  One context per (device, stream); no global state. */
+ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream);
+ihs_status ihs_ctx_destroy(ihs_ctx ctx);
+ihs_status ihs_ctx_set_stream(ihs_ctx ctx, void *stream);
+/* Wait for the ctx stream; return the first asynchronous error or device-side
+ * status (IHS_ERR_NOT_SPD, IHS_ERR_NOT_CONVERGED) raised since the last call,
+ * and clear it. */
+ihs_status ihs_ctx_synchronize(ihs_ctx ctx);
+/* Number of kernels this ctx has launched so far (bench evidence). */
+int64_t ihs_ctx_kernel_launches(ihs_ctx ctx);
+
+/* Multi-GPU (BASELINE.json north_star: one allreduce of [SA | g] per
+ * iteration).  ihs_nccl_unique_id writes NCCL's 128-byte id (call on rank 0,
+ * broadcast it); ihs_ctx_set_comm creates this rank's communicator.  NCCL is
+ * resolved at run time from the libnccl.so.2 already loaded in the process. */
+ihs_status ihs_nccl_unique_id(void *out128);
+ihs_status ihs_ctx_set_comm(ihs_ctx ctx, int rank, int world, const void *unique_id128);
+/* In-place sum of count doubles across the ctx communicator (a3). */
+ihs_status ihs_allreduce_sum(ihs_ctx ctx, double *buf, int64_t count);
+
+/* a1: export buckets/signs of global rows [row_begin, row_begin+count), arrays
+ * of count*s entries ordered (row, block) -- bit-exact test interface.
+ * Device pointers. */
+ihs_status ihs_hash(ihs_ctx ctx, const ihs_sketch_spec *spec, uint64_t iter,
+                    int64_t row_begin, int64_t count, int32_t *bucket, int8_t *sign);
+
+/* a2: SA = S^(iter) A_local (m x d), the local partial sketch
+ * (SJLT scaled by 1/sqrt(s)). */
+ihs_status ihs_sketch(ihs_ctx ctx, const ihs_matrix *A, const ihs_sketch_spec *spec,
+                      uint64_t iter, double *SA);
+
+/* a5: g = A_local^T (b_local - A_local x) (d), local partial. */
+ihs_status ihs_grad(ihs_ctx ctx, const ihs_matrix *A, const double *b, const double *x,
+                    double *g);
+
+/* a2 + a5 in one pass over A where the layout allows (dense CountSketch with
+ * d <= 256, CSR); otherwise two passes.  Writes SA (m x d) and g (d); g may
+ * equal SA + m*d so that [SA | g] is one packed buffer for the allreduce. */
+ihs_status ihs_sketch_grad(ihs_ctx ctx, const ihs_matrix *A, const ihs_sketch_spec *spec,
+                           uint64_t iter, const double *b, const double *x,
+                           double *SA, double *g);
+
+/* a4: H = (SA)^T SA (d x d, full symmetric), fp64 on the DMMA tensor pipe
+ * (PAPER.md:95, 104-106).  `scale` multiplies every SA entry on load (1.0, or
+ * 1/sqrt(s) for an unscaled SJLT sum). */
+ihs_status ihs_gram(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, double scale,
+                    double *H);
+
+/* a6, OLS: x_next = x + H^{-1} g by Cholesky (Eq. (2) with C = R^d).  A
+ * non-positive pivot sets IHS_ERR_NOT_SPD (device status) and writes x_next = x.
+ * H is not modified.  x_next may alias x. */
+ihs_status ihs_ols_update(ihs_ctx ctx, const double *H, const double *g, int64_t d,
+                          const double *x, double *x_next);
+
+/* a6, l1 ball {||x||_1 <= radius}: projected gradient on
+ * 1/2 (y-x)^T H (y-x) - g^T (y-x) (reading R10).  inner_iters (device int32,
+ * may be NULL) receives the step count; the cap sets IHS_ERR_NOT_CONVERGED
+ * (device status) with the last iterate written. */
+ihs_status ihs_l1ball_update(ihs_ctx ctx, const double *H, const double *g, int64_t d,
+                             const double *x, double radius, const ihs_inner_cfg *cfg,
+                             double *x_next, int32_t *inner_iters);
+
+/* a1-a7: n_iters IHS steps from x0 (NULL = 0), hash iterations iter0.. .
+ * A/b/x0/x/x_hist may be HOST or DEVICE pointers (detected per pointer); host
+ * inputs are copied in and results copied out inside the call.  x_hist
+ * (optional, (n_iters+1) x d) receives x^0..x^T.  trace (host, optional)
+ * receives n_iters records and makes the call synchronous.  With a
+ * communicator set, [SA | g] is summed across ranks every iteration and every
+ * rank computes the same x.  Returns after the last step is enqueued (or
+ * completed when any host pointer or trace is involved). */
+ihs_status ihs_solve_ols(ihs_ctx ctx, const ihs_matrix *A, const double *b,
+                         const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0,
+                         const double *x0, double *x, double *x_hist,
+                         ihs_iter_record *trace);
+
+ihs_status ihs_solve_l1ball(ihs_ctx ctx, const ihs_matrix *A, const double *b, double radius,
+                            const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0,
+                            const ihs_inner_cfg *cfg, const double *x0, double *x,
+                            double *x_hist, ihs_iter_record *trace);
+
+/* a7 bookkeeping: err2[k] = ||A_local (X[k] - xref)||^2 and ref2 = ||A_local xref||^2
+ * for k < count (X is count x d, device).  One pass over A.  Summed across
+ * ranks by the caller; e_k = sqrt(err2[k] / ref2). */
+ihs_status ihs_pred_err2(ihs_ctx ctx, const ihs_matrix *A, const double *X, int32_t count,
+                         const double *xref, double *err2, double *ref2);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IHS_H */

@@ -1,0 +1,588 @@
+// C ABI of libihs.so (include/ihs.h): context, scratch arena, argument
+// validation, kernel dispatch, the IHS solve loops and the NCCL exchange.
+// Every numerical step runs in the kernels of this directory.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/ihs.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ihs {
+cudaError_t launch_pred_err2_impl(int layout, int64_t n, int64_t d, const double *values, const int64_t *row_ptr,
+                                  const int32_t *col, const double *X, int count, const double *xref,
+                                  double *err2, double *scratch, int num_sms, cudaStream_t st, LaunchCounter lc);
+}
+
+using namespace ihs;
+
+// ----------------------------------------------------------------------------
+// NCCL, resolved at run time (the libnccl.so.2 torch already loaded).
+// ----------------------------------------------------------------------------
+namespace {
+typedef int nccl_result;
+typedef void *nccl_comm;
+struct nccl_uid { char internal[128]; };
+struct NcclApi {
+  bool loaded = false;
+  nccl_result (*GetUniqueId)(nccl_uid *) = nullptr;
+  nccl_result (*CommInitRank)(nccl_comm *, int, nccl_uid, int) = nullptr;
+  nccl_result (*AllReduce)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+  nccl_result (*CommDestroy)(nccl_comm) = nullptr;
+};
+NcclApi g_nccl;
+bool load_nccl() {
+  if (g_nccl.loaded) return true;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.GetUniqueId = (nccl_result(*)(nccl_uid *))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (nccl_result(*)(nccl_comm *, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce =
+      (nccl_result(*)(const void *, void *, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (nccl_result(*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+  g_nccl.loaded = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+  return g_nccl.loaded;
+}
+constexpr int kNcclFloat64 = 8, kNcclSum = 0;
+
+enum Slot {
+  S_PERM, S_HIST, S_TILES, S_GPART, S_GRAM, S_SJLT, S_CHOL, S_PACK, S_H, S_X, S_MISC, S_ERR,
+  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_NSLOTS
+};
+}  // namespace
+
+struct ihs_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  int *d_status = nullptr;
+  int64_t launches = 0;
+  void *slot[S_NSLOTS] = {};
+  size_t cap[S_NSLOTS] = {};
+  nccl_comm comm = nullptr;
+  int rank = 0, world = 1;
+  ihs_status sticky = IHS_OK;
+};
+
+namespace {
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+ihs_status from_cuda(cudaError_t e) {
+  if (e == cudaSuccess) return IHS_OK;
+  if (e == cudaErrorMemoryAllocation) return IHS_ERR_OUT_OF_MEMORY;
+  return IHS_ERR_CUDA;
+}
+
+#define IHS_TRY(expr)                         \
+  do {                                        \
+    ihs_status _s = (expr);                   \
+    if (_s != IHS_OK) return _s;              \
+  } while (0)
+#define IHS_CUDA(expr) IHS_TRY(from_cuda(expr))
+
+template <typename T>
+ihs_status scratch(ihs_ctx c, Slot s, size_t bytes, T **out) {
+  bytes = std::max<size_t>(bytes, 256);
+  if (c->cap[s] < bytes) {
+    if (c->slot[s]) {
+      cudaError_t e = cudaFreeAsync(c->slot[s], c->stream);
+      if (e != cudaSuccess) return from_cuda(e);
+      c->slot[s] = nullptr;
+      c->cap[s] = 0;
+    }
+    size_t want = bytes + bytes / 8;
+    void *p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, want, c->stream);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return IHS_ERR_OUT_OF_MEMORY;
+    }
+    c->slot[s] = p;
+    c->cap[s] = want;
+  }
+  *out = reinterpret_cast<T *>(c->slot[s]);
+  return IHS_OK;
+}
+
+LaunchCounter lc_of(ihs_ctx c) { return LaunchCounter{&c->launches}; }
+
+ihs_status check_spec(const ihs_sketch_spec *spec) {
+  if (!spec) return IHS_ERR_INVALID_ARGUMENT;
+  if (spec->m < 1 || spec->s < 1) return IHS_ERR_INVALID_ARGUMENT;
+  if (spec->family == IHS_COUNTSKETCH) {
+    if (spec->s != 1) return IHS_ERR_INVALID_ARGUMENT;
+  } else if (spec->family == IHS_SJLT) {
+    if (spec->s > spec->m) return IHS_ERR_INVALID_ARGUMENT;
+    if (spec->m % spec->s != 0) return IHS_ERR_DIMENSION_MISMATCH;
+  } else {
+    return IHS_ERR_INVALID_ARGUMENT;
+  }
+  if (spec->m / spec->s > 0xffffffffLL || spec->m > (int64_t(1) << 31)) return IHS_ERR_UNSUPPORTED;
+  return IHS_OK;
+}
+
+ihs_status check_matrix(const ihs_matrix *A) {
+  if (!A || A->reserved != 0) return IHS_ERR_INVALID_ARGUMENT;
+  if (A->n_rows < 0 || A->n_cols < 1 || A->row_offset < 0) return IHS_ERR_INVALID_ARGUMENT;
+  if (A->n_rows >= (int64_t(1) << 31)) return IHS_ERR_UNSUPPORTED;
+  if (A->layout == IHS_DENSE_ROW_MAJOR) {
+    if (A->n_rows > 0 && !A->values) return IHS_ERR_INVALID_ARGUMENT;
+    if (A->n_cols > (int64_t(1) << 30)) return IHS_ERR_UNSUPPORTED;
+  } else if (A->layout == IHS_CSR) {
+    if (!A->row_ptr || A->nnz < 0) return IHS_ERR_INVALID_ARGUMENT;
+    if (A->nnz > 0 && (!A->values || !A->col_idx)) return IHS_ERR_INVALID_ARGUMENT;
+  } else {
+    return IHS_ERR_INVALID_ARGUMENT;
+  }
+  return IHS_OK;
+}
+
+double spec_scale(const ihs_sketch_spec *spec) { return spec->s > 1 ? 1.0 / std::sqrt((double)spec->s) : 1.0; }
+
+// ---- a2 (and a5 when g != null), local partials ------------------------------
+ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter,
+                            const double *b, const double *x, double *SA, double *g) {
+  const uint64_t key = iter_key(spec->seed, iter);
+  const int64_t n = A->n_rows, d = A->n_cols, m = spec->m;
+  const int s = spec->s;
+  cudaStream_t st = c->stream;
+  if (A->layout == IHS_CSR) {
+    if (SA) IHS_CUDA(cudaMemsetAsync(SA, 0, (size_t)m * d * 8, st));
+    if (g) IHS_CUDA(cudaMemsetAsync(g, 0, (size_t)d * 8, st));
+    IHS_CUDA(launch_csr_sketch_grad(n, d, A->row_ptr, A->col_idx, A->values, A->row_offset, key, m, s, SA, b, x, g, st,
+                                    lc_of(c)));
+    if (SA && s > 1) IHS_CUDA(launch_scale(SA, m * d, spec_scale(spec), st, lc_of(c)));
+    return IHS_OK;
+  }
+  // dense
+  const bool use_sort = (s == 1) && cs_sort_supported(m);
+  const bool fuse = SA && use_sort && g && d <= 256;
+  if (SA) {
+    if (use_sort) {
+      CsSortPlan p = cs_sort_plan(n, m);
+      int32_t *hist, *tiles;
+      uint32_t *perm;
+      IHS_TRY(scratch(c, S_HIST, p.hist_bytes(), &hist));
+      IHS_TRY(scratch(c, S_TILES, p.tiles_bytes(), &tiles));
+      IHS_TRY(scratch(c, S_PERM, p.perm_bytes(), &perm));
+      IHS_CUDA(launch_cs_sort(p, key, A->row_offset, hist, tiles, perm, st, lc_of(c)));
+      double *gpart = nullptr;
+      if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)m * d * 8, &gpart));
+      IHS_CUDA(launch_cs_gather(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st, lc_of(c)));
+      if (fuse) IHS_CUDA(launch_reduce_rows(gpart, m, d, g, st, lc_of(c)));
+    } else {
+      SjltPlan p;
+      if (!sjlt_plan(n, d, m, s, c->num_sms, p)) return IHS_ERR_UNSUPPORTED;
+      double *part;
+      IHS_TRY(scratch(c, S_SJLT, p.partial_bytes(), &part));
+      IHS_CUDA(launch_sjlt_dense(p, A->values, key, A->row_offset, part, SA, spec_scale(spec), st, lc_of(c)));
+    }
+  }
+  if (g && !fuse) {
+    if (d > 1024) return IHS_ERR_UNSUPPORTED;
+    const int64_t nb = grad_dense_blocks(n, d, c->num_sms);
+    double *gpart;
+    IHS_TRY(scratch(c, S_GPART, (size_t)nb * d * 8, &gpart));
+    if (n == 0) {
+      IHS_CUDA(cudaMemsetAsync(g, 0, (size_t)d * 8, st));
+    } else {
+      IHS_CUDA(launch_grad_dense(A->values, n, d, b, x, gpart, nb, st, lc_of(c)));
+      IHS_CUDA(launch_reduce_rows(gpart, nb, d, g, st, lc_of(c)));
+    }
+  }
+  return IHS_OK;
+}
+
+ihs_status gram_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {
+  GramPlan p = gram_plan(m, d, c->num_sms);
+  double *part;
+  IHS_TRY(scratch(c, S_GRAM, p.partial_bytes(), &part));
+  IHS_CUDA(launch_gram(p, SA, scale, part, H, c->stream, lc_of(c)));
+  return IHS_OK;
+}
+
+ihs_status ols_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const double *x, double *xn) {
+  double *sc;
+  IHS_TRY(scratch(c, S_CHOL, chol_scratch_bytes(d), &sc));
+  IHS_CUDA(launch_ols_update(H, g, d, x, xn, sc, c->d_status, c->num_sms, c->stream, lc_of(c)));
+  return IHS_OK;
+}
+
+ihs_inner_cfg default_inner() {
+  ihs_inner_cfg k;
+  k.max_inner = 20000;
+  k.power_iters = 50;
+  k.inner_tol = 1e-14;
+  k.lip_safety = 1.05;
+  return k;
+}
+
+ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const double *x, double radius,
+                   const ihs_inner_cfg *cfg, double *xn, int32_t *inner) {
+  ihs_inner_cfg k = cfg ? *cfg : default_inner();
+  if (k.max_inner < 1 || k.power_iters < 1 || !(k.inner_tol >= 0.0) || !(k.lip_safety > 0.0))
+    return IHS_ERR_INVALID_ARGUMENT;
+  if ((size_t)5 * d * 8 > 200 * 1024) return IHS_ERR_UNSUPPORTED;
+  IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.inner_tol, k.lip_safety, xn, inner,
+                                nullptr, c->d_status, c->stream, lc_of(c)));
+  return IHS_OK;
+}
+
+bool is_host_ptr(const void *p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered || a.type == cudaMemoryTypeHost;
+}
+
+ihs_status sync_status(ihs_ctx c) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return from_cuda(e);
+  int st = 0;
+  e = cudaMemcpy(&st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return from_cuda(e);
+  if (st != 0) {
+    int zero = 0;
+    cudaMemcpy(c->d_status, &zero, sizeof(int), cudaMemcpyHostToDevice);
+  }
+  return (ihs_status)st;
+}
+
+// Shared IHS loop (a1-a7).  constraint 0 = OLS, 1 = l1 ball.
+ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const double *b_in, double radius,
+                      const ihs_sketch_spec *spec, int32_t T, uint64_t iter0, const ihs_inner_cfg *cfg,
+                      const double *x0_in, double *x_out, double *xh_out, ihs_iter_record *trace) {
+  IHS_TRY(check_matrix(A_in));
+  IHS_TRY(check_spec(spec));
+  if (T < 0 || !b_in || !x_out) return IHS_ERR_INVALID_ARGUMENT;
+  if (constraint == 1 && !(radius >= 0.0)) return IHS_ERR_INVALID_ARGUMENT;
+  const int64_t n = A_in->n_rows, d = A_in->n_cols, m = spec->m;
+  cudaStream_t st = c->stream;
+  ihs_matrix A = *A_in;
+  bool any_host = false;
+  // host inputs are staged into ctx buffers inside the call (e2e path)
+  if (A.layout == IHS_DENSE_ROW_MAJOR && n > 0 && is_host_ptr(A.values)) {
+    double *dv;
+    IHS_TRY(scratch(c, S_A, (size_t)n * d * 8, &dv));
+    IHS_CUDA(cudaMemcpyAsync(dv, A.values, (size_t)n * d * 8, cudaMemcpyHostToDevice, st));
+    A.values = dv;
+    any_host = true;
+  }
+  if (A.layout == IHS_CSR && is_host_ptr(A.row_ptr)) {
+    int64_t *rp;
+    IHS_TRY(scratch(c, S_RP, (size_t)(n + 1) * 8, &rp));
+    IHS_CUDA(cudaMemcpyAsync(rp, A.row_ptr, (size_t)(n + 1) * 8, cudaMemcpyHostToDevice, st));
+    A.row_ptr = rp;
+    if (A.nnz > 0) {
+      int32_t *cl;
+      double *vl;
+      IHS_TRY(scratch(c, S_COL, (size_t)A.nnz * 4, &cl));
+      IHS_TRY(scratch(c, S_A, (size_t)A.nnz * 8, &vl));
+      IHS_CUDA(cudaMemcpyAsync(cl, A.col_idx, (size_t)A.nnz * 4, cudaMemcpyHostToDevice, st));
+      IHS_CUDA(cudaMemcpyAsync(vl, A.values, (size_t)A.nnz * 8, cudaMemcpyHostToDevice, st));
+      A.col_idx = cl;
+      A.values = vl;
+    }
+    any_host = true;
+  }
+  const double *b = b_in;
+  if (is_host_ptr(b_in)) {
+    double *db;
+    IHS_TRY(scratch(c, S_B, (size_t)std::max<int64_t>(n, 1) * 8, &db));
+    if (n > 0) IHS_CUDA(cudaMemcpyAsync(db, b_in, (size_t)n * 8, cudaMemcpyHostToDevice, st));
+    b = db;
+    any_host = true;
+  }
+  // packed [SA | g], H, iterate history (device)
+  double *pack, *H, *xh;
+  IHS_TRY(scratch(c, S_PACK, (size_t)(m * d + d) * 8, &pack));
+  IHS_TRY(scratch(c, S_H, (size_t)d * d * 8, &H));
+  const bool xh_host = xh_out && is_host_ptr(xh_out);
+  const bool x_host = is_host_ptr(x_out);
+  if (xh_out && !xh_host) {
+    xh = xh_out;
+  } else {
+    IHS_TRY(scratch(c, S_XH, (size_t)(T + 1) * d * 8, &xh));
+  }
+  int32_t *inner_dev = nullptr;
+  if (constraint == 1) IHS_TRY(scratch(c, S_MISC, (size_t)std::max(T, 1) * 4, &inner_dev));
+  if (x0_in) {
+    IHS_CUDA(cudaMemcpyAsync(xh, x0_in, (size_t)d * 8, is_host_ptr(x0_in) ? cudaMemcpyHostToDevice
+                                                                           : cudaMemcpyDeviceToDevice, st));
+  } else {
+    IHS_CUDA(cudaMemsetAsync(xh, 0, (size_t)d * 8, st));
+  }
+  double *SA = pack, *g = pack + m * d;
+  const double scale = 1.0;  // SA leaves sketch_grad_impl already scaled by 1/sqrt(s)
+  cudaEvent_t ev[5] = {};
+  if (trace)
+    for (auto &e : ev) IHS_CUDA(cudaEventCreate(&e));
+  ihs_status result = IHS_OK;
+  for (int32_t t = 0; t < T; ++t) {
+    const double *x = xh + (int64_t)t * d;
+    double *xn = xh + (int64_t)(t + 1) * d;
+    if (trace) cudaEventRecord(ev[0], st);
+    IHS_TRY(sketch_grad_impl(c, &A, spec, iter0 + (uint64_t)t, b, x, SA, g));
+    if (trace) cudaEventRecord(ev[1], st);
+    if (c->world > 1) {
+      if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
+      if (g_nccl.AllReduce(pack, pack, (size_t)(m * d + d), kNcclFloat64, kNcclSum, c->comm, st) != 0)
+        return IHS_ERR_COMM;
+    }
+    if (trace) cudaEventRecord(ev[2], st);
+    IHS_TRY(gram_impl(c, SA, m, d, scale, H));
+    if (trace) cudaEventRecord(ev[3], st);
+    if (constraint == 0) IHS_TRY(ols_impl(c, H, g, d, x, xn));
+    else IHS_TRY(l1_impl(c, H, g, d, x, radius, cfg, xn, inner_dev + t));
+    if (trace) {
+      cudaEventRecord(ev[4], st);
+      IHS_CUDA(cudaEventSynchronize(ev[4]));
+      float ms[4];
+      for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
+      ihs_iter_record &r = trace[t];
+      r.t_sketch_grad = ms[0];
+      r.t_comm = ms[1];
+      r.t_gram = ms[2];
+      r.t_solve = ms[3];
+      r.inner_iters = 0;
+      if (constraint == 1) cudaMemcpy(&r.inner_iters, inner_dev + t, 4, cudaMemcpyDeviceToHost);
+      ihs_status s = sync_status(c);
+      r.status = s;
+      if (s == IHS_ERR_NOT_SPD || (s != IHS_OK && s != IHS_ERR_NOT_CONVERGED)) {
+        result = s;
+        T = t + 1;
+        break;
+      }
+      if (s == IHS_ERR_NOT_CONVERGED) result = s;
+    }
+  }
+  if (trace)
+    for (auto &e : ev) cudaEventDestroy(e);
+  const double *xlast = xh + (int64_t)T * d;
+  if (x_host) {
+    IHS_CUDA(cudaMemcpyAsync(x_out, xlast, (size_t)d * 8, cudaMemcpyDeviceToHost, st));
+  } else if (x_out != xlast) {
+    IHS_CUDA(cudaMemcpyAsync(x_out, xlast, (size_t)d * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  if (xh_out && xh_host)
+    IHS_CUDA(cudaMemcpyAsync(xh_out, xh, (size_t)(T + 1) * d * 8, cudaMemcpyDeviceToHost, st));
+  if (any_host || x_host || xh_host || trace) {
+    ihs_status s = sync_status(c);
+    if (result == IHS_OK) result = s;
+  }
+  return result;
+}
+}  // namespace
+
+extern "C" {
+
+int ihs_abi_version(void) { return IHS_ABI_VERSION; }
+
+const char *ihs_status_string(ihs_status s) {
+  switch (s) {
+    case IHS_OK: return "ok";
+    case IHS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case IHS_ERR_DIMENSION_MISMATCH: return "dimension mismatch";
+    case IHS_ERR_NOT_SPD: return "Hessian sketch not positive definite";
+    case IHS_ERR_NOT_CONVERGED: return "inner solver did not converge";
+    case IHS_ERR_CUDA: return "CUDA error";
+    case IHS_ERR_COMM: return "communication error";
+    case IHS_ERR_OUT_OF_MEMORY: return "out of device memory";
+    case IHS_ERR_UNSUPPORTED: return "unsupported shape";
+  }
+  return "unknown status";
+}
+
+ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
+  if (!out) return IHS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return IHS_ERR_CUDA;
+  }
+  DevGuard g(device);
+  ihs_ctx c = new ihs_ctx_s();
+  c->device = device;
+  c->stream = (cudaStream_t)stream;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMalloc(&c->d_status, sizeof(int)) != cudaSuccess) {
+    delete c;
+    return IHS_ERR_OUT_OF_MEMORY;
+  }
+  cudaMemset(c->d_status, 0, sizeof(int));
+  *out = c;
+  return IHS_OK;
+}
+
+ihs_status ihs_ctx_destroy(ihs_ctx c) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (int s = 0; s < S_NSLOTS; ++s)
+    if (c->slot[s]) cudaFree(c->slot[s]);
+  if (c->d_status) cudaFree(c->d_status);
+  if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
+  delete c;
+  return IHS_OK;
+}
+
+ihs_status ihs_ctx_set_stream(ihs_ctx c, void *stream) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  c->stream = (cudaStream_t)stream;
+  return IHS_OK;
+}
+
+ihs_status ihs_ctx_synchronize(ihs_ctx c) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return from_cuda(e);
+  return sync_status(c);
+}
+
+int64_t ihs_ctx_kernel_launches(ihs_ctx c) { return c ? c->launches : -1; }
+
+ihs_status ihs_nccl_unique_id(void *out128) {
+  if (!out128) return IHS_ERR_INVALID_ARGUMENT;
+  if (!load_nccl()) return IHS_ERR_COMM;
+  nccl_uid id;
+  if (g_nccl.GetUniqueId(&id) != 0) return IHS_ERR_COMM;
+  std::memcpy(out128, &id, sizeof(id));
+  return IHS_OK;
+}
+
+ihs_status ihs_ctx_set_comm(ihs_ctx c, int rank, int world, const void *uid) {
+  if (!c || world < 1 || rank < 0 || rank >= world) return IHS_ERR_INVALID_ARGUMENT;
+  c->rank = rank;
+  c->world = world;
+  if (world == 1) return IHS_OK;
+  if (!uid) return IHS_ERR_INVALID_ARGUMENT;
+  if (!load_nccl()) return IHS_ERR_COMM;
+  DevGuard g(c->device);
+  nccl_uid id;
+  std::memcpy(&id, uid, sizeof(id));
+  if (g_nccl.CommInitRank(&c->comm, world, id, rank) != 0) return IHS_ERR_COMM;
+  return IHS_OK;
+}
+
+ihs_status ihs_allreduce_sum(ihs_ctx c, double *buf, int64_t count) {
+  if (!c || (!buf && count > 0) || count < 0) return IHS_ERR_INVALID_ARGUMENT;
+  if (c->world == 1 || count == 0) return IHS_OK;
+  if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
+  DevGuard g(c->device);
+  if (g_nccl.AllReduce(buf, buf, (size_t)count, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0) return IHS_ERR_COMM;
+  return IHS_OK;
+}
+
+ihs_status ihs_hash(ihs_ctx c, const ihs_sketch_spec *spec, uint64_t iter, int64_t row_begin, int64_t count,
+                    int32_t *bucket, int8_t *sign) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  IHS_TRY(check_spec(spec));
+  if (row_begin < 0 || count < 0 || (count > 0 && (!bucket || !sign))) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  IHS_CUDA(launch_hash_export(iter_key(spec->seed, iter), (uint32_t)spec->s, (uint32_t)(spec->m / spec->s), row_begin,
+                              count, bucket, sign, c->stream, lc_of(c)));
+  return IHS_OK;
+}
+
+ihs_status ihs_sketch(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter, double *SA) {
+  if (!c || !SA) return IHS_ERR_INVALID_ARGUMENT;
+  IHS_TRY(check_matrix(A));
+  IHS_TRY(check_spec(spec));
+  DevGuard g(c->device);
+  return sketch_grad_impl(c, A, spec, iter, nullptr, nullptr, SA, nullptr);
+}
+
+ihs_status ihs_grad(ihs_ctx c, const ihs_matrix *A, const double *b, const double *x, double *gout) {
+  if (!c || !gout || !x || (!b && A && A->n_rows > 0)) return IHS_ERR_INVALID_ARGUMENT;
+  IHS_TRY(check_matrix(A));
+  DevGuard g(c->device);
+  ihs_sketch_spec dummy{IHS_COUNTSKETCH, 1, 1, 0};
+  return sketch_grad_impl(c, A, &dummy, 0, b, x, nullptr, gout);
+}
+
+ihs_status ihs_sketch_grad(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter, const double *b,
+                           const double *x, double *SA, double *gout) {
+  if (!c || !SA || !gout || !x || (!b && A && A->n_rows > 0)) return IHS_ERR_INVALID_ARGUMENT;
+  IHS_TRY(check_matrix(A));
+  IHS_TRY(check_spec(spec));
+  DevGuard g(c->device);
+  return sketch_grad_impl(c, A, spec, iter, b, x, SA, gout);
+}
+
+ihs_status ihs_gram(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {
+  if (!c || !SA || !H || m < 1 || d < 1 || !std::isfinite(scale)) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return gram_impl(c, SA, m, d, scale, H);
+}
+
+ihs_status ihs_ols_update(ihs_ctx c, const double *H, const double *gv, int64_t d, const double *x, double *xn) {
+  if (!c || !H || !gv || !x || !xn || d < 1) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return ols_impl(c, H, gv, d, x, xn);
+}
+
+ihs_status ihs_l1ball_update(ihs_ctx c, const double *H, const double *gv, int64_t d, const double *x, double radius,
+                             const ihs_inner_cfg *cfg, double *xn, int32_t *inner) {
+  if (!c || !H || !gv || !x || !xn || d < 1 || !(radius >= 0.0)) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return l1_impl(c, H, gv, d, x, radius, cfg, xn, inner);
+}
+
+ihs_status ihs_solve_ols(ihs_ctx c, const ihs_matrix *A, const double *b, const ihs_sketch_spec *spec, int32_t n_iters,
+                         uint64_t iter0, const double *x0, double *x, double *x_hist, ihs_iter_record *trace) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return solve_impl(c, 0, A, b, 0.0, spec, n_iters, iter0, nullptr, x0, x, x_hist, trace);
+}
+
+ihs_status ihs_solve_l1ball(ihs_ctx c, const ihs_matrix *A, const double *b, double radius,
+                            const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0, const ihs_inner_cfg *cfg,
+                            const double *x0, double *x, double *x_hist, ihs_iter_record *trace) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return solve_impl(c, 1, A, b, radius, spec, n_iters, iter0, cfg, x0, x, x_hist, trace);
+}
+
+ihs_status ihs_pred_err2(ihs_ctx c, const ihs_matrix *A, const double *X, int32_t count, const double *xref,
+                         double *err2, double *ref2) {
+  if (!c || !xref || !err2 || !ref2 || count < 0 || (count > 0 && !X)) return IHS_ERR_INVALID_ARGUMENT;
+  IHS_TRY(check_matrix(A));
+  if (A->layout == IHS_DENSE_ROW_MAJOR && A->n_cols > 1024) return IHS_ERR_UNSUPPORTED;
+  DevGuard g(c->device);
+  const int64_t d = A->n_cols;
+  const int64_t nb = grad_dense_blocks(A->n_rows, d, c->num_sms);
+  double *sc, *acc;
+  IHS_TRY(scratch(c, S_ERR, (size_t)(((d + 31) / 32) * 32 + nb) * 8, &sc));
+  IHS_TRY(scratch(c, S_MISC, (size_t)(count + 1) * 8, &acc));
+  IHS_CUDA(launch_pred_err2_impl(A->layout, A->n_rows, d, A->values, A->row_ptr, A->col_idx, X, count, xref, acc, sc,
+                                 c->num_sms, c->stream, lc_of(c)));
+  if (count > 0) IHS_CUDA(cudaMemcpyAsync(err2, acc, (size_t)count * 8, cudaMemcpyDeviceToDevice, c->stream));
+  IHS_CUDA(cudaMemcpyAsync(ref2, acc + count, 8, cudaMemcpyDeviceToDevice, c->stream));
+  return IHS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Shared device helpers for the sm_100a IHS kernels (product path only; the
+// oracle under oracle/ shares nothing with this file).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ihs {
+
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ull;
+
+// splitmix64 step (reading R1): golden-gamma add + finaliser.
+__host__ __device__ __forceinline__ uint64_t sm64(uint64_t x) {
+  x += kGamma;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+// k_t = SM(SM(seed) ^ t): one key per IHS iteration, computed on the host.
+__host__ __device__ __forceinline__ uint64_t iter_key(uint64_t seed, uint64_t t) {
+  return sm64(sm64(seed) ^ t);
+}
+
+// Bucket (within [0, m)) and sign bit of global row gi in SJLT block j.
+// bucket = j*M + hi32(hi32(w) * M);  neg = bit 0 of w.
+__device__ __forceinline__ uint32_t hash_bucket(uint64_t key, uint64_t gi, uint32_t j, uint32_t s,
+                                                uint32_t M, bool &neg) {
+  uint64_t w = sm64(key ^ (gi * (uint64_t)s + (uint64_t)j));
+  neg = (w & 1ull) != 0;
+  return j * M + __umulhi((uint32_t)(w >> 32), M);
+}
+
+__device__ __forceinline__ double ldg_stream(const double *p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Transpose-reduce U per-lane partial sums (one per row) across the warp in
+// U-1 + log2(32/U) shuffles instead of U*5.  On return p[0] holds the full sum
+// for row reduced_row_of_lane<U>(lane).
+template <int U>
+__device__ __forceinline__ void transpose_reduce(double (&p)[U], int lane) {
+  static_assert(U == 1 || U == 2 || U == 4 || U == 8 || U == 16 || U == 32, "U");
+  int sh = 16;
+#pragma unroll
+  for (int w = U / 2; w >= 1; w >>= 1, sh >>= 1) {
+    const bool upper = (lane & sh) != 0;
+#pragma unroll
+    for (int i = 0; i < w; ++i) {
+      double send = upper ? p[i] : p[i + w];
+      double keep = upper ? p[i + w] : p[i];
+      p[i] = keep + __shfl_xor_sync(0xffffffffu, send, sh);
+    }
+  }
+#pragma unroll
+  for (; sh >= 1; sh >>= 1) p[0] += __shfl_xor_sync(0xffffffffu, p[0], sh);
+}
+
+template <int U>
+__device__ __forceinline__ int reduced_row_of_lane(int lane) {
+  int u = 0, sh = 16;
+#pragma unroll
+  for (int w = U / 2; w >= 1; w >>= 1, sh >>= 1) u += (lane & sh) ? w : 0;
+  return u;
+}
+
+template <int U>
+__device__ __forceinline__ int owner_lane_of_row(int u) {
+  int lane = 0, sh = 16;
+#pragma unroll
+  for (int w = U / 2; w >= 1; w >>= 1, sh >>= 1)
+    if (u & w) lane |= sh;
+  return lane;
+}
+
+// Device-side status word (first error wins).
+__device__ __forceinline__ void set_status(int *status, int code) {
+  if (status) atomicCAS(status, 0, code);
+}
+
+}  // namespace ihs

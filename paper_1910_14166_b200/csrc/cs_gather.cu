@@ -1,0 +1,147 @@
+// a2 (+ a5 fused, NEXT-1 single pass) for dense CountSketch: one warp per
+// (bucket, 32*NV-column slice) walks the bucket's rows in ascending row order
+// (the stable sort of cs_sort.cu) and sums sign*row in registers -- the same
+// left-to-right fp64 sum as the oracle's loop, so SA is bit-identical to it at
+// P = 1.  With the gradient fused, the same loaded rows also give
+// r_i = b_i - a_i.x (transpose-reduced across the warp) and g += r_i a_i, so A
+// is read from HBM once per IHS iteration.
+//
+// PAPER.md:236-240 (section 2: stream A, bucket h(i) accumulates +-row i) and
+// Eq. (2), PAPER.md:83-86 (the linear term A^T(b - A x^t)).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ihs {
+
+namespace {
+constexpr int kScanTile = 4096;
+
+__device__ __forceinline__ int32_t scanned_at(const int32_t *hist, const int32_t *tile_sums, int64_t e) {
+  return hist[e] + tile_sums[e / kScanTile];
+}
+
+template <int NV, int U, bool FUSE>
+__global__ void __launch_bounds__(64) cs_gather_kernel(const double *__restrict__ A, int64_t n, int d, int m,
+                                                       int nslices, const int32_t *__restrict__ hist,
+                                                       const int32_t *__restrict__ tile_sums, int64_t nchunks,
+                                                       const uint32_t *__restrict__ perm,
+                                                       const double *__restrict__ bvec,
+                                                       const double *__restrict__ x, double *__restrict__ SA,
+                                                       double *__restrict__ gpart) {
+  const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (warp >= m * nslices) return;
+  const int b = warp / nslices;
+  const int slice = warp - b * nslices;
+  const int64_t beg = scanned_at(hist, tile_sums, (int64_t)b * nchunks);
+  const int64_t end = (b + 1 < m) ? scanned_at(hist, tile_sums, (int64_t)(b + 1) * nchunks) : n;
+
+  int col[NV];
+  bool cval[NV];
+  double acc[NV], gacc[NV], xv[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    col[k] = slice * 32 * NV + lane + 32 * k;
+    cval[k] = col[k] < d;
+    acc[k] = 0.0;
+    gacc[k] = 0.0;
+    xv[k] = (FUSE && cval[k]) ? x[col[k]] : 0.0;
+  }
+
+  for (int64_t base = beg; base < end; base += 32) {
+    const uint32_t pe = (base + lane < end) ? perm[base + lane] : 0u;
+    const int cnt = (int)((end - base) < 32 ? (end - base) : 32);
+#pragma unroll 1
+    for (int u0 = 0; u0 < cnt; u0 += U) {
+      double v[U][NV];
+      uint32_t e[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        e[u] = __shfl_sync(0xffffffffu, pe, u0 + u);
+        const double *rowp = A + (int64_t)(e[u] & 0x7fffffffu) * d;
+        const bool rv = (u0 + u) < cnt;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[u][k] = (rv && cval[k]) ? ldg_stream(rowp + col[k]) : 0.0;
+      }
+      if constexpr (FUSE) {
+        double p[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          p[u] = 0.0;
+#pragma unroll
+          for (int k = 0; k < NV; ++k) p[u] = fma(v[u][k], xv[k], p[u]);
+        }
+        transpose_reduce<U>(p, lane);
+        const int myu = reduced_row_of_lane<U>(lane);
+        const uint32_t me = __shfl_sync(0xffffffffu, pe, u0 + myu);
+        const double res = (u0 + myu < cnt) ? bvec[me & 0x7fffffffu] - p[0] : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const double ru = __shfl_sync(0xffffffffu, res, owner_lane_of_row<U>(u));
+#pragma unroll
+          for (int k = 0; k < NV; ++k) gacc[k] = fma(ru, v[u][k], gacc[k]);
+        }
+      }
+      // ascending rows of the bucket: the oracle's summation order
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u0 + u < cnt) {
+          const bool neg = (e[u] >> 31) != 0;
+#pragma unroll
+          for (int k = 0; k < NV; ++k) acc[k] += neg ? -v[u][k] : v[u][k];
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    if (cval[k]) {
+      SA[(int64_t)b * d + col[k]] = acc[k];
+      if constexpr (FUSE) gpart[(int64_t)b * d + col[k]] = gacc[k];
+    }
+  }
+}
+
+template <int NV, int U>
+cudaError_t launch_nv(bool fuse, const double *A, int64_t n, int d, int m, int nslices, const int32_t *hist,
+                      const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
+                      const double *x, double *SA, double *gpart, cudaStream_t st) {
+  const int64_t warps = (int64_t)m * nslices;
+  const unsigned grid = (unsigned)((warps + 1) / 2);
+  if (fuse)
+    cs_gather_kernel<NV, U, true><<<grid, 64, 0, st>>>(A, n, d, m, nslices, hist, tile_sums, nchunks, perm, bvec, x,
+                                                        SA, gpart);
+  else
+    cs_gather_kernel<NV, U, false><<<grid, 64, 0, st>>>(A, n, d, m, nslices, hist, tile_sums, nchunks, perm,
+                                                         nullptr, nullptr, SA, nullptr);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_cs_gather(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
+                             const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
+                             const double *x, double *SA, double *gpart, cudaStream_t st, LaunchCounter lc) {
+  const bool fuse = gpart != nullptr;
+  int nv = (int)((d + 31) / 32);
+  int nslices = 1;
+  if (nv > 8) {
+    if (fuse) return cudaErrorInvalidValue;  // fused path needs a whole row per warp
+    nslices = (int)((d + 255) / 256);
+    nv = 8;
+  }
+  cudaError_t e;
+  const int di = (int)d, mi = (int)m;
+  switch (nv) {
+    case 1: e = launch_nv<1, 16>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
+    case 2: e = launch_nv<2, 16>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
+    case 3: e = launch_nv<3, 8>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
+    case 4: e = launch_nv<4, 8>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
+    case 5:
+    case 6: e = launch_nv<6, 4>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
+    default: e = launch_nv<8, 4>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
+  }
+  lc.add();
+  return e;
+}
+
+}  // namespace ihs

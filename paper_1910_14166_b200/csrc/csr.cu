@@ -1,0 +1,93 @@
+// a2 + a5 for CSR A (BASELINE.json configs[2]): one streaming pass over the
+// CSR arrays.  Each stored entry (i, c, v) is added into its s buckets
+// (O(s nnz(A))), and r_i = b_i - a_i.x feeds g += r_i a_i
+// (Eq. (2)).  With ~1 nonzero per row there is no reuse inside a row, so the
+// sketch scatters with native fp64 reductions into an L2-resident SA
+// (REDG.E.ADD.F64) and the gradient accumulates per CTA in shared memory
+// before one flush.  The summation order is not fixed (documented tolerance,
+// DESIGN.md section 6).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ihs {
+
+namespace {
+template <bool SKETCH, bool GRAD, bool GSMEM>
+__global__ void __launch_bounds__(256) csr_sketch_grad_kernel(int64_t n, int d, const int64_t *__restrict__ row_ptr,
+                                                              const int32_t *__restrict__ col,
+                                                              const double *__restrict__ val, int64_t row_offset,
+                                                              uint64_t key, uint32_t M, int s, double *SA,
+                                                              const double *__restrict__ bvec,
+                                                              const double *__restrict__ x, double *g) {
+  extern __shared__ double gs[];
+  if (GRAD && GSMEM) {
+    for (int c = threadIdx.x; c < d; c += blockDim.x) gs[c] = 0.0;
+    __syncthreads();
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    if (e1 == e0) continue;
+    if (GRAD) {
+      double dot = 0.0;
+      for (int64_t e = e0; e < e1; ++e) dot = fma(val[e], x[col[e]], dot);
+      const double res = bvec[i] - dot;
+      for (int64_t e = e0; e < e1; ++e) {
+        if (GSMEM) atomicAdd(&gs[col[e]], val[e] * res);
+        else atomicAdd(&g[col[e]], val[e] * res);
+      }
+    }
+    if (SKETCH) {
+      for (int j = 0; j < s; ++j) {
+        bool neg;
+        const uint32_t b = hash_bucket(key, (uint64_t)(row_offset + i), (uint32_t)j, (uint32_t)s, M, neg);
+        double *row = SA + (int64_t)b * d;
+        for (int64_t e = e0; e < e1; ++e) {
+          const double v = val[e];
+          atomicAdd(row + col[e], neg ? -v : v);
+        }
+      }
+    }
+  }
+  if (GRAD && GSMEM) {
+    __syncthreads();
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
+      const double t = gs[c];
+      if (t != 0.0) atomicAdd(&g[c], t);
+    }
+  }
+}
+
+template <bool SKETCH, bool GRAD>
+void launch_t(int grid, int64_t n, int d, const int64_t *row_ptr, const int32_t *col, const double *val,
+              int64_t row_offset, uint64_t key, uint32_t M, int s, double *SA, const double *bvec, const double *x,
+              double *g, cudaStream_t st) {
+  const size_t smem = (size_t)d * 8;
+  if (GRAD && smem <= 96 * 1024) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(csr_sketch_grad_kernel<SKETCH, GRAD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    csr_sketch_grad_kernel<SKETCH, GRAD, true><<<grid, 256, smem, st>>>(n, d, row_ptr, col, val, row_offset, key, M,
+                                                                       s, SA, bvec, x, g);
+  } else {
+    csr_sketch_grad_kernel<SKETCH, GRAD, false><<<grid, 256, 0, st>>>(n, d, row_ptr, col, val, row_offset, key, M, s,
+                                                                     SA, bvec, x, g);
+  }
+}
+}  // namespace
+
+cudaError_t launch_csr_sketch_grad(int64_t n, int64_t d, const int64_t *row_ptr, const int32_t *col,
+                                   const double *val, int64_t row_offset, uint64_t key, int64_t m, int s,
+                                   double *SA_unscaled, const double *bvec, const double *x, double *g,
+                                   cudaStream_t st, LaunchCounter lc) {
+  if (n <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  const uint32_t M = (uint32_t)(m / s);
+  const bool sk = SA_unscaled != nullptr, gr = g != nullptr;
+  if (sk && gr) launch_t<true, true>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, SA_unscaled, bvec, x, g, st);
+  else if (sk) launch_t<true, false>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, SA_unscaled, bvec, x, g, st);
+  else if (gr) launch_t<false, true>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, SA_unscaled, bvec, x, g, st);
+  lc.add();
+  return cudaGetLastError();
+}
+
+}  // namespace ihs

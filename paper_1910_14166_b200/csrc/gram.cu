@@ -1,0 +1,164 @@
+// a4: H = (SA)^T SA, the approximate Hessian (section 1;
+// O(m d^2)), the one dense contraction of the path.  fp64 on
+// the DMMA tensor pipe (mma.sync m8n8k4 f64 -> DMMA.8x8x4; tcgen05 has no f64
+// kind on sm_100a).  Only upper-triangular 64x64 tiles are computed (symmetry
+// halves the flops); split-K partials are summed in a fixed order and mirrored.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ihs {
+
+namespace {
+constexpr int GT = 64;       // CTA tile edge
+constexpr int KC = 32;       // rows of SA per smem stage
+constexpr int LDS = GT + 4;  // padded row stride (== 4 mod 16 doubles: conflict-free fragments)
+
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void tri_decode(int t, int tiles, int &P, int &Q) {
+  // row-major enumeration of {(P, Q): P <= Q}
+  int p = 0, rem = t;
+  while (rem >= tiles - p) {
+    rem -= tiles - p;
+    ++p;
+  }
+  P = p;
+  Q = p + rem;
+}
+
+__device__ __forceinline__ void cp_async8(double *smem, const double *gmem, bool pred) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 8 : 0;  // zero-fill when out of range
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+// 4 warps; warp (wm, wn) owns the 32x32 sub-tile [32wm, +32) x [32wn, +32) as
+// 4x4 DMMA 8x8 tiles.  Double-buffered cp.async stages of KC rows.
+__global__ void __launch_bounds__(128) gram_kernel(const double *__restrict__ SA, int64_t m, int d, int tiles,
+                                                   int ntri, int64_t kchunk, double *__restrict__ partials) {
+  extern __shared__ double sm[];
+  double *Xp = sm;                   // [2][KC][LDS]
+  double *Xq = sm + 2 * KC * LDS;    // [2][KC][LDS]
+  int P, Q;
+  tri_decode(blockIdx.x, tiles, P, Q);
+  const bool diag = (P == Q);
+  const int64_t k0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t k1 = min(m, k0 + kchunk);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load_stage = [&](int buf, int64_t kb) {
+    // KC x 64 doubles per matrix: 2048 / 128 threads = 16 each
+#pragma unroll
+    for (int it = 0; it < (KC * GT) / 128; ++it) {
+      int e = it * 128 + tid;
+      int r = e / GT, c = e % GT;
+      int64_t row = kb + r;
+      bool rin = row < k1;
+      int cp = P * GT + c, cq = Q * GT + c;
+      cp_async8(&Xp[(buf * KC + r) * LDS + c], SA + (rin ? row : 0) * d + (cp < d ? cp : 0), rin && cp < d);
+      if (!diag) cp_async8(&Xq[(buf * KC + r) * LDS + c], SA + (rin ? row : 0) * d + (cq < d ? cq : 0), rin && cq < d);
+    }
+    cp_async_commit();
+  };
+
+  const int nstages = (int)((k1 - k0 + KC - 1) / KC);
+  if (nstages > 0) load_stage(0, k0);
+  for (int s = 0; s < nstages; ++s) {
+    const int buf = s & 1;
+    if (s + 1 < nstages) {
+      load_stage(buf ^ 1, k0 + (int64_t)(s + 1) * KC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double *xp = Xp + buf * KC * LDS;
+    const double *xq = (diag ? Xp : Xq) + buf * KC * LDS;
+#pragma unroll
+    for (int kk = 0; kk < KC; kk += 4) {
+      const int kr = kk + (lane & 3);
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = xp[kr * LDS + 32 * wm + 8 * i + (lane >> 2)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = xq[kr * LDS + 32 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  double *out = partials + ((int64_t)blockIdx.y * ntri + blockIdx.x) * (GT * GT);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int r = 32 * wm + 8 * i + (lane >> 2);
+      int c = 32 * wn + 8 * j + 2 * (lane & 3);
+      out[r * GT + c] = acc[i][j][0];
+      out[r * GT + c + 1] = acc[i][j][1];
+    }
+}
+
+// H[p][q] = H[q][p] = scale^2 * sum_split partial (fixed order).
+__global__ void gram_reduce_kernel(const double *__restrict__ partials, int d, int tiles, int ntri, int nsplit,
+                                   double scale2, double *__restrict__ H) {
+  int P, Q;
+  tri_decode(blockIdx.x, tiles, P, Q);
+  for (int e = threadIdx.x; e < GT * GT; e += blockDim.x) {
+    int r = e / GT, c = e % GT;
+    int p = P * GT + r, q = Q * GT + c;
+    if (p >= d || q >= d) continue;
+    if (P == Q && q < p) continue;
+    double s = 0.0;
+    for (int k = 0; k < nsplit; ++k) s += partials[((int64_t)k * ntri + blockIdx.x) * (GT * GT) + e];
+    s *= scale2;
+    H[(int64_t)p * d + q] = s;
+    H[(int64_t)q * d + p] = s;
+  }
+}
+}  // namespace
+
+GramPlan gram_plan(int64_t m, int64_t d, int num_sms) {
+  GramPlan p;
+  p.m = m;
+  p.d = d;
+  p.tiles = (int)((d + GT - 1) / GT);
+  p.ntri = p.tiles * (p.tiles + 1) / 2;
+  // split K so that ~2 waves of CTAs run, with at least 2 stages per CTA
+  int64_t want = std::max<int64_t>(1, (2 * (int64_t)num_sms + p.ntri - 1) / p.ntri);
+  int64_t maxsplit = std::max<int64_t>(1, (m + 2 * KC - 1) / (2 * KC));
+  int64_t ns = std::min(want, maxsplit);
+  int64_t kc = (m + ns - 1) / ns;
+  kc = (kc + KC - 1) / KC * KC;
+  p.kchunk = std::max<int64_t>(kc, KC);
+  p.nsplit = (int)std::max<int64_t>(1, (m + p.kchunk - 1) / p.kchunk);
+  return p;
+}
+
+cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
+                        cudaStream_t st, LaunchCounter lc) {
+  const size_t smem = (size_t)4 * KC * LDS * 8;
+  cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid(p.ntri, p.nsplit);
+  gram_kernel<<<grid, 128, smem, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kchunk, partials);
+  gram_reduce_kernel<<<p.ntri, 256, 0, st>>>(partials, (int)p.d, p.tiles, p.ntri, p.nsplit, scale * scale, H);
+  lc.add(2);
+  return cudaGetLastError();
+}
+
+}  // namespace ihs

@@ -1,0 +1,103 @@
+// Host-side launchers of the sm_100a kernels (internal to libihs.so).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ihs {
+
+struct LaunchCounter {
+  int64_t *count = nullptr;
+  void add(int64_t k = 1) const { if (count) *count += k; }
+};
+
+// ---- a1: hash export --------------------------------------------------------
+cudaError_t launch_hash_export(uint64_t key, uint32_t s, uint32_t M, int64_t row_begin, int64_t count,
+                               int32_t *bucket, int8_t *sign, cudaStream_t st, LaunchCounter lc);
+
+// ---- a1 + a2 (s = 1 dense): stable counting sort of local rows by bucket ----
+struct CsSortPlan {
+  int64_t n = 0;          // local rows
+  int64_t m = 0;          // buckets
+  int64_t chunk = 0;      // rows per CTA chunk
+  int64_t nchunks = 0;
+  int64_t entries = 0;    // m * nchunks
+  int64_t ntiles = 0;     // scan tiles
+  size_t hist_bytes() const { return (size_t)(entries + 1) * 4; }
+  size_t tiles_bytes() const { return (size_t)(ntiles + 1) * 4; }
+  size_t perm_bytes() const { return (size_t)n * 4; }
+};
+CsSortPlan cs_sort_plan(int64_t n, int64_t m);
+bool cs_sort_supported(int64_t m);
+// hist: entries+1 int32 (bucket-major offsets after the scan); perm: n int32
+// (local row | sign << 31), rows of bucket b at [hist[b*nchunks], hist[(b+1)*nchunks]).
+cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset, int32_t *hist,
+                           int32_t *tile_sums, uint32_t *perm, cudaStream_t st, LaunchCounter lc);
+
+// ---- a2 (+a5 fused): bucket-ordered segmented signed row sums ---------------
+// SA[b, :] = sum over rows of bucket b (ascending) of sign * A[row, :], times scale.
+// If b_vec/x/gpart are non-null: gpart[b, :] = sum_rows A[row,:] * (b_row - A[row,:].x).
+cudaError_t launch_cs_gather(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
+                             const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
+                             const double *x, double *SA, double *gpart, cudaStream_t st, LaunchCounter lc);
+
+// ---- a2 dense SJLT (s > 1): smem-tile accumulation --------------------------
+struct SjltPlan {
+  int64_t n = 0, d = 0, m = 0;
+  int s = 0;
+  int dc = 0;       // columns per CTA tile
+  int nslices = 0;  // ceil(d / dc)
+  int nsplit = 0;   // row splits (partials reduced in fixed order)
+  size_t smem = 0;
+  size_t partial_bytes() const { return (size_t)nsplit * m * d * 8; }
+};
+bool sjlt_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, SjltPlan &p);
+cudaError_t launch_sjlt_dense(const SjltPlan &p, const double *A, uint64_t key, int64_t row_offset,
+                              double *partials, double *SA, double scale, cudaStream_t st, LaunchCounter lc);
+
+// ---- CSR sketch and gradient (atomics into L2) ------------------------------
+// SA must be zeroed first when sketching.  g must be zeroed when gradient.
+cudaError_t launch_csr_sketch_grad(int64_t n, int64_t d, const int64_t *row_ptr, const int32_t *col,
+                                   const double *val, int64_t row_offset, uint64_t key, int64_t m, int s,
+                                   double *SA_unscaled, const double *bvec, const double *x, double *g,
+                                   cudaStream_t st, LaunchCounter lc);
+cudaError_t launch_scale(double *buf, int64_t count, double scale, cudaStream_t st, LaunchCounter lc);
+
+// ---- a5 dense gradient -------------------------------------------------------
+int64_t grad_dense_blocks(int64_t n, int64_t d, int num_sms);
+cudaError_t launch_grad_dense(const double *A, int64_t n, int64_t d, const double *bvec, const double *x,
+                              double *gpart, int64_t nblocks, cudaStream_t st, LaunchCounter lc);
+// out[c] = sum_{r < rows} part[r*d + c] (fixed order), c < d.
+cudaError_t launch_reduce_rows(const double *part, int64_t rows, int64_t d, double *out, cudaStream_t st,
+                               LaunchCounter lc);
+
+// ---- a4 Gram on DMMA ---------------------------------------------------------
+struct GramPlan {
+  int64_t m = 0, d = 0;
+  int tiles = 0;    // tiles per side (64-wide)
+  int ntri = 0;     // upper-triangular tiles
+  int nsplit = 0;   // split-K
+  int64_t kchunk = 0;
+  size_t partial_bytes() const { return (size_t)nsplit * ntri * 64 * 64 * 8; }
+};
+GramPlan gram_plan(int64_t m, int64_t d, int num_sms);
+cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
+                        cudaStream_t st, LaunchCounter lc);
+
+// ---- a6 OLS: Cholesky solve ----------------------------------------------------
+size_t chol_scratch_bytes(int64_t d);
+cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,
+                              double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc);
+
+// ---- a6 l1 ball: projected gradient -----------------------------------------
+size_t pg_scratch_bytes(int64_t d);
+cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
+                                 int max_inner, int power_iters, double tol, double safety, double *x_next,
+                                 int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
+                                 LaunchCounter lc);
+
+// ---- a7 error norms ----------------------------------------------------------
+cudaError_t launch_pred_err2(int layout, int64_t n, int64_t d, const double *values, const int64_t *row_ptr,
+                             const int32_t *col, const double *X, int count, const double *xref,
+                             double *acc /* count+1, zeroed */, cudaStream_t st, LaunchCounter lc);
+
+}  // namespace ihs

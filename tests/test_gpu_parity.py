@@ -1,0 +1,297 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element
+by element on the same seeded inputs, at sizes that span several tiles and a
+ragged tail.  Tolerances (BASELINE.json north_star):
+  buckets/signs          bit-exact
+  SA, H                  relative Frobenius <= 1e-12 (dense CountSketch SA: bit-exact)
+  g                      |g - g_ora|_c <= 1e-12 * sum_i |A_ic r_i|   (reading R12)
+  iterates               ||A(x - x_ora)|| / ||A x_ora|| <= 1e-9      (reading R8(i))
+"""
+import numpy as np
+import pytest
+import torch
+
+import synthetic
+
+pytestmark = pytest.mark.gpu
+
+DEV = torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1910_14166_b200 as P
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    P.lib()
+    return P
+
+
+def rel_fro(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+def grad_bound(A, b, x):
+    r = b - A @ x
+    return 1e-12 * (np.abs(A) * np.abs(r)[:, None]).sum(0) + 1e-300
+
+
+def dense_case(cfg_name, n, seed_shift=0):
+    cfg = synthetic.CONFIGS[cfg_name].scaled(n)
+    prob = synthetic.problem(cfg, "cpu")
+    return cfg, prob["A"].numpy(), prob["b"].numpy(), prob
+
+
+# ---------------------------------------------------------------- a1 hash
+@pytest.mark.parametrize("m,s,row_begin,count", [(200, 1, 0, 2000), (1024, 1, 3, 100_003), (8192, 4, 0, 65_536),
+                                                 (2048, 1, (1 << 21) - 77, 77), (4096, 8, (1 << 25) - 1000, 1000),
+                                                 (7, 7, 123, 10), (1, 1, 0, 5)])
+def test_hash_bit_exact(P, oracle_mod, m, s, row_begin, count):
+    for t in (0, 1, 29):
+        bg, sg = P.ihs_hash(P.Spec(m=m, s=s, seed=0), t, row_begin, count)
+        bo, so = oracle_mod.hash_rows(0, t, m, s, row_begin, count)
+        np.testing.assert_array_equal(bg.cpu().numpy(), bo)
+        np.testing.assert_array_equal(sg.cpu().numpy(), so)
+
+
+# ---------------------------------------------------------------- a2 sketch
+@pytest.mark.parametrize("n,d,m", [(2000, 10, 200), (65_536 + 77, 128, 1024), (40_000, 256, 2048), (5000, 96, 64),
+                                   (3000, 33, 300), (1000, 300, 128), (100, 17, 500), (1, 5, 3), (0, 8, 16)])
+def test_countsketch_dense_bit_exact(P, oracle_mod, n, d, m):
+    rng = np.random.default_rng(n + d)
+    A = rng.standard_normal((n, d))
+    for t in (0, 5):
+        SA = P.ihs_sketch(torch.from_numpy(A).to(DEV), P.Spec(m=m, s=1, seed=7), t).cpu().numpy()
+        np.testing.assert_array_equal(SA, oracle_mod.sketch_dense(A, 7, t, m, 1))
+
+
+def test_countsketch_row_offset_shards(P, oracle_mod):
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((9000, 40))
+    Ad = torch.from_numpy(A).to(DEV)
+    spec = P.Spec(m=256, s=1, seed=3)
+    full = oracle_mod.sketch_dense(A, 3, 2, 256, 1)
+    tot = np.zeros_like(full)
+    for k in range(0, 9000, 3000):
+        part = P.ihs_sketch(P.Dense(Ad[k:k + 3000], row_offset=k), spec, 2).cpu().numpy()
+        np.testing.assert_array_equal(part, oracle_mod.sketch_dense(A[k:k + 3000], 3, 2, 256, 1, row_offset=k))
+        tot += part
+    assert rel_fro(tot, full) <= 1e-12
+
+
+@pytest.mark.parametrize("n,d,m,s", [(65_536 + 11, 96, 4096, 8), (20_000, 10, 200, 4), (30_000, 40, 512, 2),
+                                     (5000, 7, 4096, 8), (257, 3, 64, 64), (0, 4, 16, 2)])
+def test_sjlt_dense(P, oracle_mod, n, d, m, s):
+    rng = np.random.default_rng(n + m)
+    A = rng.standard_normal((n, d))
+    SA = P.ihs_sketch(torch.from_numpy(A).to(DEV), P.Spec(m=m, s=s, seed=0), 4).cpu().numpy()
+    ref = oracle_mod.sketch_dense(A, 0, 4, m, s)
+    assert rel_fro(SA, ref) <= 1e-12
+
+
+def csr_case(n, d, p, seed):
+    cfg = synthetic.Config("csr", n, d, "csr", "normal", "sjlt", 64, 4, 1, "ols", density=p, data_seed=seed)
+    rp, cl, vl = synthetic.csr_A(cfg, "cpu")
+    return rp.numpy(), cl.numpy(), vl.numpy()
+
+
+@pytest.mark.parametrize("n,d,p,m,s", [(65_536, 1024, 1e-3, 8192, 4), (20_000, 50, 0.05, 500, 1),
+                                       (3000, 300, 0.04, 3000, 4), (100, 10, 0.0, 8, 2)])
+def test_csr_sketch_and_grad(P, oracle_mod, n, d, p, m, s):
+    rp, cl, vl = csr_case(n, d, p, 3)
+    A = (torch.from_numpy(rp).to(DEV), torch.from_numpy(cl).to(DEV), torch.from_numpy(vl).to(DEV), d)
+    spec = P.Spec(m=m, s=s, seed=0)
+    SA = P.ihs_sketch(A, spec, 1).cpu().numpy()
+    ref = oracle_mod.sketch_csr(rp, cl, vl, d, 0, 1, m, s)
+    assert rel_fro(SA, ref) <= 1e-12
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(n)
+    x = rng.standard_normal(d)
+    g = P.ihs_grad(A, torch.from_numpy(b).to(DEV), torch.from_numpy(x).to(DEV)).cpu().numpy()
+    go = oracle_mod.grad_csr(rp, cl, vl, d, b, x)
+    import scipy.sparse as sp
+    M = sp.csr_matrix((vl, cl, rp), shape=(n, d))
+    r = b - M @ x
+    bound = 1e-12 * (abs(M).T @ np.abs(r)) + 1e-300
+    assert (np.abs(g - go) <= bound).all()
+    pack, SA2, g2 = P.ihs_sketch_grad(A, spec, 1, torch.from_numpy(b).to(DEV), torch.from_numpy(x).to(DEV))
+    assert rel_fro(SA2.cpu().numpy(), ref) <= 1e-12
+    assert (np.abs(g2.cpu().numpy() - go) <= bound).all()
+
+
+# ---------------------------------------------------------------- a5 gradient
+@pytest.mark.parametrize("cfg_name,n", [("C1", 2000), ("C2", 70_001), ("C4", 30_000), ("C5", 50_000)])
+def test_grad_dense(P, oracle_mod, cfg_name, n):
+    cfg, A, b, _ = dense_case(cfg_name, n)
+    x = np.random.default_rng(2).standard_normal(cfg.d)
+    g = P.ihs_grad(torch.from_numpy(A).to(DEV), torch.from_numpy(b).to(DEV), torch.from_numpy(x).to(DEV))
+    go = oracle_mod.grad_dense(A, b, x)
+    assert (np.abs(g.cpu().numpy() - go) <= grad_bound(A, b, x)).all()
+
+
+@pytest.mark.parametrize("n,d,m", [(70_001, 128, 1024), (30_000, 256, 2048), (2000, 10, 200), (9000, 96, 300),
+                                   (500, 1, 7)])
+def test_fused_sketch_grad(P, oracle_mod, n, d, m):
+    rng = np.random.default_rng(d)
+    A = rng.standard_normal((n, d))
+    b = rng.standard_normal(n)
+    x = rng.standard_normal(d)
+    pack, SA, g = P.ihs_sketch_grad(torch.from_numpy(A).to(DEV), P.Spec(m=m), 3, torch.from_numpy(b).to(DEV),
+                                    torch.from_numpy(x).to(DEV))
+    np.testing.assert_array_equal(SA.cpu().numpy(), oracle_mod.sketch_dense(A, 0, 3, m, 1))
+    assert (np.abs(g.cpu().numpy() - oracle_mod.grad_dense(A, b, x)) <= grad_bound(A, b, x)).all()
+
+
+# ---------------------------------------------------------------- a4 Gram
+@pytest.mark.parametrize("m,d", [(200, 10), (1024, 128), (2048, 256), (4096, 96), (777, 130), (64, 1), (3, 70),
+                                 (8192, 1024)])
+def test_gram(P, oracle_mod, m, d):
+    rng = np.random.default_rng(m * d)
+    SA = rng.standard_normal((m, d))
+    H = P.ihs_gram(torch.from_numpy(SA).to(DEV)).cpu().numpy()
+    Ho = oracle_mod.gram(SA)
+    assert rel_fro(H, Ho) <= 1e-12
+    np.testing.assert_array_equal(H, H.T)
+    H2 = P.ihs_gram(torch.from_numpy(SA).to(DEV), scale=0.5).cpu().numpy()
+    assert rel_fro(H2, 0.25 * Ho) <= 1e-12
+
+
+# ---------------------------------------------------------------- a6 inner QP
+def spd(rng, d, cond=13.0):
+    Q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    return (Q * np.geomspace(1.0, cond, d)) @ Q.T * 50.0
+
+
+@pytest.mark.parametrize("d", [1, 10, 96, 128, 160, 256])
+def test_ols_update(P, oracle_mod, d):
+    rng = np.random.default_rng(d)
+    H = spd(rng, d)
+    g = rng.standard_normal(d)
+    x = rng.standard_normal(d)
+    xn = P.ihs_ols_update(torch.from_numpy(H).to(DEV), torch.from_numpy(g).to(DEV), torch.from_numpy(x).to(DEV))
+    xo = oracle_mod.ols_step(H, g, x)
+    u, uo = xn.cpu().numpy() - x, xo - x
+    assert np.linalg.norm(u - uo) <= 1e-12 * np.linalg.norm(uo)
+
+
+def test_ols_update_not_spd(P):
+    ctx = P.Context(0)
+    H = torch.diag(torch.tensor([1.0, -1.0, 2.0], dtype=torch.float64, device=DEV))
+    x = torch.ones(3, dtype=torch.float64, device=DEV)
+    xn = P.ihs_ols_update(H, x, x, ctx=ctx)
+    assert ctx.status() == P.ERR_NOT_SPD
+    assert torch.equal(xn, x)
+    assert ctx.status() == P.OK  # status is cleared once read
+
+
+@pytest.mark.parametrize("d,tau", [(16, 1.0), (256, 10.0), (64, 1e9), (5, 0.0)])
+def test_l1ball_update(P, oracle_mod, d, tau):
+    rng = np.random.default_rng(d)
+    H = spd(rng, d)
+    g = rng.standard_normal(d) * 10
+    x = np.zeros(d)
+    inner = torch.zeros(1, dtype=torch.int32, device=DEV)
+    xn = P.ihs_l1ball_update(torch.from_numpy(H).to(DEV), torch.from_numpy(g).to(DEV), torch.from_numpy(x).to(DEV),
+                             tau, inner=inner).cpu().numpy()
+    xo, it, st = oracle_mod.l1ball_step(H, g, x, tau)
+    assert st == oracle_mod.OK
+    assert np.linalg.norm(xn - xo) <= 1e-10 * max(1.0, np.linalg.norm(xo))
+    assert int(inner.item()) >= 1
+    assert np.abs(xn).sum() <= tau * (1 + 1e-12) + 1e-300
+
+
+# ---------------------------------------------------------------- a1-a7 IHS loops
+def iterate_parity(A, xg, xo, oracle_mod):
+    return max(oracle_mod.pred_rel_err(a, b, A) for a, b in zip(xg[1:], xo[1:]))
+
+
+def test_ihs_ols_C1_full(P, oracle_mod):
+    cfg = synthetic.CONFIGS["C1"]
+    prob = synthetic.problem(cfg, "cpu")
+    A, b = prob["A"].numpy(), prob["b"].numpy()
+    out = P.ihs_solve_ols(prob["A"].to(DEV), prob["b"].to(DEV), P.Spec(m=cfg.m), cfg.T, trace=True)
+    xh = out["x_hist"].cpu().numpy()
+    xo, _ = oracle_mod.ihs_solve(A, b, m=cfg.m, s=1, T=cfg.T)
+    assert iterate_parity(A, xh, xo, oracle_mod) <= 1e-9
+    xopt = oracle_mod.exact_ols(A, b)
+    e = [oracle_mod.pred_rel_err(x, xopt, A) for x in xh]
+    assert e[-1] < 1e-4 and all(e[t + 1] < e[t] for t in range(4))
+    assert len(out["trace"]) == cfg.T and all(r["status"] == 0 for r in out["trace"])
+
+
+@pytest.mark.parametrize("cfg_name,n,T", [("C2", 1 << 16, 8), ("C5", 1 << 15, 6), ("C3", 1 << 16, 4)])
+def test_ihs_ols_scaled_configs(P, oracle_mod, cfg_name, n, T):
+    cfg = synthetic.CONFIGS[cfg_name].scaled(n)
+    prob = synthetic.problem(cfg, "cpu")
+    spec = P.Spec(m=cfg.m, s=cfg.s)
+    b = prob["b"].numpy()
+    if cfg.layout == "dense":
+        A = prob["A"].numpy()
+        out = P.ihs_solve_ols(prob["A"].to(DEV), prob["b"].to(DEV), spec, T)
+        xo, _ = oracle_mod.ihs_solve(A, b, m=cfg.m, s=cfg.s, T=T)
+        par = iterate_parity(A, out["x_hist"].cpu().numpy(), xo, oracle_mod)
+    else:
+        rp, cl, vl = (t.numpy() for t in prob["csr"])
+        Ad = tuple(t.to(DEV) for t in prob["csr"]) + (cfg.d,)
+        out = P.ihs_solve_ols(Ad, prob["b"].to(DEV), spec, T)
+        xo, _ = oracle_mod.ihs_solve(b=b, csr=(rp, cl, vl), d=cfg.d, m=cfg.m, s=cfg.s, T=T)
+        xg = out["x_hist"].cpu().numpy()
+        par = max(oracle_mod.pred_rel_err(a, c, csr=(rp, cl, vl), d=cfg.d) for a, c in zip(xg[1:], xo[1:]))
+    assert par <= 1e-9
+
+
+def test_ihs_l1ball_scaled_C4(P, oracle_mod):
+    cfg = synthetic.CONFIGS["C4"].scaled(1 << 15)
+    prob = synthetic.problem(cfg, "cpu")
+    A, b, tau = prob["A"].numpy(), prob["b"].numpy(), prob["tau"]
+    T = 8
+    out = P.ihs_solve_l1ball(prob["A"].to(DEV), prob["b"].to(DEV), tau, P.Spec(m=cfg.m), T, trace=True)
+    xo, inner = oracle_mod.ihs_solve(A, b, m=cfg.m, s=1, T=T, constraint="l1ball", tau=tau)
+    assert iterate_parity(A, out["x_hist"].cpu().numpy(), xo, oracle_mod) <= 1e-9
+    its = [r["inner_iters"] for r in out["trace"]]
+    assert all(i >= 1 for i in its)
+
+
+def test_solve_with_host_buffers(P, oracle_mod):
+    """e2e path: host A/b/x, copies inside the call."""
+    cfg = synthetic.CONFIGS["C1"]
+    prob = synthetic.problem(cfg, "cpu")
+    A = prob["A"].pin_memory()
+    b = prob["b"].pin_memory()
+    out = P.ihs_solve_ols(A, b, P.Spec(m=cfg.m), cfg.T)
+    assert out["x"].device.type == "cpu"
+    xo, _ = oracle_mod.ihs_solve(A.numpy(), b.numpy(), m=cfg.m, s=1, T=cfg.T)
+    assert oracle_mod.pred_rel_err(out["x"].numpy(), xo[-1], A.numpy()) <= 1e-9
+
+
+def test_pred_err2(P, oracle_mod):
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((50_000, 128))
+    X = rng.standard_normal((4, 128))
+    xr = rng.standard_normal(128)
+    e2, r2 = P.ihs_pred_err2(torch.from_numpy(A).to(DEV), torch.from_numpy(X).to(DEV), torch.from_numpy(xr).to(DEV))
+    e = np.sqrt(e2.cpu().numpy() / r2.item())
+    ref = np.array([oracle_mod.pred_rel_err(x, xr, A) for x in X])
+    np.testing.assert_allclose(e, ref, rtol=1e-11)
+
+
+def test_invalid_arguments(P):
+    A = torch.zeros((10, 4), dtype=torch.float64, device=DEV)
+    with pytest.raises(P.IhsError) as e:
+        P.ihs_sketch(A, P.Spec(m=10, s=3, family=P.SJLT), 0)
+    assert e.value.status == P.ERR_DIMENSION_MISMATCH
+    with pytest.raises(P.IhsError):
+        P.ihs_sketch(A, P.Spec(m=10, s=2, family=P.COUNTSKETCH), 0)
+    with pytest.raises(P.IhsError):
+        P.ihs_sketch(A, P.Spec(m=0), 0)
+
+
+def test_deterministic_rerun(P):
+    rng = np.random.default_rng(9)
+    A = torch.from_numpy(rng.standard_normal((100_000, 96))).to(DEV)
+    a = P.ihs_sketch(A, P.Spec(m=4096, s=8), 2)
+    b = P.ihs_sketch(A, P.Spec(m=4096, s=8), 2)
+    assert torch.equal(a, b)
+    H1 = P.ihs_gram(a)
+    H2 = P.ihs_gram(b)
+    assert torch.equal(H1, H2)
