@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Benchmark of the IHS hot path on B200 (BASELINE.json metric: "sketch rows/sec &
+HBM GB/s vs peak; IHS time-to-1e-10 rel error, 1/2/4/8 GPU").
+
+A step is one IHS iteration over the whole configuration:
+hash + stable bucket sort (a1), fused sketch + gradient over A (a2 + a5), the
+all-reduce of [SA | g] across ranks (a3), the DMMA Gram (a4) and the Cholesky
+update (a6).  Default workload: BASELINE.json configs[1] (C2, dense OLS,
+A 2^22 x 128 fp64 AR(1) rows, CountSketch m = 1024), row-sharded over the N
+ranks (strong scaling: the problem is fixed, N GPUs share its rows).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl product|reference]
+
+Prints ONE JSON line on rank 0.  value = rows of A sketched per second over the
+whole job (n_global * K / max-over-ranks device time).  The oracle (oracle/) is
+executed only by the cpu_baseline leg and by --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sketch rows/sec & HBM GB/s vs peak; IHS time-to-1e-10 rel error, 1/2/4/8 GPU"
+UNIT = "rows/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-10 solve")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def config_obj(cfg, world, extra=None):
+    o = {"workload": f"{cfg.name}: {'CSR' if cfg.layout == 'csr' else 'dense'} OLS A {cfg.n}x{cfg.d} fp64 "
+                     f"({cfg.dist}), {cfg.family} m={cfg.m} s={cfg.s}",
+         "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "sketch": cfg.family,
+         "parallelism": f"row-shard x{world} + allreduce[SA|g]" if world > 1 else "single GPU",
+         "l2": "inputs larger than L2 (A = %.2f GiB per step)" % (cfg.a_bytes / 2**30)}
+    if extra:
+        o.update(extra)
+    return o
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """dram read+write bytes per launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)
+        return d.get(kernel)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import synthetic
+    cfg = synthetic.CONFIGS[args.config]
+    rows = min(cfg.n, 1 << 20)
+    scfg = cfg.scaled(rows)
+    prob = synthetic.problem(scfg, "cpu")
+    if cfg.layout != "dense":
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for dense configs"}))
+        return 0
+    A, b = prob["A"].numpy(), prob["b"].numpy()
+    x = np.zeros(cfg.d)
+    for w in range(args.warmup):
+        xh, _ = oracle.ihs_solve(A, b, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=w, x0=x)
+        x = xh[-1]
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        xh, _ = oracle.ihs_solve(A, b, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=args.warmup + k, x0=x)
+        x = xh[-1]
+    el = time.perf_counter() - t0
+    value = rows * args.steps / el
+    sample = f"first {rows} rows of {cfg.name} ({rows}x{cfg.d}), one oracle IHS iteration per step"
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded, BASELINE.json recipe)", "config": config_obj(cfg, 1),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+# ----------------------------------------------------------------------------- product arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_14166_b200 as P
+    import synthetic
+    from paper_1910_14166_b200.dist import CudaOps, ShardedIHS, shard_rows
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synthetic.CONFIGS[args.config]
+    if cfg.layout != "dense" or cfg.s != 1 or cfg.constraint != "ols":
+        raise SystemExit("bench.py times the dense CountSketch OLS configs (C1, C2)")
+    r0, r1 = shard_rows(cfg.n, rank, world)
+    # ---- inputs, resident in HBM before timing
+    A = synthetic.dense_A(cfg, dev, rows=(r0, r1))
+    xs = synthetic.x_star(cfg, dev)
+    b = (A @ xs + synthetic.noise(cfg, dev)[r0:r1]).contiguous()
+    del xs
+    ctx = P.Context(local)
+    spec = P.Spec(m=cfg.m, s=cfg.s, seed=cfg.hash_seed)
+    Am = P.Dense(A, row_offset=r0)
+    S = ShardedIHS(Am, b, spec, ops=CudaOps(ctx))
+    d = cfg.d
+    xa = torch.zeros(d, dtype=torch.float64, device=dev)
+    xb = torch.empty_like(xa)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    t = 0
+    for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
+        S.step(t, xa, xb)
+        xa, xb = xb, xa
+        t += 1
+    barrier()
+    ctx.set_profiling(True)
+    ctx.profile_reset()
+    l0 = ctx.kernel_launches
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        S.step(t, xa, xb)
+        xa, xb = xb, xa
+        t += 1
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.kernel_launches - l0
+    ms_local = e0.elapsed_time(e1)
+    mt = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mt, op=dist.ReduceOp.MAX)
+    ms = float(mt.item())
+    ms_step = ms / args.steps
+    value = cfg.n * args.steps / (ms / 1e3)
+    prof = {name: ctx.profile(k) for k, name in enumerate(P.KERNEL_GROUPS)}
+    ctx.set_profiling(False)
+    # ---- roofline of the dominant kernel: the fused sketch+gradient gather
+    peaks, peak_src = measured_peaks()
+    n_loc = r1 - r0
+    sk_ms, sk_n = prof["sketch"]
+    alg_bytes = 8 * n_loc * d + 12 * n_loc + 16 * cfg.m * d  # A once, b + perm per row, SA + g partials
+    sk_avg = sk_ms / max(sk_n, 1)
+    achieved = alg_bytes / (sk_avg / 1e3) / 1e9 if sk_n else None
+    roof = {"kernel": "cs_gather_kernel<4,8,true> (fused CountSketch sketch + gradient)", "bound": "hbm",
+            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"] if achieved else None,
+            "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+            "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": sk_avg,
+            "traffic": ncu_traffic("cs_gather_kernel"),
+            "share_of_step": (sk_ms / ms_local) if ms_local > 0 else None}
+    breakdown = {name: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for name, v in prof.items() if v[1]}
+    # ---- time to 1e-10 (IHS solve from x^0 = 0; errors post hoc, outside the timing)
+    ttt = None
+    if not args.no_ttt:
+        xopt = S.exact_ols()
+        Tmax = 60
+        xh = S.solve(Tmax, iter0=1000)
+        err = S.pred_errors(xh, xopt).cpu().tolist()
+        tstar = next((k for k, e in enumerate(err) if e <= 1e-10), None)
+        ttt = {"target": 1e-10, "iterations": tstar, "err_at_20": err[20], "err_final": err[-1],
+               "errors_first": [float("%.3e" % e) for e in err[:tstar + 1 if tstar else 31]]}
+        if tstar:
+            barrier()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            x0 = torch.zeros(d, dtype=torch.float64, device=dev)
+            xh2 = torch.zeros((tstar + 1, d), dtype=torch.float64, device=dev)
+            f0.record(stream)
+            for k in range(tstar):
+                S.step(1000 + k, xh2[k], xh2[k + 1])
+            f1.record(stream)
+            f1.synchronize()
+            tt = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ttt["ms"] = float(tt.item())
+            ttt["bitwise_same_as_first_run"] = bool(torch.equal(xh2[tstar], xh[tstar]))
+            del x0
+        del xh
+    # ---- e2e: the public solve call with HOST (pinned) buffers, copies inside
+    e2e = None
+    if not args.no_e2e:
+        try:
+            T_e2e = (ttt or {}).get("iterations") or 30
+            A_h = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
+            A_h.copy_(A)
+            b_h = torch.empty(b.shape, dtype=torch.float64, pin_memory=True)
+            b_h.copy_(b)
+            ctx2 = P.Context(local)
+            if world > 1:
+                uid = [P.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(uid, src=0)
+                ctx2.set_comm(rank, world, uid[0])
+            xo_h = torch.empty(d, dtype=torch.float64, pin_memory=True)
+            P.ihs_solve_ols(P.Dense(A_h, row_offset=r0), b_h, spec, T_e2e, iter0=1000, ctx=ctx2, x_out=xo_h,
+                            x_hist=torch.empty((T_e2e + 1, d), dtype=torch.float64, device=dev))
+            barrier()
+            reps = 3
+            times = []
+            for _ in range(reps):
+                barrier()
+                t0 = time.perf_counter()
+                P.ihs_solve_ols(P.Dense(A_h, row_offset=r0), b_h, spec, T_e2e, iter0=1000, ctx=ctx2, x_out=xo_h,
+                                x_hist=torch.empty((T_e2e + 1, d), dtype=torch.float64, device=dev))
+                times.append(time.perf_counter() - t0)
+            te = torch.tensor([statistics.median(times)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            sec = float(te.item())
+            e2e = {"value": cfg.n * T_e2e / sec, "unit": UNIT, "h2d_bytes_per_step": 8 * n_loc * d + 8 * n_loc,
+                   "d2h_bytes_per_step": 8 * d, "ms_per_step": sec * 1e3,
+                   "step": f"one ihs_solve_ols call ({T_e2e} IHS iterations) on host-pinned A, b; x read back",
+                   "x_matches_device_run": bool(torch.equal(xo_h.to(dev), xh2[T_e2e])) if ttt and ttt.get("iterations")
+                   and T_e2e == ttt["iterations"] else None}
+            ctx2.close()
+            del A_h, b_h
+        except Exception as ex:  # report, do not hide
+            e2e = {"value": None, "unit": UNIT, "error": repr(ex)[:300]}
+    # ---- cpu baseline: the oracle, as it stands, rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        A_np = A.cpu().numpy()
+        b_np = b.cpu().numpy()
+        x = torch.zeros(d, dtype=torch.float64).numpy()
+        it = 0
+        t0 = time.perf_counter()
+        while True:
+            xh_o, _ = oracle.ihs_solve(A_np, b_np, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=it, x0=x)
+            x = xh_o[-1]
+            it += 1
+            el = time.perf_counter() - t0
+            if el >= args.cpu_seconds or it >= 50:
+                break
+        cpu = {"value": cfg.n * it / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"full {cfg.name} rows ({cfg.n}x{d}), {it} oracle IHS iterations, single thread, "
+                         f"{el:.1f} s", "host_cores_available": os.cpu_count()}
+        del A_np
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
+               "config": config_obj(cfg, world, {"per_gpu_rows": n_loc}),
+               "hbm_GBps_step": (8 * cfg.n * d / world) / (ms_step / 1e3) / 1e9,
+               "roofline": roof, "breakdown_ms": breakdown, "time_to_1e-10": ttt, "e2e": e2e,
+               "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
+               "gpu": torch.cuda.get_device_name(dev)}
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

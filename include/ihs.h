@@ -107,6 +107,26 @@ ihs_status ihs_ctx_synchronize(ihs_ctx ctx);
 /* Number of kernels this ctx has launched so far (bench evidence). */
 int64_t ihs_ctx_kernel_launches(ihs_ctx ctx);
 
+/* Per-kernel timing (bench evidence): when enabled, CUDA events are recorded on
+ * the ctx stream around every launch of the kernel groups below.
+ * ihs_ctx_profile synchronises and returns the summed elapsed ms and the
+ * number of timed launches of one group since the last reset. */
+typedef enum {
+    IHS_K_SORT = 0,        /* a1: hash + stable counting sort (hist, scan, scatter) */
+    IHS_K_SKETCH = 1,      /* a2 (+a5): bucket-ordered CountSketch gather, fused gradient */
+    IHS_K_SJLT = 2,        /* a2: dense SJLT smem-tile kernel + split reduction */
+    IHS_K_CSR = 3,         /* a2 + a5 on CSR */
+    IHS_K_GRAD = 4,        /* a5 standalone dense gradient */
+    IHS_K_REDUCE = 5,      /* fixed-order partial reductions */
+    IHS_K_GRAM = 6,        /* a4 DMMA Gram + reduction */
+    IHS_K_CHOL = 7,        /* a6 Cholesky update */
+    IHS_K_PG = 8,          /* a6 projected gradient */
+    IHS_K_COUNT = 9
+} ihs_kernel_group;
+ihs_status ihs_ctx_set_profiling(ihs_ctx ctx, int enable);
+ihs_status ihs_ctx_profile(ihs_ctx ctx, int group, double *total_ms, int64_t *launches);
+ihs_status ihs_ctx_profile_reset(ihs_ctx ctx);
+
 /* Multi-GPU (BASELINE.json north_star: one allreduce of [SA | g] per
  * iteration).  ihs_nccl_unique_id writes NCCL's 128-byte id (call on rank 0,
  * broadcast it); ihs_ctx_set_comm creates this rank's communicator.  NCCL is

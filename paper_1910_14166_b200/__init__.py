@@ -27,6 +27,8 @@ ABI_VERSION = 1
 OK, ERR_INVALID_ARGUMENT, ERR_DIMENSION_MISMATCH, ERR_NOT_SPD, ERR_NOT_CONVERGED, ERR_CUDA, ERR_COMM, \
     ERR_OUT_OF_MEMORY, ERR_UNSUPPORTED = range(9)
 COUNTSKETCH, SJLT = 0, 1
+K_SORT, K_SKETCH, K_SJLT, K_CSR, K_GRAD, K_REDUCE, K_GRAM, K_CHOL, K_PG = range(9)
+KERNEL_GROUPS = ("sort", "sketch", "sjlt", "csr", "grad", "reduce", "gram", "chol", "pg")
 DENSE, CSR = 0, 1
 
 
@@ -65,6 +67,9 @@ _EXPORTS = {
     "ihs_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ihs_ctx_synchronize": (C.c_int, [C.c_void_p]),
     "ihs_ctx_kernel_launches": (C.c_int64, [C.c_void_p]),
+    "ihs_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
+    "ihs_ctx_profile": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "ihs_ctx_profile_reset": (C.c_int, [C.c_void_p]),
     "ihs_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "ihs_ctx_set_comm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "ihs_allreduce_sum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
@@ -207,6 +212,18 @@ class Context:
     @property
     def kernel_launches(self) -> int:
         return int(lib().ihs_ctx_kernel_launches(self.h))
+
+    def set_profiling(self, enable: bool):
+        _check(lib().ihs_ctx_set_profiling(self.h, int(enable)), "ihs_ctx_set_profiling")
+
+    def profile(self, group: int):
+        """(summed ms, launches) of one kernel group since the last reset."""
+        ms, k = C.c_double(), C.c_int64()
+        _check(lib().ihs_ctx_profile(self._bind(), group, C.byref(ms), C.byref(k)), "ihs_ctx_profile")
+        return ms.value, k.value
+
+    def profile_reset(self):
+        _check(lib().ihs_ctx_profile_reset(self._bind()), "ihs_ctx_profile_reset")
 
     def set_comm(self, rank: int, world: int, unique_id: bytes | None):
         buf = None if unique_id is None else C.create_string_buffer(unique_id, 128)

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -69,6 +70,21 @@ struct ihs_ctx_s {
   nccl_comm comm = nullptr;
   int rank = 0, world = 1;
   ihs_status sticky = IHS_OK;
+  // profiling: (group, start, stop) per timed launch; events reused after reset
+  bool profiling = false;
+  bool gather_tma = true;  // IHS_GATHER=ldg selects the register-prefetch gather kernel
+  struct Rec { int group; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  size_t pool_used = 0;
+  cudaEvent_t ev() {
+    if (pool_used == pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      pool.push_back(e);
+    }
+    return pool[pool_used++];
+  }
 };
 
 namespace {
@@ -124,6 +140,24 @@ ihs_status scratch(ihs_ctx c, Slot s, size_t bytes, T **out) {
 
 LaunchCounter lc_of(ihs_ctx c) { return LaunchCounter{&c->launches}; }
 
+// RAII: events around one kernel-group launch when profiling is on.
+struct Prof {
+  ihs_ctx c;
+  int group;
+  cudaEvent_t b = nullptr;
+  Prof(ihs_ctx c_, int g) : c(c_), group(g) {
+    if (c->profiling) {
+      cudaEvent_t a = c->ev();
+      b = c->ev();
+      cudaEventRecord(a, c->stream);
+      c->recs.push_back({group, a, b});
+    }
+  }
+  ~Prof() {
+    if (b) cudaEventRecord(b, c->stream);
+  }
+};
+
 ihs_status check_spec(const ihs_sketch_spec *spec) {
   if (!spec) return IHS_ERR_INVALID_ARGUMENT;
   if (spec->m < 1 || spec->s < 1) return IHS_ERR_INVALID_ARGUMENT;
@@ -167,8 +201,11 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
   if (A->layout == IHS_CSR) {
     if (SA) IHS_CUDA(cudaMemsetAsync(SA, 0, (size_t)m * d * 8, st));
     if (g) IHS_CUDA(cudaMemsetAsync(g, 0, (size_t)d * 8, st));
-    IHS_CUDA(launch_csr_sketch_grad(n, d, A->row_ptr, A->col_idx, A->values, A->row_offset, key, m, s, SA, b, x, g, st,
-                                    lc_of(c)));
+    {
+      Prof pr(c, IHS_K_CSR);
+      IHS_CUDA(launch_csr_sketch_grad(n, d, A->row_ptr, A->col_idx, A->values, A->row_offset, key, m, s, SA, b, x, g,
+                                      st, lc_of(c)));
+    }
     if (SA && s > 1) IHS_CUDA(launch_scale(SA, m * d, spec_scale(spec), st, lc_of(c)));
     return IHS_OK;
   }
@@ -183,16 +220,30 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       IHS_TRY(scratch(c, S_HIST, p.hist_bytes(), &hist));
       IHS_TRY(scratch(c, S_TILES, p.tiles_bytes(), &tiles));
       IHS_TRY(scratch(c, S_PERM, p.perm_bytes(), &perm));
-      IHS_CUDA(launch_cs_sort(p, key, A->row_offset, hist, tiles, perm, st, lc_of(c)));
+      {
+        Prof pr(c, IHS_K_SORT);
+        IHS_CUDA(launch_cs_sort(p, key, A->row_offset, hist, tiles, perm, st, lc_of(c)));
+      }
       double *gpart = nullptr;
       if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)m * d * 8, &gpart));
-      IHS_CUDA(launch_cs_gather(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st, lc_of(c)));
-      if (fuse) IHS_CUDA(launch_reduce_rows(gpart, m, d, g, st, lc_of(c)));
+      {
+        Prof pr(c, IHS_K_SKETCH);
+        if (c->gather_tma && cs_gather_tma_supported(d, A->values))
+          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st,
+                                        lc_of(c)));
+        else
+          IHS_CUDA(launch_cs_gather(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st, lc_of(c)));
+      }
+      if (fuse) {
+        Prof pr(c, IHS_K_REDUCE);
+        IHS_CUDA(launch_reduce_rows(gpart, m, d, g, st, lc_of(c)));
+      }
     } else {
       SjltPlan p;
       if (!sjlt_plan(n, d, m, s, c->num_sms, p)) return IHS_ERR_UNSUPPORTED;
       double *part;
       IHS_TRY(scratch(c, S_SJLT, p.partial_bytes(), &part));
+      Prof pr(c, IHS_K_SJLT);
       IHS_CUDA(launch_sjlt_dense(p, A->values, key, A->row_offset, part, SA, spec_scale(spec), st, lc_of(c)));
     }
   }
@@ -204,7 +255,11 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
     if (n == 0) {
       IHS_CUDA(cudaMemsetAsync(g, 0, (size_t)d * 8, st));
     } else {
-      IHS_CUDA(launch_grad_dense(A->values, n, d, b, x, gpart, nb, st, lc_of(c)));
+      {
+        Prof pr(c, IHS_K_GRAD);
+        IHS_CUDA(launch_grad_dense(A->values, n, d, b, x, gpart, nb, st, lc_of(c)));
+      }
+      Prof pr(c, IHS_K_REDUCE);
       IHS_CUDA(launch_reduce_rows(gpart, nb, d, g, st, lc_of(c)));
     }
   }
@@ -215,6 +270,7 @@ ihs_status gram_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double s
   GramPlan p = gram_plan(m, d, c->num_sms);
   double *part;
   IHS_TRY(scratch(c, S_GRAM, p.partial_bytes(), &part));
+  Prof pr(c, IHS_K_GRAM);
   IHS_CUDA(launch_gram(p, SA, scale, part, H, c->stream, lc_of(c)));
   return IHS_OK;
 }
@@ -222,6 +278,7 @@ ihs_status gram_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double s
 ihs_status ols_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const double *x, double *xn) {
   double *sc;
   IHS_TRY(scratch(c, S_CHOL, chol_scratch_bytes(d), &sc));
+  Prof pr(c, IHS_K_CHOL);
   IHS_CUDA(launch_ols_update(H, g, d, x, xn, sc, c->d_status, c->num_sms, c->stream, lc_of(c)));
   return IHS_OK;
 }
@@ -241,6 +298,7 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
   if (k.max_inner < 1 || k.power_iters < 1 || !(k.inner_tol >= 0.0) || !(k.lip_safety > 0.0))
     return IHS_ERR_INVALID_ARGUMENT;
   if ((size_t)5 * d * 8 > 200 * 1024) return IHS_ERR_UNSUPPORTED;
+  Prof pr(c, IHS_K_PG);
   IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.inner_tol, k.lip_safety, xn, inner,
                                 nullptr, c->d_status, c->stream, lc_of(c)));
   return IHS_OK;
@@ -433,6 +491,7 @@ ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
     return IHS_ERR_OUT_OF_MEMORY;
   }
   cudaMemset(c->d_status, 0, sizeof(int));
+  if (const char *e = getenv("IHS_GATHER")) c->gather_tma = std::strcmp(e, "ldg") != 0;
   *out = c;
   return IHS_OK;
 }
@@ -445,6 +504,7 @@ ihs_status ihs_ctx_destroy(ihs_ctx c) {
     if (c->slot[s]) cudaFree(c->slot[s]);
   if (c->d_status) cudaFree(c->d_status);
   if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
+  for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   delete c;
   return IHS_OK;
 }
@@ -464,6 +524,39 @@ ihs_status ihs_ctx_synchronize(ihs_ctx c) {
 }
 
 int64_t ihs_ctx_kernel_launches(ihs_ctx c) { return c ? c->launches : -1; }
+
+ihs_status ihs_ctx_set_profiling(ihs_ctx c, int enable) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  c->profiling = enable != 0;
+  return IHS_OK;
+}
+
+ihs_status ihs_ctx_profile(ihs_ctx c, int group, double *total_ms, int64_t *launches) {
+  if (!c || group < 0 || group >= IHS_K_COUNT || !total_ms || !launches) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  IHS_CUDA(cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  int64_t k = 0;
+  for (auto &r : c->recs)
+    if (r.group == group) {
+      float ms = 0.f;
+      IHS_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+      tot += ms;
+      ++k;
+    }
+  *total_ms = tot;
+  *launches = k;
+  return IHS_OK;
+}
+
+ihs_status ihs_ctx_profile_reset(ihs_ctx c) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  IHS_CUDA(cudaStreamSynchronize(c->stream));
+  c->recs.clear();
+  c->pool_used = 0;
+  return IHS_OK;
+}
 
 ihs_status ihs_nccl_unique_id(void *out128) {
   if (!out128) return IHS_ERR_INVALID_ARGUMENT;

@@ -91,4 +91,16 @@ __device__ __forceinline__ void set_status(int *status, int code) {
   if (status) atomicCAS(status, 0, code);
 }
 
+// Opt a kernel into large dynamic shared memory once per call site and size
+// (raised only when a launch needs more): cudaFuncSetAttribute must not run on
+// every launch.
+#define IHS_SMEM_ATTR(func, bytes)                                                                   \
+  do {                                                                                               \
+    static size_t _ihs_attr_cur = 48 * 1024;                                                         \
+    if ((size_t)(bytes) > _ihs_attr_cur) {                                                           \
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(bytes));         \
+      _ihs_attr_cur = (size_t)(bytes);                                                               \
+    }                                                                                                \
+  } while (0)
+
 }  // namespace ihs

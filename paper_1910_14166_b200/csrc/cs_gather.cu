@@ -20,6 +20,70 @@ __device__ __forceinline__ int32_t scanned_at(const int32_t *hist, const int32_t
   return hist[e] + tile_sums[e / kScanTile];
 }
 
+// Rows of a bucket are consumed in batches of U.  Batch k+1's rows are loaded
+// while batch k is reduced (two register buffers), and the perm entries are
+// fetched two batches ahead, so each warp keeps 2*U rows in flight.  Loads are
+// never predicated: a predicated load followed by a zero-fill of the same
+// register serialises on the scoreboard.  Out-of-range columns read column
+// d-1 (and carry x = 0); out-of-range rows re-read the bucket's last row and
+// are skipped by the accumulations.
+template <int NV, int U, bool FUSE>
+struct GatherWarp {
+  const double *__restrict__ A;
+  const uint32_t *__restrict__ perm;
+  const double *__restrict__ bvec;
+  int64_t beg, len;
+  int d, lane;
+  int colc[NV];
+  double acc[NV], gacc[NV], xv[NV];
+
+  __device__ __forceinline__ uint32_t perm_at(int64_t k) const {
+    int64_t i = k * U + (lane & (U - 1));
+    return perm[beg + (i < len ? i : len - 1)];
+  }
+  __device__ __forceinline__ void load(double (&v)[U][NV], uint32_t pk) const {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t e = __shfl_sync(0xffffffffu, pk, u);
+      const double *rowp = A + (int64_t)(e & 0x7fffffffu) * d;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[u][k] = ldg_stream(rowp + colc[k]);
+    }
+  }
+  __device__ __forceinline__ void process(const double (&v)[U][NV], uint32_t pk, int64_t k) {
+    const int cnt = (int)min((int64_t)U, len - k * U);
+    if constexpr (FUSE) {
+      double p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        p[u] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) p[u] = fma(v[u][c], xv[c], p[u]);
+      }
+      transpose_reduce<U>(p, lane);
+      const int myu = reduced_row_of_lane<U>(lane);
+      const uint32_t me = __shfl_sync(0xffffffffu, pk, myu);
+      const double res = (myu < cnt) ? bvec[me & 0x7fffffffu] - p[0] : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double ru = __shfl_sync(0xffffffffu, res, owner_lane_of_row<U>(u));
+#pragma unroll
+        for (int c = 0; c < NV; ++c) gacc[c] = fma(ru, v[u][c], gacc[c]);
+      }
+    }
+    // ascending rows of the bucket: the oracle's summation order
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t e = __shfl_sync(0xffffffffu, pk, u);
+      if (u < cnt) {
+        const bool neg = (e >> 31) != 0;
+#pragma unroll
+        for (int c = 0; c < NV; ++c) acc[c] += neg ? -v[u][c] : v[u][c];
+      }
+    }
+  }
+};
+
 template <int NV, int U, bool FUSE>
 __global__ void __launch_bounds__(64) cs_gather_kernel(const double *__restrict__ A, int64_t n, int d, int m,
                                                        int nslices, const int32_t *__restrict__ hist,
@@ -36,68 +100,45 @@ __global__ void __launch_bounds__(64) cs_gather_kernel(const double *__restrict_
   const int64_t beg = scanned_at(hist, tile_sums, (int64_t)b * nchunks);
   const int64_t end = (b + 1 < m) ? scanned_at(hist, tile_sums, (int64_t)(b + 1) * nchunks) : n;
 
+  GatherWarp<NV, U, FUSE> w;
+  w.A = A;
+  w.perm = perm;
+  w.bvec = bvec;
+  w.beg = beg;
+  w.len = end - beg;
+  w.d = d;
+  w.lane = lane;
   int col[NV];
-  bool cval[NV];
-  double acc[NV], gacc[NV], xv[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     col[k] = slice * 32 * NV + lane + 32 * k;
-    cval[k] = col[k] < d;
-    acc[k] = 0.0;
-    gacc[k] = 0.0;
-    xv[k] = (FUSE && cval[k]) ? x[col[k]] : 0.0;
+    w.colc[k] = col[k] < d ? col[k] : d - 1;
+    w.acc[k] = 0.0;
+    w.gacc[k] = 0.0;
+    w.xv[k] = (FUSE && col[k] < d) ? x[col[k]] : 0.0;
   }
-
-  for (int64_t base = beg; base < end; base += 32) {
-    const uint32_t pe = (base + lane < end) ? perm[base + lane] : 0u;
-    const int cnt = (int)((end - base) < 32 ? (end - base) : 32);
+  const int64_t nb = (w.len + U - 1) / U;
+  if (nb > 0) {
+    double va[U][NV], vb[U][NV];
+    uint32_t p0 = w.perm_at(0), p1 = w.perm_at(1 < nb ? 1 : 0);
+    w.load(va, p0);
 #pragma unroll 1
-    for (int u0 = 0; u0 < cnt; u0 += U) {
-      double v[U][NV];
-      uint32_t e[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        e[u] = __shfl_sync(0xffffffffu, pe, u0 + u);
-        const double *rowp = A + (int64_t)(e[u] & 0x7fffffffu) * d;
-        const bool rv = (u0 + u) < cnt;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) v[u][k] = (rv && cval[k]) ? ldg_stream(rowp + col[k]) : 0.0;
-      }
-      if constexpr (FUSE) {
-        double p[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          p[u] = 0.0;
-#pragma unroll
-          for (int k = 0; k < NV; ++k) p[u] = fma(v[u][k], xv[k], p[u]);
-        }
-        transpose_reduce<U>(p, lane);
-        const int myu = reduced_row_of_lane<U>(lane);
-        const uint32_t me = __shfl_sync(0xffffffffu, pe, u0 + myu);
-        const double res = (u0 + myu < cnt) ? bvec[me & 0x7fffffffu] - p[0] : 0.0;
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const double ru = __shfl_sync(0xffffffffu, res, owner_lane_of_row<U>(u));
-#pragma unroll
-          for (int k = 0; k < NV; ++k) gacc[k] = fma(ru, v[u][k], gacc[k]);
-        }
-      }
-      // ascending rows of the bucket: the oracle's summation order
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if (u0 + u < cnt) {
-          const bool neg = (e[u] >> 31) != 0;
-#pragma unroll
-          for (int k = 0; k < NV; ++k) acc[k] += neg ? -v[u][k] : v[u][k];
-        }
-      }
+    for (int64_t k = 0; k < nb; k += 2) {
+      const uint32_t p2 = w.perm_at(k + 2 < nb ? k + 2 : nb - 1);
+      if (k + 1 < nb) w.load(vb, p1);
+      w.process(va, p0, k);
+      const uint32_t p3 = w.perm_at(k + 3 < nb ? k + 3 : nb - 1);
+      if (k + 2 < nb) w.load(va, p2);
+      if (k + 1 < nb) w.process(vb, p1, k + 1);
+      p0 = p2;
+      p1 = p3;
     }
   }
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    if (cval[k]) {
-      SA[(int64_t)b * d + col[k]] = acc[k];
-      if constexpr (FUSE) gpart[(int64_t)b * d + col[k]] = gacc[k];
+    if (col[k] < d) {
+      SA[(int64_t)b * d + col[k]] = w.acc[k];
+      if constexpr (FUSE) gpart[(int64_t)b * d + col[k]] = w.gacc[k];
     }
   }
 }

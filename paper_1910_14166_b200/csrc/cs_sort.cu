@@ -216,13 +216,12 @@ cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset
                            int32_t *tile_sums, uint32_t *perm, cudaStream_t st, LaunchCounter lc) {
   const uint32_t m = (uint32_t)p.m;
   size_t hsmem = 4 * (size_t)m;
-  if (hsmem > 48 * 1024) cudaFuncSetAttribute(cs_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem);
+  IHS_SMEM_ATTR(cs_hist_kernel, hsmem);
   cs_hist_kernel<<<(unsigned)p.nchunks, kHistThreads, hsmem, st>>>(p.n, p.chunk, p.nchunks, m, key, row_offset, hist);
   scan_tiles_kernel<<<(unsigned)p.ntiles, 1024, 0, st>>>(hist, p.entries, tile_sums);
   scan_sums_kernel<<<1, 1024, 0, st>>>(tile_sums, p.ntiles);
   size_t ssmem = (4 + 2 * kScatterWarps) * (size_t)m;
-  if (ssmem > 48 * 1024)
-    cudaFuncSetAttribute(cs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem);
+  IHS_SMEM_ATTR(cs_scatter_kernel, ssmem);
   if (p.n > 0)
     cs_scatter_kernel<<<(unsigned)p.nchunks, kScatterWarps * 32, ssmem, st>>>(p.n, p.chunk, p.nchunks, m, key,
                                                                               row_offset, hist, tile_sums, perm);

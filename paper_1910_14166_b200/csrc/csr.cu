@@ -63,9 +63,7 @@ void launch_t(int grid, int64_t n, int d, const int64_t *row_ptr, const int32_t 
               double *g, cudaStream_t st) {
   const size_t smem = (size_t)d * 8;
   if (GRAD && smem <= 96 * 1024) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(csr_sketch_grad_kernel<SKETCH, GRAD, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+    IHS_SMEM_ATTR((csr_sketch_grad_kernel<SKETCH, GRAD, true>), smem);
     csr_sketch_grad_kernel<SKETCH, GRAD, true><<<grid, 256, smem, st>>>(n, d, row_ptr, col, val, row_offset, key, M,
                                                                        s, SA, bvec, x, g);
   } else {

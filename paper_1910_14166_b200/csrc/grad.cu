@@ -22,13 +22,16 @@ __global__ void __launch_bounds__(kWarps * 32) grad_dense_kernel(const double *_
   const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
   const int64_t r0 = min(n, gw * rows_per_warp);
   const int64_t r1 = min(n, r0 + rows_per_warp);
-  int col[NV];
+  // unpredicated loads from clamped addresses (see cs_gather.cu); clamped
+  // columns carry x = 0 and clamped rows carry r = 0.
+  int col[NV], colc[NV];
   bool cval[NV];
   double xv[NV], gacc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     col[k] = lane + 32 * k;
     cval[k] = col[k] < d;
+    colc[k] = cval[k] ? col[k] : d - 1;
     xv[k] = cval[k] ? x[col[k]] : 0.0;
     gacc[k] = 0.0;
   }
@@ -37,10 +40,10 @@ __global__ void __launch_bounds__(kWarps * 32) grad_dense_kernel(const double *_
     double v[U][NV];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const bool rv = base + u < r1;
-      const double *rowp = A + (base + u) * d;
+      const int64_t row = (base + u < r1) ? base + u : r1 - 1;
+      const double *rowp = A + row * d;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) v[u][k] = (rv && cval[k]) ? ldg_stream(rowp + col[k]) : 0.0;
+      for (int k = 0; k < NV; ++k) v[u][k] = ldg_stream(rowp + colc[k]);
     }
     double p[U];
 #pragma unroll
@@ -82,13 +85,12 @@ __global__ void __launch_bounds__(kWarps * 32) sqnorm_dense_kernel(const double 
   const int64_t r0 = min(n, gw * rows_per_warp);
   const int64_t r1 = min(n, r0 + rows_per_warp);
   double xv[NV];
-  int col[NV];
-  bool cval[NV];
+  int colc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
-    col[k] = lane + 32 * k;
-    cval[k] = col[k] < d;
-    xv[k] = cval[k] ? vvec[col[k]] : 0.0;
+    const int c = lane + 32 * k;
+    colc[k] = c < d ? c : d - 1;
+    xv[k] = c < d ? vvec[c] : 0.0;
   }
   double acc = 0.0;
   const int myu = reduced_row_of_lane<U>(lane);
@@ -98,11 +100,11 @@ __global__ void __launch_bounds__(kWarps * 32) sqnorm_dense_kernel(const double 
     double p[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const bool rv = base + u < r1;
-      const double *rowp = A + (base + u) * d;
+      const int64_t row = (base + u < r1) ? base + u : r1 - 1;
+      const double *rowp = A + row * d;
       p[u] = 0.0;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) p[u] = fma((rv && cval[k]) ? ldg_stream(rowp + col[k]) : 0.0, xv[k], p[u]);
+      for (int k = 0; k < NV; ++k) p[u] = fma(ldg_stream(rowp + colc[k]), xv[k], p[u]);
     }
     transpose_reduce<U>(p, lane);
     if (owner && base + myu < r1) acc = fma(p[0], p[0], acc);
@@ -173,8 +175,7 @@ void launch_grad_t(const double *A, int64_t n, int d, const double *bvec, const 
   int64_t rpw = (n + warps - 1) / warps;
   rpw = (rpw + U - 1) / U * U;
   size_t smem = (size_t)kWarps * d * 8;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(grad_dense_kernel<NV, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  IHS_SMEM_ATTR((grad_dense_kernel<NV, U>), smem);
   grad_dense_kernel<NV, U><<<(unsigned)nblocks, kWarps * 32, smem, st>>>(A, n, d, bvec, x, gpart, rpw);
 }
 

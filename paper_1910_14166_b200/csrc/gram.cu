@@ -153,7 +153,7 @@ GramPlan gram_plan(int64_t m, int64_t d, int num_sms) {
 cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
                         cudaStream_t st, LaunchCounter lc) {
   const size_t smem = (size_t)4 * KC * LDS * 8;
-  cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  IHS_SMEM_ATTR(gram_kernel, smem);
   dim3 grid(p.ntri, p.nsplit);
   gram_kernel<<<grid, 128, smem, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kchunk, partials);
   gram_reduce_kernel<<<p.ntri, 256, 0, st>>>(partials, (int)p.d, p.tiles, p.ntri, p.nsplit, scale * scale, H);

@@ -155,8 +155,7 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
   (void)scratch;
   const size_t smem = (size_t)5 * d * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(pg_l1ball_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  IHS_SMEM_ATTR(pg_l1ball_kernel, smem);
   pg_l1ball_kernel<<<1, kThreads, smem, st>>>(H, g, (int)d, x, radius, max_inner, power_iters, tol, safety, x_next,
                                               inner_iters, status);
   lc.add();

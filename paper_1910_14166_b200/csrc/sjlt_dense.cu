@@ -84,7 +84,7 @@ void launch_dc(const SjltPlan &p, const double *A, uint64_t key, int64_t row_off
                cudaStream_t st) {
   const int threads = 32 * std::min(p.s, 16);
   const int64_t rps = (p.n + p.nsplit - 1) / p.nsplit;
-  cudaFuncSetAttribute(sjlt_dense_kernel<DC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+  IHS_SMEM_ATTR(sjlt_dense_kernel<DC>, p.smem);
   dim3 grid(p.nslices, p.nsplit);
   sjlt_dense_kernel<DC><<<grid, threads, p.smem, st>>>(A, p.n, (int)p.d, (int)p.m, p.s, key, row_offset,
                                                        std::max<int64_t>(rps, 1), partials);
