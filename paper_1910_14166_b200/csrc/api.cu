@@ -72,7 +72,7 @@ struct ihs_ctx_s {
   ihs_status sticky = IHS_OK;
   // profiling: (group, start, stop) per timed launch; events reused after reset
   bool profiling = false;
-  bool gather_tma = true;  // IHS_GATHER=ldg selects the register-prefetch gather kernel
+  int gather = 1;  // CountSketch gather: 0 = register-staged LDG, 1 = TMA bulk, 2 = cp.async ring (IHS_GATHER)
   struct Rec { int group; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
@@ -228,9 +228,12 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)m * d * 8, &gpart));
       {
         Prof pr(c, IHS_K_SKETCH);
-        if (c->gather_tma && cs_gather_tma_supported(d, A->values))
+        if (c->gather == 1 && cs_gather_tma_supported(d, A->values))
           IHS_CUDA(launch_cs_gather_tma(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st,
                                         lc_of(c)));
+        else if (c->gather == 2 && cs_gather_async_supported(d, A->values))
+          IHS_CUDA(launch_cs_gather_async(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st,
+                                          lc_of(c)));
         else
           IHS_CUDA(launch_cs_gather(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st, lc_of(c)));
       }
@@ -491,7 +494,8 @@ ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
     return IHS_ERR_OUT_OF_MEMORY;
   }
   cudaMemset(c->d_status, 0, sizeof(int));
-  if (const char *e = getenv("IHS_GATHER")) c->gather_tma = std::strcmp(e, "ldg") != 0;
+  if (const char *e = getenv("IHS_GATHER"))
+    c->gather = !std::strcmp(e, "ldg") ? 0 : !std::strcmp(e, "async") ? 2 : 1;
   *out = c;
   return IHS_OK;
 }

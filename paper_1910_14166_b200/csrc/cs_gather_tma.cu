@@ -17,8 +17,8 @@ namespace ihs {
 
 namespace {
 constexpr int kScanTile = 4096;
-constexpr int kStages = 3;
-constexpr int kRows = 8;  // rows per stage
+constexpr int kStages = 6;
+constexpr int kRows = 4;  // rows per stage
 
 __device__ __forceinline__ int32_t scanned_at(const int32_t *hist, const int32_t *tile_sums, int64_t e) {
   return hist[e] + tile_sums[e / kScanTile];
@@ -52,12 +52,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// Warps 0-3 consume (one column per thread, two for d > 128); warp 4 produces:
-// it prefetches the perm entries of the next stage, waits until the stage's
-// slot is released (empty barrier, one arrival per consumer warp) and issues
-// one bulk copy per row, completing on the slot's full barrier.
-constexpr int kConsumers = 128;
-template <bool FUSE>
+// Warps 0-1 consume: thread t owns columns t + 64 q (q < NC) of the bucket's
+// SA row and gradient partial; it reads the stage's rows from shared memory in
+// ring order, so every column is a left-to-right sum.  With the gradient fused,
+// each warp transpose-reduces its partial dot products of the stage's 8 rows,
+// the two warp partials meet in shared memory behind a named barrier, and every
+// thread forms the same residual r_i = b_i - (p0 + p1).  Warp 2 produces: it
+// prefetches the next stage's perm entries and b values, waits until the slot
+// is released (one arrival per consumer warp) and issues one bulk copy per row.
+constexpr int kConsumers = 64;
+constexpr int kCW = kConsumers / 32;
+template <bool FUSE, int NC>
 __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
     const double *__restrict__ A, int64_t n, int d, int m, const int32_t *__restrict__ hist,
     const int32_t *__restrict__ tile_sums, int64_t nchunks, const uint32_t *__restrict__ perm,
@@ -65,10 +70,11 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
     double *__restrict__ gpart) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *ring = reinterpret_cast<double *>(smem_raw);                                // [kStages][kRows][d]
-  uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)kStages * kRows * d);  // [kStages]
+  double *bs = ring + (size_t)kStages * kRows * d;                                    // [kStages][kRows]
+  double *pd = bs + kStages * kRows;                                                  // [kStages][kCW][kRows]
+  uint64_t *full = reinterpret_cast<uint64_t *>(pd + kStages * kCW * kRows);          // [kStages]
   uint64_t *empty = full + kStages;                                                   // [kStages]
   uint32_t *rid = reinterpret_cast<uint32_t *>(empty + kStages);                      // [kStages][kRows]
-  double *res = reinterpret_cast<double *>(rid + kStages * kRows);                    // [kStages][kRows]
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t beg = scanned_at(hist, tile_sums, (int64_t)b * nchunks);
@@ -80,25 +86,31 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers / 32);
+      mbar_init(&empty[s], kCW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kConsumers / 32) {
+  if (warp == kCW) {
     // ---------------- producer warp
     auto perm_of = [&](int64_t k) -> uint32_t {
       const int64_t i = k * kRows + lane;
       return (lane < kRows && k < nb && i < len) ? perm[beg + i] : 0u;
     };
     uint32_t e = perm_of(0);
+    double bv = (FUSE && lane < kRows && 0 < nb) ? bvec[e & 0x7fffffffu] : 0.0;
     for (int64_t k = 0; k < nb; ++k) {
       const int s = (int)(k % kStages);
       const int cnt = (int)min((int64_t)kRows, len - k * kRows);
       const uint32_t enext = perm_of(k + 1);  // in flight while we wait for the slot
+      double bnext = 0.0;
+      if (FUSE && lane < kRows && k + 1 < nb) bnext = bvec[enext & 0x7fffffffu];
       if (k >= kStages) mbar_wait(&empty[s], (uint32_t)(((k / kStages) - 1) & 1));
-      if (lane < cnt) rid[s * kRows + lane] = e;
+      if (lane < cnt) {
+        rid[s * kRows + lane] = e;
+        if (FUSE) bs[s * kRows + lane] = bv;
+      }
       __syncwarp();
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -108,61 +120,87 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
       if (lane < cnt)
         bulk_g2s(ring + ((size_t)s * kRows + lane) * d, A + (int64_t)(e & 0x7fffffffu) * d, row_bytes, &full[s]);
       e = enext;
+      bv = bnext;
     }
     return;
   }
   // ---------------- consumer warps
-  const int c0 = tid, c1 = tid + kConsumers;
-  const bool v0 = c0 < d, v1 = c1 < d;
-  double acc0 = 0.0, acc1 = 0.0, g0 = 0.0, g1 = 0.0;
-  double xv[8];
-  if constexpr (FUSE) {
+  int cc[NC];
+  bool cv[NC];
+  double acc[NC], gac[NC], xv[NC];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) xv[q] = (lane + 32 * q < d) ? x[lane + 32 * q] : 0.0;
+  for (int q = 0; q < NC; ++q) {
+    const int c = tid + kConsumers * q;
+    cv[q] = c < d;
+    cc[q] = cv[q] ? c : d - 1;
+    acc[q] = 0.0;
+    gac[q] = 0.0;
+    xv[q] = (FUSE && cv[q]) ? x[c] : 0.0;
   }
+  const int myu = reduced_row_of_lane<kRows>(lane);
+  const bool owner = owner_lane_of_row<kRows>(myu) == lane;
   for (int64_t k = 0; k < nb; ++k) {
     const int s = (int)(k % kStages);
     const int cnt = (int)min((int64_t)kRows, len - k * kRows);
     mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
     const double *st = ring + (size_t)s * kRows * d;
-    if constexpr (FUSE) {
-      for (int r = warp; r < cnt; r += kConsumers / 32) {
-        const double *row = st + (size_t)r * d;
-        double p = 0.0;
+    double a[kRows][NC];
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (lane + 32 * q < d) p = fma(row[lane + 32 * q], xv[q], p);
-        p = warp_sum(p);
-        if (lane == 0) res[s * kRows + r] = bvec[rid[s * kRows + r] & 0x7fffffffu] - p;
-      }
-      asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+    for (int r = 0; r < kRows; ++r) {
+      const int rr = r < cnt ? r : 0;  // rows past the end were not copied: read row 0
+#pragma unroll
+      for (int q = 0; q < NC; ++q) a[r][q] = st[(size_t)rr * d + cc[q]];
     }
-#pragma unroll 4
-    for (int r = 0; r < cnt; ++r) {
-      const double *row = st + (size_t)r * d;
-      const bool neg = (rid[s * kRows + r] >> 31) != 0;
-      if (v0) {
-        const double a = row[c0];
-        acc0 += neg ? -a : a;
-        if constexpr (FUSE) g0 = fma(res[s * kRows + r], a, g0);
+    double res[kRows];
+    if constexpr (FUSE) {
+      double p[kRows];
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        p[r] = a[r][0] * xv[0];
+#pragma unroll
+        for (int q = 1; q < NC; ++q) p[r] = fma(a[r][q], xv[q], p[r]);
       }
-      if (v1) {
-        const double a = row[c1];
-        acc1 += neg ? -a : a;
-        if constexpr (FUSE) g1 = fma(res[s * kRows + r], a, g1);
+      transpose_reduce<kRows>(p, lane);
+      if (owner) pd[(s * kCW + warp) * kRows + myu] = p[0];
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+#pragma unroll
+      for (int r = 0; r < kRows; ++r) {
+        double dot = pd[(s * kCW + 0) * kRows + r];
+#pragma unroll
+        for (int w = 1; w < kCW; ++w) dot += pd[(s * kCW + w) * kRows + r];
+        res[r] = (r < cnt) ? bs[s * kRows + r] - dot : 0.0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) {
+      if (r < cnt) {
+        const bool neg = (rid[s * kRows + r] >> 31) != 0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) {
+          acc[q] += neg ? -a[r][q] : a[r][q];
+          if constexpr (FUSE) gac[q] = fma(res[r], a[r][q], gac[q]);
+        }
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
-  if (v0) {
-    SA[(int64_t)b * d + c0] = acc0;
-    if constexpr (FUSE) gpart[(int64_t)b * d + c0] = g0;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    if (cv[q]) {
+      SA[(int64_t)b * d + tid + kConsumers * q] = acc[q];
+      if constexpr (FUSE) gpart[(int64_t)b * d + tid + kConsumers * q] = gac[q];
+    }
   }
-  if (v1) {
-    SA[(int64_t)b * d + c1] = acc1;
-    if constexpr (FUSE) gpart[(int64_t)b * d + c1] = g1;
-  }
+}
+
+template <bool FUSE, int NC>
+void launch_tma_t(size_t smem, const double *A, int64_t n, int d, int m, const int32_t *hist, const int32_t *tile_sums,
+                  int64_t nchunks, const uint32_t *perm, const double *bvec, const double *x, double *SA,
+                  double *gpart, cudaStream_t st) {
+  IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC>), smem);
+  cs_gather_tma_kernel<FUSE, NC><<<(unsigned)m, kConsumers + 32, smem, st>>>(A, n, d, m, hist, tile_sums, nchunks,
+                                                                              perm, bvec, x, SA, gpart);
 }
 }  // namespace
 
@@ -173,16 +211,18 @@ bool cs_gather_tma_supported(int64_t d, const void *A) {
 cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
                                  const double *x, double *SA, double *gpart, cudaStream_t st, LaunchCounter lc) {
-  const size_t smem = (size_t)kStages * kRows * d * 8 + 2 * kStages * 8 + kStages * kRows * 4 + kStages * kRows * 8 + 64;
-  if (gpart) {
-    IHS_SMEM_ATTR(cs_gather_tma_kernel<true>, smem);
-    cs_gather_tma_kernel<true><<<(unsigned)m, kConsumers + 32, smem, st>>>(A, n, (int)d, (int)m, hist, tile_sums, nchunks,
-                                                                    perm, bvec, x, SA, gpart);
-  } else {
-    IHS_SMEM_ATTR(cs_gather_tma_kernel<false>, smem);
-    cs_gather_tma_kernel<false><<<(unsigned)m, kConsumers + 32, smem, st>>>(A, n, (int)d, (int)m, hist, tile_sums, nchunks,
-                                                                     perm, nullptr, nullptr, SA, nullptr);
-  }
+  const size_t smem = (size_t)kStages * kRows * d * 8 + (size_t)kStages * kRows * 8 * (1 + kCW) + 2 * kStages * 8 +
+                      kStages * kRows * 4 + 64;
+  const int nc = (int)((d + kConsumers - 1) / kConsumers);
+  const bool f = gpart != nullptr;
+#define IHS_TMA(NC)                                                                                           \
+  (f ? launch_tma_t<true, NC>(smem, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st) \
+     : launch_tma_t<false, NC>(smem, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, nullptr, nullptr, SA,   \
+                               nullptr, st))
+  if (nc <= 1) IHS_TMA(1);
+  else if (nc == 2) IHS_TMA(2);
+  else IHS_TMA(4);
+#undef IHS_TMA
   lc.add();
   return cudaGetLastError();
 }

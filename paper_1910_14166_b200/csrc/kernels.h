@@ -40,6 +40,13 @@ cudaError_t launch_cs_gather(const double *A, int64_t n, int64_t d, int64_t m, c
                              const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
                              const double *x, double *SA, double *gpart, cudaStream_t st, LaunchCounter lc);
 
+// cp.async-fed variant (per-warp shared-memory ring).  Requires even d <= 256
+// and a 16-byte aligned A.
+bool cs_gather_async_supported(int64_t d, const void *A);
+cudaError_t launch_cs_gather_async(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
+                                   const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm,
+                                   const double *bvec, const double *x, double *SA, double *gpart, cudaStream_t st,
+                                   LaunchCounter lc);
 // TMA-fed variant: one CTA per bucket, bulk copies of whole rows into a smem
 // ring.  Requires even d <= 256 and a 16-byte aligned A.
 bool cs_gather_tma_supported(int64_t d, const void *A);

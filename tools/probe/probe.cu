@@ -73,6 +73,14 @@ int main(){
   cudaMemcpy(dp,perm.data(),n*4,cudaMemcpyHostToDevice); cudaMemcpy(doff,off.data(),(m+1)*4,cudaMemcpyHostToDevice);
   #define G(U) for(int r=0;r<3;r++){cudaEventRecord(e0); gather_rows<U,4><<<m*32/64,64>>>(A,dp,doff,m,d,out); cudaEventRecord(e1); cudaEventSynchronize(e1);} cudaEventElapsedTime(&ms,e0,e1); printf("gather U=%d warp/bucket: %.3f ms %.1f GB/s\n", U, ms, (double)n*d*8/ms/1e6);
   G(4) G(8) G(16)
+  // contiguous: bucket b = rows [b*n/m, (b+1)*n/m)
+  { std::vector<int> id(n), of2(m+1); for (int i=0;i<n;i++) id[i]=i; for (int b=0;b<=m;b++) of2[b]=(int)((long)b*n/m);
+    cudaMemcpy(dp,id.data(),n*4,cudaMemcpyHostToDevice); cudaMemcpy(doff,of2.data(),(m+1)*4,cudaMemcpyHostToDevice); }
+  printf("contiguous:\n"); G(8) G(16)
+  // interleaved: bucket b = rows b, b+m, b+2m, ... (the band pattern of sorted buckets, perfectly in sync)
+  { std::vector<int> id(n), of2(m+1); int k=0; for (int b=0;b<m;b++){ of2[b]=k; for (int i=b;i<n;i+=m) id[k++]=i; } of2[m]=n;
+    cudaMemcpy(dp,id.data(),n*4,cudaMemcpyHostToDevice); cudaMemcpy(doff,of2.data(),(m+1)*4,cudaMemcpyHostToDevice); }
+  printf("strided b+k*m:\n"); G(8) G(16)
   CK(cudaGetLastError());
   // dmma
   for (int r=0;r<2;r++){ cudaEventRecord(e0); dmma_loop<<<148*4,256>>>(out, 4096); cudaEventRecord(e1); cudaEventSynchronize(e1);} cudaEventElapsedTime(&ms,e0,e1);
