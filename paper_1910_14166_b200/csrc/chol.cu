@@ -1,9 +1,8 @@
 // a6, OLS: x^{t+1} = x^t + H^{-1} g (Eq. (2) with C = R^d, PAPER.md:83-86;
-// T_solve = O(d^3)).  Right-looking Cholesky H = L L^T in
-// one CTA (H in shared memory when d^2 * 8 fits, else in an L2-resident global
-// scratch), then forward / back substitution by one warp and the update
-// x + u.  A pivot <= 0 sets IHS_ERR_NOT_SPD (reading R13) and x_next = x.
-// Latency-bound: d = 10..256 take O(d) barrier steps.
+// T_solve = O(d^3)).  d <= 160: blocked Cholesky H = L L^T
+// in one CTA with H in shared memory (this file); d > 160: multi-CTA panel
+// factorisation (chol_large.cu).  A pivot <= 0 sets IHS_ERR_NOT_SPD (reading
+// R13) and x_next = x.  Latency-bound: O(d) dependent column steps.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -12,213 +11,6 @@
 namespace ihs {
 
 namespace {
-constexpr int kThreads = 512;
-constexpr size_t kSmemLimit = 200 * 1024;
-
-// Right-looking elimination with ONE barrier per column: step j subtracts
-// a_ij a_cj / a_jj from the trailing lower triangle (j < c <= i) while column
-// j itself stays unscaled; a final pass turns the stored (a_ij, a_jj) into
-// L_ij = a_ij / sqrt(a_jj).  The row stride is d + 1 so the column reads
-// a_cj of a warp spread over the banks.
-__global__ void __launch_bounds__(kThreads) chol_solve_kernel(const double *__restrict__ H,
-                                                              const double *__restrict__ g, int d,
-                                                              const double *__restrict__ x, double *x_next,
-                                                              double *scratch, int *status, int use_smem) {
-  extern __shared__ double sm[];
-  const int lda = d + 1;
-  double *a = use_smem ? sm : scratch;                                 // d x lda, lower triangle used
-  double *z = use_smem ? sm + (size_t)d * lda : scratch + (size_t)d * lda;  // d
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;          // 32 x 16 thread grid
-  constexpr int kRows = kThreads / 32;
-  for (int i = ty; i < d; i += kRows)
-    for (int c = tx; c <= i; c += 32) a[(int64_t)i * lda + c] = H[(int64_t)i * d + c];
-  for (int i = tid; i < d; i += kThreads) z[i] = g[i];
-  __syncthreads();
-  bool bad = false;
-  for (int j = 0; j < d; ++j) {
-    const double piv = a[(int64_t)j * lda + j];
-    if (!(piv > 0.0)) {  // every thread reads the same pivot: uniform exit
-      bad = true;
-      break;
-    }
-    const double rinv = 1.0 / piv;
-    for (int i = j + 1 + ty; i < d; i += kRows) {
-      const double aij = a[(int64_t)i * lda + j] * rinv;
-      double *ai = a + (int64_t)i * lda;
-      for (int c = j + 1 + tx; c <= i; c += 32) ai[c] -= aij * a[(int64_t)c * lda + j];
-    }
-    __syncthreads();
-  }
-  if (bad) {
-    for (int i = tid; i < d; i += kThreads) x_next[i] = x[i];
-    if (tid == 0) set_status(status, 3 /* IHS_ERR_NOT_SPD */);
-    return;
-  }
-  // L_ij = a_ij / sqrt(a_jj), L_jj = sqrt(a_jj)
-  for (int i = ty; i < d; i += kRows)
-    for (int c = tx; c < i; c += 32) a[(int64_t)i * lda + c] /= sqrt(a[(int64_t)c * lda + c]);
-  __syncthreads();
-  for (int i = tid; i < d; i += kThreads) a[(int64_t)i * lda + i] = sqrt(a[(int64_t)i * lda + i]);
-  __syncthreads();
-  if (tid < 32) {
-    const int lane = tid;
-    // forward: L y = g (column-oriented; row i subtracts terms j = 0..i-1 in order)
-    for (int j = 0; j < d; ++j) {
-      __syncwarp();
-      const double yj = z[j] / a[(int64_t)j * lda + j];
-      __syncwarp();
-      if (lane == 0) z[j] = yj;
-      for (int i = j + 1 + lane; i < d; i += 32) z[i] -= a[(int64_t)i * lda + j] * yj;
-    }
-    // backward: L^T u = y
-    for (int i = d - 1; i >= 0; --i) {
-      __syncwarp();
-      const double ui = z[i] / a[(int64_t)i * lda + i];
-      __syncwarp();
-      if (lane == 0) z[i] = ui;
-      for (int k = lane; k < i; k += 32) z[k] -= a[(int64_t)i * lda + k] * ui;
-    }
-    __syncwarp();
-    for (int i = lane; i < d; i += 32) x_next[i] = x[i] + z[i];
-  }
-}
-
-// d <= 32*S (and <= 16*R): thread (ty, tx) of a 16 x 32 grid keeps the lower-
-// triangle elements (ty + 16r, tx + 32s) in REGISTERS for the whole
-// factorisation.  Step j: the owners of column j publish it through a
-// double-buffered shared vector (one barrier per column); every thread then
-// applies a_ic -= a_ij a_cj / a_jj to its elements with c > j.  The unscaled
-// columns are also kept in shared memory; a final pass scales them to
-// L_ij = a_ij / sqrt(a_jj).  The two triangular solves run in warp 0 with the
-// right-hand side in registers and one shuffle per step.
-template <int R, int S>
-__global__ void __launch_bounds__(kThreads) chol_reg_kernel(const double *__restrict__ H,
-                                                            const double *__restrict__ g, int d,
-                                                            const double *__restrict__ x, double *x_next,
-                                                            int *status) {
-  static_assert(16 * R >= 32 * S || true, "");
-  extern __shared__ double sm[];
-  const int lda = d + 1;
-  double *L = sm;                          // d x lda: unscaled columns, then L
-  double *colbuf = sm + (size_t)d * lda;   // 2 x (32 S)
-  double *rdiag = colbuf + 2 * 32 * S;     // 32 S: 1 / L_jj
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  double a[R][S];
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int i = ty + 16 * r, c = tx + 32 * s;
-      a[r][s] = (i < d && c <= i) ? H[(int64_t)i * d + c] : 0.0;
-    }
-  bool bad = false;
-  for (int j = 0; j < d; ++j) {
-    const int js = j >> 5, jt = j & 31;
-    double *cb = colbuf + (j & 1) * 32 * S;
-    if (tx == jt) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = ty + 16 * r;
-        if (i >= j && i < d) {
-          double v = 0.0;
-#pragma unroll
-          for (int s = 0; s < S; ++s)
-            if (s == js) v = a[r][s];
-          cb[i] = v;
-          L[(int64_t)i * lda + j] = v;
-        }
-      }
-    }
-    __syncthreads();
-    const double piv = cb[j];
-    if (!(piv > 0.0)) {
-      bad = true;
-      break;
-    }
-    const double rinv = 1.0 / piv;
-    double ci[R], cc[S];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = ty + 16 * r;
-      ci[r] = (i > j && i < d) ? cb[i] * rinv : 0.0;
-    }
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int c = tx + 32 * s;
-      cc[s] = (c > j && c < d) ? cb[c] : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-      for (int s = 0; s < S; ++s) a[r][s] -= ci[r] * cc[s];
-  }
-  if (bad) {
-    for (int i = tid; i < d; i += kThreads) x_next[i] = x[i];
-    if (tid == 0) set_status(status, 3 /* IHS_ERR_NOT_SPD */);
-    return;
-  }
-  // (elements above the diagonal in a[][] picked up garbage products above; they are never read)
-  __syncthreads();
-  for (int j = tid; j < d; j += kThreads) rdiag[j] = 1.0 / sqrt(L[(int64_t)j * lda + j]);
-  __syncthreads();
-  for (int i = ty; i < d; i += 16)
-    for (int c = tx; c <= i; c += 32)
-      L[(int64_t)i * lda + c] = (c == i) ? sqrt(L[(int64_t)i * lda + i]) : L[(int64_t)i * lda + c] * rdiag[c];
-  __syncthreads();
-  if (tid < 32) {
-    const int lane = tid;
-    double z[S];
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int i = lane + 32 * s;
-      z[s] = i < d ? g[i] : 0.0;
-    }
-    // forward: L y = g
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      for (int jj = 0; jj < 32; ++jj) {
-        const int j = 32 * s + jj;
-        if (j >= d) break;
-        const double yj = __shfl_sync(0xffffffffu, z[s], jj) * rdiag[j];
-        if (lane == jj) z[s] = yj;
-#pragma unroll
-        for (int q = s; q < S; ++q) {
-          const int i = lane + 32 * q;
-          if (i > j && i < d) z[q] -= L[(int64_t)i * lda + j] * yj;
-        }
-      }
-    }
-    // backward: L^T u = y
-#pragma unroll
-    for (int s = S - 1; s >= 0; --s) {
-      for (int jj = 31; jj >= 0; --jj) {
-        const int i = 32 * s + jj;
-        if (i >= d) continue;
-        const double ui = __shfl_sync(0xffffffffu, z[s], jj) * rdiag[i];
-        if (lane == jj) z[s] = ui;
-#pragma unroll
-        for (int q = 0; q <= s; ++q) {
-          const int k = lane + 32 * q;
-          if (k < i) z[q] -= L[(int64_t)i * lda + k] * ui;
-        }
-      }
-    }
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      const int i = lane + 32 * s;
-      if (i < d) x_next[i] = x[i] + z[s];
-    }
-  }
-}
-
-template <int R, int S>
-void launch_reg(const double *H, const double *g, int d, const double *x, double *x_next, int *status,
-                cudaStream_t st) {
-  const size_t smem = ((size_t)d * (d + 1) + 3 * 32 * S) * 8;
-  IHS_SMEM_ATTR((chol_reg_kernel<R, S>), smem);
-  chol_reg_kernel<R, S><<<1, kThreads, smem, st>>>(H, g, d, x, x_next, status);
-}
-
 // ----------------------------------------------------------------------------
 // Blocked right-looking Cholesky in one CTA for D = ceil(d/32)*32 <= 160 (the
 // matrix is padded with an identity block).  Per 32-column block kb:
@@ -404,7 +196,11 @@ void launch_blocked(const double *H, const double *g, int d, const double *x, do
 }
 }  // namespace
 
-size_t chol_scratch_bytes(int64_t d) { return (size_t)(d * (d + 1) + d) * 8; }
+size_t chol_large_scratch_bytes(int64_t d);
+cudaError_t launch_chol_large(const double *H, const double *g, int64_t d, const double *x, double *x_next,
+                              double *scratch, int *status, cudaStream_t st, LaunchCounter lc);
+
+size_t chol_scratch_bytes(int64_t d) { return d > 160 ? chol_large_scratch_bytes(d) : 256; }
 
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,
                               double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc) {
@@ -421,13 +217,7 @@ cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const
     lc.add();
     return cudaGetLastError();
   }
-  const size_t need = (size_t)(d * (d + 1) + d) * 8;
-  const int use_smem = need <= kSmemLimit;
-  const size_t smem = use_smem ? need : 0;
-  IHS_SMEM_ATTR(chol_solve_kernel, smem);
-  chol_solve_kernel<<<1, kThreads, smem, st>>>(H, g, (int)d, x, x_next, scratch, status, use_smem);
-  lc.add();
-  return cudaGetLastError();
+  return launch_chol_large(H, g, d, x, x_next, scratch, status, st, lc);
 }
 
 }  // namespace ihs

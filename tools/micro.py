@@ -16,7 +16,7 @@ def bench(fn, reps=50):
 dev = torch.device("cuda", 0)
 what = sys.argv[1] if len(sys.argv) > 1 else "all"
 if what in ("chol", "all"):
-    for d in (10, 96, 128, 160, 256):
+    for d in (10, 96, 128, 160, 256, 1024):
         Q, _ = torch.linalg.qr(torch.randn(d, d, dtype=torch.float64, device=dev))
         H = (Q * torch.linspace(1, 13, d, dtype=torch.float64, device=dev)) @ Q.T
         g = torch.randn(d, dtype=torch.float64, device=dev); x = torch.zeros_like(g); xn = torch.empty_like(g)
