@@ -138,6 +138,51 @@ def ncu_traffic(kernel: str):
         return None
 
 
+DMMA_TFLOPS = 36.7  # fp64 DMMA peak measured on this pool's B200 (tools/probe/probe.cu, profiles/r01_probe.txt)
+
+
+def roofline(prof, cfg, n_loc, nnz_loc, ms_step):
+    """Achieved vs peak for the dominant kernel group of the step, from the
+    library's CUDA events (algorithmic bytes / flops per launch)."""
+    peaks, peak_src = measured_peaks()
+    d, m = cfg.d, cfg.m
+    groups = {k: v for k, v in prof.items() if v[1] > 0}
+    if not groups:
+        return None
+    name = max(groups, key=lambda k: groups[k][0])
+    tot, k = groups[name]
+    avg = tot / k
+    out = {"kernel_group": name, "avg_launch_ms": avg, "share_of_step": tot / ms_step if ms_step else None}
+    if name in ("sketch", "sjlt", "csr", "grad"):
+        if name == "sketch":
+            alg = 8 * n_loc * d + 12 * n_loc + 16 * m * d  # A once, b + perm per row, SA + g partials
+            out["kernel"] = "cs_gather_tma_kernel<fused> (CountSketch sketch + gradient, one read of A)"
+        elif name == "sjlt":
+            alg = 8 * n_loc * d + 8 * m * d  # A once + SA
+            out["kernel"] = "sjlt_dense_kernel (smem-tile SJLT sketch; shared-memory bound, DESIGN.md 9)"
+        elif name == "grad":
+            alg = 8 * n_loc * d + 8 * n_loc
+            out["kernel"] = "grad_dense_kernel"
+        else:
+            alg = 8 * (n_loc + 1) + 12 * nnz_loc + 8 * n_loc + 8 * m * d
+            out["kernel"] = "csr_sketch_grad_kernel (CSR sketch + gradient)"
+        ach = alg / (avg / 1e3) / 1e9
+        out.update({"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": ach / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": alg,
+                    "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"})
+    elif name == "gram":
+        fl = 2.0 * m * d * d / 2  # symmetric half: m d^2 FMA-pairs
+        ach = fl / (avg / 1e3) / 1e12
+        out.update({"kernel": "gram_kernel (DMMA m8n8k4 f64)", "bound": "tensor", "achieved": ach,
+                    "peak": DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_TFLOPS,
+                    "algorithmic_flops_per_launch": fl, "peak_source": "measured fp64 DMMA (probe)"})
+    else:
+        out.update({"kernel": name, "bound": "latency", "achieved": None, "peak": None, "unit": None,
+                    "frac": None})
+    out["traffic"] = ncu_traffic(name)
+    return out
+
+
 # ----------------------------------------------------------------------------- reference arm
 def run_reference(args):
     rank, world, _ = dist_env()
@@ -194,18 +239,29 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cfg = synthetic.CONFIGS[args.config]
-    if cfg.layout != "dense" or cfg.s != 1 or cfg.constraint != "ols":
-        raise SystemExit("bench.py times the dense CountSketch OLS configs (C1, C2)")
     r0, r1 = shard_rows(cfg.n, rank, world)
     # ---- inputs, resident in HBM before timing
-    A = synthetic.dense_A(cfg, dev, rows=(r0, r1))
     xs = synthetic.x_star(cfg, dev)
-    b = (A @ xs + synthetic.noise(cfg, dev)[r0:r1]).contiguous()
+    radius = float(xs.abs().sum()) if cfg.constraint == "l1ball" else 0.0
+    if cfg.layout == "dense":
+        A = synthetic.dense_A(cfg, dev, rows=(r0, r1))
+        b = (A @ xs + synthetic.noise(cfg, dev)[r0:r1]).contiguous()
+        Am = P.Dense(A, row_offset=r0)
+        nnz = n_loc_nnz = None
+    else:  # CSR: every rank draws the whole structure once and keeps its row block
+        rp, cl, vl = synthetic.csr_A(cfg, dev)
+        b = (synthetic.csr_matvec(rp, cl, vl, xs) + synthetic.noise(cfg, dev))[r0:r1].contiguous()
+        e0, e1 = int(rp[r0]), int(rp[r1])
+        Am = P.Csr((rp[r0:r1 + 1] - e0).contiguous(), cl[e0:e1].contiguous(), vl[e0:e1].contiguous(), cfg.d,
+                   row_offset=r0)
+        nnz = int(rp[-1])
+        n_loc_nnz = e1 - e0
+        del rp, cl, vl
+        A = None
     del xs
     ctx = P.Context(local)
     spec = P.Spec(m=cfg.m, s=cfg.s, seed=cfg.hash_seed)
-    Am = P.Dense(A, row_offset=r0)
-    S = ShardedIHS(Am, b, spec, ops=CudaOps(ctx))
+    S = ShardedIHS(Am, b, spec, ops=CudaOps(ctx), constraint=cfg.constraint, radius=radius)
     d = cfg.d
     xa = torch.zeros(d, dtype=torch.float64, device=dev)
     xb = torch.empty_like(xa)
@@ -249,24 +305,13 @@ def main():
     value = cfg.n * args.steps / (ms / 1e3)
     prof = {name: ctx.profile(k) for k, name in enumerate(P.KERNEL_GROUPS)}
     ctx.set_profiling(False)
-    # ---- roofline of the dominant kernel: the fused sketch+gradient gather
-    peaks, peak_src = measured_peaks()
+    # ---- roofline of the dominant kernel group (C2: the fused sketch+gradient gather)
     n_loc = r1 - r0
-    sk_ms, sk_n = prof["sketch"]
-    alg_bytes = 8 * n_loc * d + 12 * n_loc + 16 * cfg.m * d  # A once, b + perm per row, SA + g partials
-    sk_avg = sk_ms / max(sk_n, 1)
-    achieved = alg_bytes / (sk_avg / 1e3) / 1e9 if sk_n else None
-    roof = {"kernel": "cs_gather_kernel<4,8,true> (fused CountSketch sketch + gradient)", "bound": "hbm",
-            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"] if achieved else None,
-            "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-            "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": sk_avg,
-            "traffic": ncu_traffic("cs_gather_kernel"),
-            "share_of_step": (sk_ms / ms_local) if ms_local > 0 else None}
+    roof = roofline(prof, cfg, n_loc, n_loc_nnz, ms_local)
     breakdown = {name: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for name, v in prof.items() if v[1]}
     # ---- time to 1e-10 (IHS solve from x^0 = 0; errors post hoc, outside the timing)
     ttt = None
-    if not args.no_ttt:
+    if not args.no_ttt and cfg.layout == "dense" and cfg.constraint == "ols":
         xopt = S.exact_ols()
         Tmax = 60
         xh = S.solve(Tmax, iter0=1000)
@@ -293,7 +338,7 @@ def main():
         del xh
     # ---- e2e: the public solve call with HOST (pinned) buffers, copies inside
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and cfg.layout == "dense" and cfg.constraint == "ols":
         try:
             T_e2e = (ttt or {}).get("iterations") or 30
             A_h = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)
@@ -332,15 +377,16 @@ def main():
             e2e = {"value": None, "unit": UNIT, "error": repr(ex)[:300]}
     # ---- cpu baseline: the oracle, as it stands, rank 0 at N = 1 only
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and cfg.layout == "dense":
         import oracle
         A_np = A.cpu().numpy()
         b_np = b.cpu().numpy()
         x = torch.zeros(d, dtype=torch.float64).numpy()
         it = 0
         t0 = time.perf_counter()
+        kw = dict(constraint="l1ball", tau=radius) if cfg.constraint == "l1ball" else {}
         while True:
-            xh_o, _ = oracle.ihs_solve(A_np, b_np, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=it, x0=x)
+            xh_o, _ = oracle.ihs_solve(A_np, b_np, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=it, x0=x, **kw)
             x = xh_o[-1]
             it += 1
             el = time.perf_counter() - t0
@@ -355,7 +401,7 @@ def main():
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
                "config": config_obj(cfg, world, {"per_gpu_rows": n_loc}),
-               "hbm_GBps_step": (8 * cfg.n * d / world) / (ms_step / 1e3) / 1e9,
+               "hbm_GBps_step": (cfg.a_bytes / world) / (ms_step / 1e3) / 1e9,
                "roofline": roof, "breakdown_ms": breakdown, "time_to_1e-10": ttt, "e2e": e2e,
                "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
                "gpu": torch.cuda.get_device_name(dev)}

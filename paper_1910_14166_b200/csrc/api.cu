@@ -209,37 +209,49 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
     if (SA && s > 1) IHS_CUDA(launch_scale(SA, m * d, spec_scale(spec), st, lc_of(c)));
     return IHS_OK;
   }
-  // dense
-  const bool use_sort = (s == 1) && cs_sort_supported(m);
+  // dense.  CountSketch (s = 1) and SJLT (s > 1): per block j of m/s buckets, a
+  // stable counting sort of the rows by bucket and one bucket-ordered gather
+  // (SJLT = s stacked independent CountSketches).  The
+  // gradient rides on block 0's read of A.  IHS_SJLT=tile selects the
+  // single-pass shared-memory tile kernel instead (s > 1).
+  const int64_t M = m / s;
+  static const bool sjlt_tile = getenv("IHS_SJLT") && !std::strcmp(getenv("IHS_SJLT"), "tile");
+  const bool use_sort = cs_sort_supported(M) && !(s > 1 && sjlt_tile);
   const bool fuse = SA && use_sort && g && d <= 256;
   if (SA) {
     if (use_sort) {
-      CsSortPlan p = cs_sort_plan(n, m);
+      CsSortPlan p = cs_sort_plan(n, M);
       int32_t *hist, *tiles;
       uint32_t *perm;
       IHS_TRY(scratch(c, S_HIST, p.hist_bytes(), &hist));
       IHS_TRY(scratch(c, S_TILES, p.tiles_bytes(), &tiles));
       IHS_TRY(scratch(c, S_PERM, p.perm_bytes(), &perm));
-      {
-        Prof pr(c, IHS_K_SORT);
-        IHS_CUDA(launch_cs_sort(p, key, A->row_offset, hist, tiles, perm, st, lc_of(c)));
-      }
       double *gpart = nullptr;
-      if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)m * d * 8, &gpart));
-      {
-        Prof pr(c, IHS_K_SKETCH);
-        if (c->gather == 1 && cs_gather_tma_supported(d, A->values))
-          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st,
-                                        lc_of(c)));
-        else if (c->gather == 2 && cs_gather_async_supported(d, A->values))
-          IHS_CUDA(launch_cs_gather_async(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st,
+      if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)M * d * 8, &gpart));
+      const double scale = spec_scale(spec);
+      for (int j = 0; j < s; ++j) {
+        double *SAj = SA + (int64_t)j * M * d;
+        double *gp = (j == 0) ? gpart : nullptr;
+        {
+          Prof pr(c, IHS_K_SORT);
+          IHS_CUDA(launch_cs_sort(p, key, A->row_offset, (uint32_t)j, (uint32_t)s, hist, tiles, perm, st, lc_of(c)));
+        }
+        {
+          Prof pr(c, IHS_K_SKETCH);
+          if (c->gather == 1 && cs_gather_tma_supported(d, A->values))
+            IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale, st,
                                           lc_of(c)));
-        else
-          IHS_CUDA(launch_cs_gather(A->values, n, d, m, hist, tiles, p.nchunks, perm, b, x, SA, gpart, st, lc_of(c)));
+          else if (c->gather == 2 && cs_gather_async_supported(d, A->values))
+            IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale,
+                                            st, lc_of(c)));
+          else
+            IHS_CUDA(launch_cs_gather(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale, st,
+                                      lc_of(c)));
+        }
       }
       if (fuse) {
         Prof pr(c, IHS_K_REDUCE);
-        IHS_CUDA(launch_reduce_rows(gpart, m, d, g, st, lc_of(c)));
+        IHS_CUDA(launch_reduce_rows(gpart, M, d, g, st, lc_of(c)));
       }
     } else {
       SjltPlan p;
@@ -300,7 +312,7 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
   ihs_inner_cfg k = cfg ? *cfg : default_inner();
   if (k.max_inner < 1 || k.power_iters < 1 || !(k.inner_tol >= 0.0) || !(k.lip_safety > 0.0))
     return IHS_ERR_INVALID_ARGUMENT;
-  if ((size_t)5 * d * 8 > 200 * 1024) return IHS_ERR_UNSUPPORTED;
+  if (!pg_supported(d)) return IHS_ERR_UNSUPPORTED;
   Prof pr(c, IHS_K_PG);
   IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.inner_tol, k.lip_safety, xn, inner,
                                 nullptr, c->d_status, c->stream, lc_of(c)));

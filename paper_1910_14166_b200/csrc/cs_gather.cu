@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(64) cs_gather_kernel(const double *__restrict_
                                                        const uint32_t *__restrict__ perm,
                                                        const double *__restrict__ bvec,
                                                        const double *__restrict__ x, double *__restrict__ SA,
-                                                       double *__restrict__ gpart, int64_t win_rows, int64_t pd) {
+                                                       double *__restrict__ gpart, int64_t win_rows, int64_t pd,
+                                                       double scale) {
   const int warp = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (warp >= m * nslices) return;
@@ -182,7 +183,7 @@ __global__ void __launch_bounds__(64) cs_gather_kernel(const double *__restrict_
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     if (col[k] < d) {
-      SA[(int64_t)b * d + col[k]] = w.acc[k];
+      SA[(int64_t)b * d + col[k]] = scale == 1.0 ? w.acc[k] : w.acc[k] * scale;
       if constexpr (FUSE) gpart[(int64_t)b * d + col[k]] = w.gacc[k];
     }
   }
@@ -201,7 +202,7 @@ __global__ void __launch_bounds__(64) cs_gather_async_kernel(const double *__res
                                                              const uint32_t *__restrict__ perm,
                                                              const double *__restrict__ bvec,
                                                              const double *__restrict__ x, double *__restrict__ SA,
-                                                             double *__restrict__ gpart) {
+                                                             double *__restrict__ gpart, double scale) {
   extern __shared__ __align__(16) double ring_all[];
   const int wib = threadIdx.x >> 5;
   const int b = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(64) cs_gather_async_kernel(const double *__res
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     if (col[k] < d) {
-      SA[(int64_t)b * d + col[k]] = acc[k];
+      SA[(int64_t)b * d + col[k]] = scale == 1.0 ? acc[k] : acc[k] * scale;
       if constexpr (FUSE) gpart[(int64_t)b * d + col[k]] = gacc[k];
     }
   }
@@ -312,17 +313,17 @@ __global__ void __launch_bounds__(64) cs_gather_async_kernel(const double *__res
 template <int NV, int U, int S>
 cudaError_t launch_async_t(bool fuse, const double *A, int64_t n, int d, int m, const int32_t *hist,
                            const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
-                           const double *x, double *SA, double *gpart, cudaStream_t st) {
+                           const double *x, double *SA, double *gpart, double scale, cudaStream_t st) {
   const size_t smem = (size_t)2 * S * U * d * 8;
   const unsigned grid = (unsigned)((m + 1) / 2);
   if (fuse) {
     IHS_SMEM_ATTR((cs_gather_async_kernel<NV, U, S, true>), smem);
     cs_gather_async_kernel<NV, U, S, true><<<grid, 64, smem, st>>>(A, n, d, m, hist, tile_sums, nchunks, perm, bvec,
-                                                                   x, SA, gpart);
+                                                                   x, SA, gpart, scale);
   } else {
     IHS_SMEM_ATTR((cs_gather_async_kernel<NV, U, S, false>), smem);
     cs_gather_async_kernel<NV, U, S, false><<<grid, 64, smem, st>>>(A, n, d, m, hist, tile_sums, nchunks, perm,
-                                                                    nullptr, nullptr, SA, nullptr);
+                                                                    nullptr, nullptr, SA, nullptr, scale);
   }
   return cudaGetLastError();
 }
@@ -330,7 +331,7 @@ cudaError_t launch_async_t(bool fuse, const double *A, int64_t n, int d, int m, 
 template <int NV, int U>
 cudaError_t launch_nv(bool fuse, const double *A, int64_t n, int d, int m, int nslices, const int32_t *hist,
                       const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
-                      const double *x, double *SA, double *gpart, cudaStream_t st) {
+                      const double *x, double *SA, double *gpart, double scale, cudaStream_t st) {
   const int64_t warps = (int64_t)m * nslices;
   // L2 streaming window (IHS_L2_WIN_MB / IHS_L2_PD): off by default -- measured slower on B200
   static const int64_t win_mb = getenv("IHS_L2_WIN_MB") ? atoll(getenv("IHS_L2_WIN_MB")) : 0;
@@ -339,10 +340,10 @@ cudaError_t launch_nv(bool fuse, const double *A, int64_t n, int d, int m, int n
   const unsigned grid = (unsigned)((warps + 1) / 2);
   if (fuse)
     cs_gather_kernel<NV, U, true><<<grid, 64, 0, st>>>(A, n, d, m, nslices, hist, tile_sums, nchunks, perm, bvec, x,
-                                                        SA, gpart, win_rows, pd);
+                                                        SA, gpart, win_rows, pd, scale);
   else
     cs_gather_kernel<NV, U, false><<<grid, 64, 0, st>>>(A, n, d, m, nslices, hist, tile_sums, nchunks, perm,
-                                                         nullptr, nullptr, SA, nullptr, win_rows, pd);
+                                                         nullptr, nullptr, SA, nullptr, win_rows, pd, scale);
   return cudaGetLastError();
 }
 }  // namespace
@@ -353,16 +354,17 @@ bool cs_gather_async_supported(int64_t d, const void *A) {
 
 cudaError_t launch_cs_gather_async(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                                    const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm,
-                                   const double *bvec, const double *x, double *SA, double *gpart, cudaStream_t st,
-                                   LaunchCounter lc) {
+                                   const double *bvec, const double *x, double *SA, double *gpart, double scale,
+                                   cudaStream_t st, LaunchCounter lc) {
   const bool fuse = gpart != nullptr;
   const int nv = (int)((d + 31) / 32);
   static const int stages = getenv("IHS_ASYNC_STAGES") ? atoi(getenv("IHS_ASYNC_STAGES")) : 3;
   cudaError_t e;
   const int di = (int)d, mi = (int)m;
 #define IHS_ASYNC(NV, U)                                                                                          \
-  (stages >= 4 ? launch_async_t<NV, U, 4>(fuse, A, n, di, mi, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st) \
-               : launch_async_t<NV, U, 3>(fuse, A, n, di, mi, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st))
+  (stages >= 4                                                                                                   \
+       ? launch_async_t<NV, U, 4>(fuse, A, n, di, mi, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, st) \
+       : launch_async_t<NV, U, 3>(fuse, A, n, di, mi, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, st))
   switch (nv) {
     case 1: e = IHS_ASYNC(1, 8); break;
     case 2: e = IHS_ASYNC(2, 8); break;
@@ -379,7 +381,8 @@ cudaError_t launch_cs_gather_async(const double *A, int64_t n, int64_t d, int64_
 
 cudaError_t launch_cs_gather(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                              const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
-                             const double *x, double *SA, double *gpart, cudaStream_t st, LaunchCounter lc) {
+                             const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
+                             LaunchCounter lc) {
   const bool fuse = gpart != nullptr;
   int nv = (int)((d + 31) / 32);
   int nslices = 1;
@@ -391,13 +394,13 @@ cudaError_t launch_cs_gather(const double *A, int64_t n, int64_t d, int64_t m, c
   cudaError_t e;
   const int di = (int)d, mi = (int)m;
   switch (nv) {
-    case 1: e = launch_nv<1, 16>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
-    case 2: e = launch_nv<2, 16>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
-    case 3: e = launch_nv<3, 8>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
-    case 4: e = launch_nv<4, 8>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
+    case 1: e = launch_nv<1, 16>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, st); break;
+    case 2: e = launch_nv<2, 16>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, st); break;
+    case 3: e = launch_nv<3, 8>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, st); break;
+    case 4: e = launch_nv<4, 8>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, st); break;
     case 5:
-    case 6: e = launch_nv<6, 4>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
-    default: e = launch_nv<8, 4>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st); break;
+    case 6: e = launch_nv<6, 4>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, st); break;
+    default: e = launch_nv<8, 4>(fuse, A, n, di, mi, nslices, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, st); break;
   }
   lc.add();
   return e;

@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
     const double *__restrict__ A, int64_t n, int d, int m, const int32_t *__restrict__ hist,
     const int32_t *__restrict__ tile_sums, int64_t nchunks, const uint32_t *__restrict__ perm,
     const double *__restrict__ bvec, const double *__restrict__ x, double *__restrict__ SA,
-    double *__restrict__ gpart) {
+    double *__restrict__ gpart, double scale) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *ring = reinterpret_cast<double *>(smem_raw);                                // [kStages][kRows][d]
   double *bs = ring + (size_t)kStages * kRows * d;                                    // [kStages][kRows]
@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     if (cv[q]) {
-      SA[(int64_t)b * d + tid + kConsumers * q] = acc[q];
+      SA[(int64_t)b * d + tid + kConsumers * q] = scale == 1.0 ? acc[q] : acc[q] * scale;
       if constexpr (FUSE) gpart[(int64_t)b * d + tid + kConsumers * q] = gac[q];
     }
   }
@@ -197,10 +197,10 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
 template <bool FUSE, int NC>
 void launch_tma_t(size_t smem, const double *A, int64_t n, int d, int m, const int32_t *hist, const int32_t *tile_sums,
                   int64_t nchunks, const uint32_t *perm, const double *bvec, const double *x, double *SA,
-                  double *gpart, cudaStream_t st) {
+                  double *gpart, double scale, cudaStream_t st) {
   IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC>), smem);
   cs_gather_tma_kernel<FUSE, NC><<<(unsigned)m, kConsumers + 32, smem, st>>>(A, n, d, m, hist, tile_sums, nchunks,
-                                                                              perm, bvec, x, SA, gpart);
+                                                                              perm, bvec, x, SA, gpart, scale);
 }
 }  // namespace
 
@@ -210,15 +210,17 @@ bool cs_gather_tma_supported(int64_t d, const void *A) {
 
 cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
-                                 const double *x, double *SA, double *gpart, cudaStream_t st, LaunchCounter lc) {
+                                 const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
+                                 LaunchCounter lc) {
   const size_t smem = (size_t)kStages * kRows * d * 8 + (size_t)kStages * kRows * 8 * (1 + kCW) + 2 * kStages * 8 +
                       kStages * kRows * 4 + 64;
   const int nc = (int)((d + kConsumers - 1) / kConsumers);
   const bool f = gpart != nullptr;
 #define IHS_TMA(NC)                                                                                           \
-  (f ? launch_tma_t<true, NC>(smem, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, st) \
+  (f ? launch_tma_t<true, NC>(smem, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart,   \
+                              scale, st)                                                                     \
      : launch_tma_t<false, NC>(smem, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, nullptr, nullptr, SA,   \
-                               nullptr, st))
+                               nullptr, scale, st))
   if (nc <= 1) IHS_TMA(1);
   else if (nc == 2) IHS_TMA(2);
   else IHS_TMA(4);

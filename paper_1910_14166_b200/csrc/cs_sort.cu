@@ -32,7 +32,7 @@ __global__ void hash_export_kernel(uint64_t key, uint32_t s, uint32_t M, int64_t
 // Per-chunk bucket histogram, written bucket-major: hist[b * nchunks + chunk].
 __global__ void __launch_bounds__(kHistThreads) cs_hist_kernel(int64_t n, int64_t chunk, int64_t nchunks,
                                                                uint32_t m, uint64_t key, int64_t row_offset,
-                                                               int32_t *__restrict__ hist) {
+                                                               uint32_t jb, uint32_t sb, int32_t *__restrict__ hist) {
   extern __shared__ int32_t cnt[];
   for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) cnt[b] = 0;
   __syncthreads();
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kHistThreads) cs_hist_kernel(int64_t n, int64_
   const int64_t r1 = min(n, r0 + chunk);
   for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
     bool neg;
-    uint32_t b = hash_bucket(key, (uint64_t)(row_offset + r), 0u, 1u, m, neg);
+    uint32_t b = hash_bucket(key, (uint64_t)(row_offset + r), jb, sb, m, neg) - jb * m;
     atomicAdd(&cnt[b], 1);
   }
   __syncthreads();
@@ -128,14 +128,19 @@ __device__ __forceinline__ int32_t scanned_at(const int32_t *hist, const int32_t
 }
 
 // Stable scatter of row ids: rows of a chunk are split over 8 warps in order;
-// each warp walks its rows 32 at a time and ranks equal buckets with
-// match_any, so positions follow ascending row order within every bucket.
+// each warp caches the buckets of its rows in registers (kMaxGroups groups of
+// 32), counts them with warp-private shared-memory atomics, and after a
+// cross-warp exclusive scan per bucket places every row with one
+// atomicAdd-return per (group, bucket) leader: a warp's shared-memory atomics
+// complete in issue order, so positions follow ascending row order within
+// every bucket (stable).
+constexpr int kMaxGroups = 16;  // rows per warp sub-chunk <= 512
 __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
-    int64_t n, int64_t chunk, int64_t nchunks, uint32_t m, uint64_t key, int64_t row_offset,
-    const int32_t *__restrict__ hist, const int32_t *__restrict__ tile_sums, uint32_t *__restrict__ perm) {
+    int64_t n, int64_t chunk, int64_t nchunks, uint32_t m, uint64_t key, int64_t row_offset, uint32_t jb,
+    uint32_t sb, const int32_t *__restrict__ hist, const int32_t *__restrict__ tile_sums, uint32_t *__restrict__ perm) {
   extern __shared__ unsigned char smem_raw[];
-  int32_t *base = reinterpret_cast<int32_t *>(smem_raw);                 // m
-  uint16_t *wcnt = reinterpret_cast<uint16_t *>(smem_raw + 4 * (size_t)m);  // 8 * m
+  int32_t *base = reinterpret_cast<int32_t *>(smem_raw);            // m
+  int32_t *wcnt = base + m;                                           // 8 * m
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t e = threadIdx.x; e < kScatterWarps * m; e += blockDim.x) wcnt[e] = 0;
   __syncthreads();
@@ -144,40 +149,47 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
   const int64_t sub = chunk / kScatterWarps;
   const int64_t ws = r0 + warp * sub;
   const int64_t we = min(r1, ws + sub);
-  uint16_t *my = wcnt + (size_t)warp * m;
-  for (int64_t r = ws + lane; r - lane < we; r += 32) {
-    const bool valid = r < we;
+  int32_t *my = wcnt + (size_t)warp * m;
+  uint32_t bk[kMaxGroups];
+#pragma unroll
+  for (int q = 0; q < kMaxGroups; ++q) {
+    const int64_t r = ws + 32 * q + lane;
     bool neg = false;
-    uint32_t b = valid ? hash_bucket(key, (uint64_t)(row_offset + r), 0u, 1u, m, neg) : 0xffffffffu;
-    unsigned mask = __match_any_sync(0xffffffffu, b);
-    if (valid && lane == __ffs(mask) - 1) my[b] = (uint16_t)(my[b] + __popc(mask));
-    __syncwarp();
+    uint32_t b = 0xffffffffu;
+    if (ws + 32 * q < we && r < we) b = hash_bucket(key, (uint64_t)(row_offset + r), jb, sb, m, neg) - jb * m;
+    bk[q] = b | (neg ? 0x80000000u : 0u);  // m < 2^31: bit 31 free for the sign
+    if (ws + 32 * q < we) {
+      const uint32_t bb = r < we ? (bk[q] & 0x7fffffffu) : 0xffffffffu;
+      const unsigned mask = __match_any_sync(0xffffffffu, bb);
+      if (r < we && lane == __ffs(mask) - 1) atomicAdd(&my[bb], __popc(mask));
+    }
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) {
     base[b] = scanned_at(hist, tile_sums, (int64_t)b * nchunks + blockIdx.x);
-    uint32_t acc = 0;
+    int32_t acc = 0;
 #pragma unroll
     for (int w = 0; w < kScatterWarps; ++w) {
-      uint32_t t = wcnt[(size_t)w * m + b];
-      wcnt[(size_t)w * m + b] = (uint16_t)acc;
+      const int32_t t = wcnt[(size_t)w * m + b];
+      wcnt[(size_t)w * m + b] = acc;
       acc += t;
     }
   }
   __syncthreads();
   const unsigned lt = lanemask_lt();
-  for (int64_t r = ws + lane; r - lane < we; r += 32) {
-    const bool valid = r < we;
-    bool neg = false;
-    uint32_t b = valid ? hash_bucket(key, (uint64_t)(row_offset + r), 0u, 1u, m, neg) : 0xffffffffu;
-    unsigned mask = __match_any_sync(0xffffffffu, b);
-    if (valid) {
-      int32_t pos = base[b] + (int32_t)my[b] + __popc(mask & lt);
-      perm[pos] = (uint32_t)r | (neg ? 0x80000000u : 0u);
+#pragma unroll
+  for (int q = 0; q < kMaxGroups; ++q) {
+    if (ws + 32 * q < we) {
+      const int64_t r = ws + 32 * q + lane;
+      const bool valid = r < we;
+      const uint32_t bb = valid ? (bk[q] & 0x7fffffffu) : 0xffffffffu;
+      const unsigned mask = __match_any_sync(0xffffffffu, bb);
+      const int leader = __ffs(mask) - 1;
+      int32_t old = 0;
+      if (valid && lane == leader) old = atomicAdd(&my[bb], __popc(mask));
+      old = __shfl_sync(0xffffffffu, old, leader);
+      if (valid) perm[base[bb] + old + __popc(mask & lt)] = (uint32_t)r | (bk[q] & 0x80000000u);
     }
-    __syncwarp();
-    if (valid && lane == __ffs(mask) - 1) my[b] = (uint16_t)(my[b] + __popc(mask));
-    __syncwarp();
   }
 }
 }  // namespace
@@ -192,7 +204,7 @@ cudaError_t launch_hash_export(uint64_t key, uint32_t s, uint32_t M, int64_t row
   return cudaGetLastError();
 }
 
-bool cs_sort_supported(int64_t m) { return m >= 1 && m * (4 + 2 * kScatterWarps) <= 200 * 1024; }
+bool cs_sort_supported(int64_t m) { return m >= 1 && m * (4 + 4 * kScatterWarps) <= 200 * 1024; }
 
 CsSortPlan cs_sort_plan(int64_t n, int64_t m) {
   CsSortPlan p;
@@ -204,7 +216,7 @@ CsSortPlan cs_sort_plan(int64_t n, int64_t m) {
   chunk = std::max<int64_t>(chunk, 1024);
   while (((n + chunk - 1) / chunk) * m > (int64_t(4) << 20) && chunk < 32768) chunk *= 2;
   chunk = (chunk + 255) / 256 * 256;
-  chunk = std::min<int64_t>(chunk, 32768);
+  chunk = std::min<int64_t>(chunk, (int64_t)kScatterWarps * 32 * 16);  // <= 16 groups of 32 rows per warp
   p.chunk = chunk;
   p.nchunks = std::max<int64_t>(1, (n + chunk - 1) / chunk);
   p.entries = m * p.nchunks;
@@ -212,19 +224,20 @@ CsSortPlan cs_sort_plan(int64_t n, int64_t m) {
   return p;
 }
 
-cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset, int32_t *hist,
+cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset, uint32_t jb, uint32_t sb, int32_t *hist,
                            int32_t *tile_sums, uint32_t *perm, cudaStream_t st, LaunchCounter lc) {
   const uint32_t m = (uint32_t)p.m;
   size_t hsmem = 4 * (size_t)m;
   IHS_SMEM_ATTR(cs_hist_kernel, hsmem);
-  cs_hist_kernel<<<(unsigned)p.nchunks, kHistThreads, hsmem, st>>>(p.n, p.chunk, p.nchunks, m, key, row_offset, hist);
+  cs_hist_kernel<<<(unsigned)p.nchunks, kHistThreads, hsmem, st>>>(p.n, p.chunk, p.nchunks, m, key, row_offset, jb, sb,
+                                                                    hist);
   scan_tiles_kernel<<<(unsigned)p.ntiles, 1024, 0, st>>>(hist, p.entries, tile_sums);
   scan_sums_kernel<<<1, 1024, 0, st>>>(tile_sums, p.ntiles);
-  size_t ssmem = (4 + 2 * kScatterWarps) * (size_t)m;
+  size_t ssmem = (4 + 4 * kScatterWarps) * (size_t)m;
   IHS_SMEM_ATTR(cs_scatter_kernel, ssmem);
   if (p.n > 0)
     cs_scatter_kernel<<<(unsigned)p.nchunks, kScatterWarps * 32, ssmem, st>>>(p.n, p.chunk, p.nchunks, m, key,
-                                                                              row_offset, hist, tile_sums, perm);
+                                                                              row_offset, jb, sb, hist, tile_sums, perm);
   lc.add(p.n > 0 ? 4 : 3);
   return cudaGetLastError();
 }

@@ -114,22 +114,26 @@ __global__ void __launch_bounds__(128) gram_kernel(const double *__restrict__ SA
     }
 }
 
-// H[p][q] = H[q][p] = scale^2 * sum_split partial (fixed order).
-__global__ void gram_reduce_kernel(const double *__restrict__ partials, int d, int tiles, int ntri, int nsplit,
-                                   double scale2, double *__restrict__ H) {
+// H[p][q] = H[q][p] = scale^2 * sum_split partial (fixed order).  One thread
+// per element of the upper tiles (grid: tile x 16 chunks of 256 elements).
+__global__ void __launch_bounds__(256) gram_reduce_kernel(const double *__restrict__ partials, int d, int tiles,
+                                                          int ntri, int nsplit, double scale2,
+                                                          double *__restrict__ H) {
   int P, Q;
   tri_decode(blockIdx.x, tiles, P, Q);
-  for (int e = threadIdx.x; e < GT * GT; e += blockDim.x) {
-    int r = e / GT, c = e % GT;
-    int p = P * GT + r, q = Q * GT + c;
-    if (p >= d || q >= d) continue;
-    if (P == Q && q < p) continue;
-    double s = 0.0;
-    for (int k = 0; k < nsplit; ++k) s += partials[((int64_t)k * ntri + blockIdx.x) * (GT * GT) + e];
-    s *= scale2;
-    H[(int64_t)p * d + q] = s;
-    H[(int64_t)q * d + p] = s;
-  }
+  const int e = blockIdx.y * 256 + threadIdx.x;
+  const int r = e / GT, c = e % GT;
+  const int p = P * GT + r, q = Q * GT + c;
+  if (p >= d || q >= d) return;
+  if (P == Q && q < p) return;
+  const double *src = partials + (int64_t)blockIdx.x * (GT * GT) + e;
+  const int64_t stride = (int64_t)ntri * (GT * GT);
+  double s = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < nsplit; ++k) s += src[k * stride];
+  s *= scale2;
+  H[(int64_t)p * d + q] = s;
+  H[(int64_t)q * d + p] = s;
 }
 }  // namespace
 
@@ -156,7 +160,8 @@ cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, doubl
   IHS_SMEM_ATTR(gram_kernel, smem);
   dim3 grid(p.ntri, p.nsplit);
   gram_kernel<<<grid, 128, smem, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kchunk, partials);
-  gram_reduce_kernel<<<p.ntri, 256, 0, st>>>(partials, (int)p.d, p.tiles, p.ntri, p.nsplit, scale * scale, H);
+  gram_reduce_kernel<<<dim3(p.ntri, (GT * GT) / 256), 256, 0, st>>>(partials, (int)p.d, p.tiles, p.ntri, p.nsplit,
+                                                                     scale * scale, H);
   lc.add(2);
   return cudaGetLastError();
 }

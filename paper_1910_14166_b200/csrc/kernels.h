@@ -30,29 +30,32 @@ CsSortPlan cs_sort_plan(int64_t n, int64_t m);
 bool cs_sort_supported(int64_t m);
 // hist: entries+1 int32 (bucket-major offsets after the scan); perm: n int32
 // (local row | sign << 31), rows of bucket b at [hist[b*nchunks], hist[(b+1)*nchunks]).
-cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset, int32_t *hist,
-                           int32_t *tile_sums, uint32_t *perm, cudaStream_t st, LaunchCounter lc);
+// Sorts by the bucket of SJLT block jb of sb (bucket - jb*m in [0, m)); CountSketch: jb = 0, sb = 1.
+cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset, uint32_t jb, uint32_t sb,
+                           int32_t *hist, int32_t *tile_sums, uint32_t *perm, cudaStream_t st, LaunchCounter lc);
 
 // ---- a2 (+a5 fused): bucket-ordered segmented signed row sums ---------------
 // SA[b, :] = sum over rows of bucket b (ascending) of sign * A[row, :], times scale.
 // If b_vec/x/gpart are non-null: gpart[b, :] = sum_rows A[row,:] * (b_row - A[row,:].x).
 cudaError_t launch_cs_gather(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                              const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
-                             const double *x, double *SA, double *gpart, cudaStream_t st, LaunchCounter lc);
+                             const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
+                             LaunchCounter lc);
 
 // cp.async-fed variant (per-warp shared-memory ring).  Requires even d <= 256
 // and a 16-byte aligned A.
 bool cs_gather_async_supported(int64_t d, const void *A);
 cudaError_t launch_cs_gather_async(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                                    const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm,
-                                   const double *bvec, const double *x, double *SA, double *gpart, cudaStream_t st,
-                                   LaunchCounter lc);
+                                   const double *bvec, const double *x, double *SA, double *gpart, double scale,
+                                   cudaStream_t st, LaunchCounter lc);
 // TMA-fed variant: one CTA per bucket, bulk copies of whole rows into a smem
 // ring.  Requires even d <= 256 and a 16-byte aligned A.
 bool cs_gather_tma_supported(int64_t d, const void *A);
 cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
-                                 const double *x, double *SA, double *gpart, cudaStream_t st, LaunchCounter lc);
+                                 const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
+                             LaunchCounter lc);
 
 // ---- a2 dense SJLT (s > 1): smem-tile accumulation --------------------------
 struct SjltPlan {
@@ -104,6 +107,8 @@ cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const
 
 // ---- a6 l1 ball: projected gradient -----------------------------------------
 size_t pg_scratch_bytes(int64_t d);
+bool pg_supported(int64_t d);
+int pg_cluster_size(int64_t d);
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
                                  int max_inner, int power_iters, double tol, double safety, double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,

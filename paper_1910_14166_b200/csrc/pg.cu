@@ -7,8 +7,12 @@
 // outer iteration); H stays L2-resident.  The projection threshold is found by
 // Michelot's fixed-point iteration, which reaches the same theta as the sorted
 // rule of the oracle (R8) in exact arithmetic.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
+
+#include <cooperative_groups.h>
 
 namespace ihs {
 
@@ -144,15 +148,200 @@ __global__ void __launch_bounds__(kThreads) pg_l1ball_kernel(const double *__res
     if (!converged) set_status(status, 4 /* IHS_ERR_NOT_CONVERGED */);
   }
 }
+
+// ----------------------------------------------------------------------------
+// Cluster version: CS CTAs (one thread-block cluster) keep H in distributed
+// shared memory -- CTA r holds rows [r R, (r+1) R) -- so no inner step touches
+// L2.  Each step: local GEMV rows -> z rows, written into every CTA's z buffer
+// through DSMEM (double-buffered by step parity), one cluster barrier, then
+// every CTA runs the identical projection / convergence test on the full
+// vector (same inputs, same code => bitwise-identical y in all CTAs).
+constexpr int kCT = 256;
+constexpr int kCW = kCT / 32;
+
+__device__ __forceinline__ void csum2(double &a, double &b, double *red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  __syncthreads();
+  if (lane == 0) {
+    red[warp] = a;
+    red[kCW + warp] = b;
+  }
+  __syncthreads();
+  double sa = 0.0, sb = 0.0;
+#pragma unroll
+  for (int w = 0; w < kCW; ++w) {
+    sa += red[w];
+    sb += red[kCW + w];
+  }
+  a = sa;
+  b = sb;
+}
+
+__global__ void __launch_bounds__(kCT) pg_cluster_kernel(const double *__restrict__ H, const double *__restrict__ g,
+                                                         int d, const double *__restrict__ x, double radius,
+                                                         int max_inner, int power_iters, double tol, double safety,
+                                                         double *x_next, int32_t *inner_iters, int *status) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int R = (d + cs - 1) / cs;
+  const int r0 = rank * R, r1 = min(d, r0 + R);
+  extern __shared__ double sm[];
+  double *Hs = sm;                   // R x d (my rows)
+  double *xs = Hs + (size_t)R * d;   // d
+  double *gs = xs + d;               // d
+  double *y = gs + d;                // d
+  double *w = y + d;                 // d : y - x, or the power-iteration vector
+  double *zb = w + d;                // 2 x d : z (or H v), double-buffered by step parity
+  __shared__ double red[2 * kCW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t e = tid; e < (int64_t)(r1 - r0) * d; e += kCT) Hs[e] = H[(int64_t)r0 * d + e];
+  for (int i = tid; i < d; i += kCT) {
+    xs[i] = x[i];
+    gs[i] = g[i];
+    y[i] = x[i];
+    w[i] = 1.0 / sqrt((double)d);
+  }
+  cluster.sync();
+  int par = 0;
+  // my rows of H v (or H (y - x)) -> every CTA's zb[par]
+  auto gemv_bcast = [&](bool pg_step, double L) {
+    double *dst = cluster.map_shared_rank(zb + par * d, lane < cs ? lane : 0);  // lane r writes CTA r
+    for (int p = r0 + warp; p < r1; p += kCW) {
+      const double *hr = Hs + (size_t)(p - r0) * d;
+      double acc = 0.0;
+      for (int q = lane; q < d; q += 32) acc = fma(hr[q], w[q], acc);
+      acc = warp_sum(acc);
+      const double val = pg_step ? y[p] - (acc - gs[p]) / L : acc;
+      if (lane < cs) dst[p] = val;
+    }
+    cluster.sync();
+  };
+  double lam = 0.0;
+  for (int it = 0; it < power_iters; ++it) {
+    gemv_bcast(false, 1.0);
+    const double *hv = zb + par * d;
+    double nn = 0.0, dummy = 0.0;
+    for (int i = tid; i < d; i += kCT) nn = fma(hv[i], hv[i], nn);
+    csum2(nn, dummy, red);
+    lam = sqrt(nn);
+    if (!(lam > 0.0)) break;
+    for (int i = tid; i < d; i += kCT) w[i] = hv[i] / lam;
+    par ^= 1;
+    __syncthreads();
+  }
+  const double L = (lam > 0.0) ? safety * lam : 1.0;
+  int k = 0;
+  bool converged = false;
+  while (k < max_inner) {
+    for (int i = tid; i < d; i += kCT) w[i] = y[i] - xs[i];
+    __syncthreads();
+    gemv_bcast(true, L);
+    const double *z = zb + par * d;
+    double n1 = 0.0, dummy = 0.0;
+    for (int i = tid; i < d; i += kCT) n1 += fabs(z[i]);
+    csum2(n1, dummy, red);
+    double theta = 0.0;
+    if (n1 > radius) {
+      theta = (n1 - radius) / (double)d;
+      double cprev = (double)d;
+      for (int guard = 0; guard <= d; ++guard) {
+        double S = 0.0, c = 0.0;
+        for (int i = tid; i < d; i += kCT) {
+          const double a = fabs(z[i]);
+          if (a > theta) {
+            S += a;
+            c += 1.0;
+          }
+        }
+        csum2(S, c, red);
+        if (c == cprev || c == 0.0) break;
+        theta = (S - radius) / c;
+        cprev = c;
+      }
+    }
+    double dn = 0.0, yy = 0.0;
+    for (int i = tid; i < d; i += kCT) {
+      const double zi = z[i];
+      double yn = zi;
+      if (n1 > radius) {
+        const double a = fabs(zi) - theta;
+        yn = a > 0.0 ? (zi < 0.0 ? -a : a) : 0.0;
+      }
+      const double e = yn - y[i];
+      dn = fma(e, e, dn);
+      yy = fma(y[i], y[i], yy);
+      w[i] = yn;  // staged: y is still read by other threads of this CTA above
+    }
+    csum2(dn, yy, red);
+    for (int i = tid; i < d; i += kCT) y[i] = w[i];
+    par ^= 1;
+    ++k;
+    if (sqrt(dn) <= tol * fmax(1.0, sqrt(yy))) {
+      converged = true;
+      break;
+    }
+    __syncthreads();
+  }
+  cluster.sync();  // no CTA may exit while others can still write into its shared memory
+  if (rank == 0) {
+    for (int i = tid; i < d; i += kCT) x_next[i] = y[i];
+    if (tid == 0) {
+      if (inner_iters) *inner_iters = k;
+      if (!converged) set_status(status, 4 /* IHS_ERR_NOT_CONVERGED */);
+    }
+  }
+}
+
 }  // namespace
 
-size_t pg_scratch_bytes(int64_t d) { return 0; }
+int pg_cluster_size(int64_t d) {
+  for (int cs : {1, 2, 4, 8, 16}) {
+    const int64_t R = (d + cs - 1) / cs;
+    if ((size_t)(R * d + 6 * d) * 8 <= 200 * 1024) return cs;
+  }
+  return 0;
+}
+
+bool pg_supported(int64_t d) { return pg_cluster_size(d) > 0 || (size_t)5 * d * 8 <= 200 * 1024; }
+
+size_t pg_scratch_bytes(int64_t) { return 0; }
 
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
                                  int max_inner, int power_iters, double tol, double safety, double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
                                  LaunchCounter lc) {
   (void)scratch;
+  static const bool use_cluster = !getenv("IHS_PG_SINGLE");
+  const int cs = use_cluster ? pg_cluster_size(d) : 0;
+  if (cs > 0) {
+    const int64_t R = (d + cs - 1) / cs;
+    const size_t smem = (size_t)(R * d + 6 * d) * 8;
+    IHS_SMEM_ATTR(pg_cluster_kernel, smem);
+    static bool nonportable = false;
+    if (cs > 8 && !nonportable) {
+      cudaFuncSetAttribute(pg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      nonportable = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kCT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    lc.add();
+    return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
+                              x_next, inner_iters, status);
+  }
   const size_t smem = (size_t)5 * d * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   IHS_SMEM_ATTR(pg_l1ball_kernel, smem);
