@@ -1,6 +1,6 @@
-// a2 (+ a5 fused) for dense CountSketch, TMA-fed: one CTA per bucket.  Thread 0
-// streams the bucket's rows (ascending, from the stable sort) into a 3-stage
-// shared-memory ring with 1-D bulk copies (cp.async.bulk -> UBLKCP), one per
+// a2 (+ a5 fused) for dense CountSketch, TMA-fed: one CTA per bucket.  A
+// producer warp streams the bucket's rows (ascending, from the stable sort)
+// into a shared-memory ring (~24 KiB in flight per CTA) with 1-D bulk copies (cp.async.bulk -> UBLKCP), one per
 // row, completing on an mbarrier per stage.  Each thread owns one column: it
 // adds sign*A[row, c] for the rows of a stage in ring order, i.e. the same
 // left-to-right fp64 sum as the oracle (SA bit-identical at P = 1).  With the
@@ -17,7 +17,8 @@ namespace ihs {
 
 namespace {
 constexpr int kScanTile = 4096;
-constexpr int kStages = 6;
+constexpr int kMaxStages = 8;
+constexpr int kRingBytes = 24 * 1024;  // bytes in flight per CTA (~168 KiB per SM at 7 CTAs)
 constexpr int kRows = 4;  // rows per stage
 
 __device__ __forceinline__ int32_t scanned_at(const int32_t *hist, const int32_t *tile_sums, int64_t e) {
@@ -58,23 +59,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // each warp transpose-reduces its partial dot products of the stage's 8 rows,
 // the two warp partials meet in shared memory behind a named barrier, and every
 // thread forms the same residual r_i = b_i - (p0 + p1).  Warp 2 produces: it
-// prefetches the next stage's perm entries and b values, waits until the slot
+// holds the perm entries and b values a window ahead, waits until the slot
 // is released (one arrival per consumer warp) and issues one bulk copy per row.
 constexpr int kConsumers = 64;
 constexpr int kCW = kConsumers / 32;
 template <bool FUSE, int NC>
-__global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
+__global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tma_kernel(
     const double *__restrict__ A, int64_t n, int d, int m, const int32_t *__restrict__ hist,
     const int32_t *__restrict__ tile_sums, int64_t nchunks, const uint32_t *__restrict__ perm,
     const double *__restrict__ bvec, const double *__restrict__ x, double *__restrict__ SA,
-    double *__restrict__ gpart, double scale) {
+    double *__restrict__ gpart, double scale, int kStages) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double *ring = reinterpret_cast<double *>(smem_raw);                                // [kStages][kRows][d]
   double *bs = ring + (size_t)kStages * kRows * d;                                    // [kStages][kRows]
   double *pd = bs + kStages * kRows;                                                  // [kStages][kCW][kRows]
   uint64_t *full = reinterpret_cast<uint64_t *>(pd + kStages * kCW * kRows);          // [kStages]
-  uint64_t *empty = full + kStages;                                                   // [kStages]
-  uint32_t *rid = reinterpret_cast<uint32_t *>(empty + kStages);                      // [kStages][kRows]
+  uint64_t *empty = full + kMaxStages;                                                // [kStages]
+  uint32_t *rid = reinterpret_cast<uint32_t *>(empty + kMaxStages);                   // [kStages][kRows]
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t beg = scanned_at(hist, tile_sums, (int64_t)b * nchunks);
@@ -94,33 +95,56 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
 
   if (warp == kCW) {
     // ---------------- producer warp
-    auto perm_of = [&](int64_t k) -> uint32_t {
-      const int64_t i = k * kRows + lane;
-      return (lane < kRows && k < nb && i < len) ? perm[beg + i] : 0u;
+    // The bucket's perm entries (and, fused, the b values they index) are
+    // loaded a 32-row window at a time, one entry per lane, two windows ahead
+    // for perm and one ahead for b (whose address depends on perm): neither
+    // dependent load sits on the per-stage path.  Each stage takes its kRows
+    // entries from the current window by shuffle.
+    constexpr int kWinStages = 32 / kRows;
+    const int64_t nwin = (len + 31) / 32;
+    auto perm_win = [&](int64_t w) -> uint32_t {
+      const int64_t i = w * 32 + lane;
+      return (w < nwin && i < len) ? perm[beg + i] : 0u;
     };
-    uint32_t e = perm_of(0);
-    double bv = (FUSE && lane < kRows && 0 < nb) ? bvec[e & 0x7fffffffu] : 0.0;
-    for (int64_t k = 0; k < nb; ++k) {
-      const int s = (int)(k % kStages);
-      const int cnt = (int)min((int64_t)kRows, len - k * kRows);
-      const uint32_t enext = perm_of(k + 1);  // in flight while we wait for the slot
-      double bnext = 0.0;
-      if (FUSE && lane < kRows && k + 1 < nb) bnext = bvec[enext & 0x7fffffffu];
-      if (k >= kStages) mbar_wait(&empty[s], (uint32_t)(((k / kStages) - 1) & 1));
-      if (lane < cnt) {
-        rid[s * kRows + lane] = e;
-        if (FUSE) bs[s * kRows + lane] = bv;
+    auto b_win = [&](int64_t w, uint32_t e) -> double {
+      return (FUSE && w < nwin && w * 32 + lane < len) ? bvec[e & 0x7fffffffu] : 0.0;
+    };
+    uint32_t p_cur = perm_win(0), p_next = perm_win(1);
+    int s = 0;
+    uint32_t ph = 0;
+    double b_cur = b_win(0, p_cur);
+    for (int64_t w = 0; w < nwin; ++w) {
+      const uint32_t p_nn = perm_win(w + 2);
+      const double b_next = b_win(w + 1, p_next);
+#pragma unroll 1
+      for (int ks = 0; ks < kWinStages; ++ks) {
+        const int64_t k = w * kWinStages + ks;
+        if (k >= nb) break;
+        const int cnt = (int)min((int64_t)kRows, len - k * kRows);
+        const int src = ks * kRows + (lane & (kRows - 1));
+        const uint32_t e = __shfl_sync(0xffffffffu, p_cur, src);
+        const double bv = FUSE ? __shfl_sync(0xffffffffu, b_cur, src) : 0.0;
+        if (k >= kStages) mbar_wait(&empty[s], ph ^ 1u);
+        if (lane < cnt) {
+          rid[s * kRows + lane] = e;
+          if (FUSE) bs[s * kRows + lane] = bv;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_expect_tx(&full[s], (uint32_t)cnt * row_bytes);
+        }
+        __syncwarp();
+        if (lane < cnt)
+          bulk_g2s(ring + ((size_t)s * kRows + lane) * d, A + (int64_t)(e & 0x7fffffffu) * d, row_bytes, &full[s]);
+        if (++s == kStages) {
+          s = 0;
+          ph ^= 1u;
+        }
       }
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&full[s], (uint32_t)cnt * row_bytes);
-      }
-      __syncwarp();
-      if (lane < cnt)
-        bulk_g2s(ring + ((size_t)s * kRows + lane) * d, A + (int64_t)(e & 0x7fffffffu) * d, row_bytes, &full[s]);
-      e = enext;
-      bv = bnext;
+      p_cur = p_next;
+      b_cur = b_next;
+      p_next = p_nn;
     }
     return;
   }
@@ -139,10 +163,11 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
   }
   const int myu = reduced_row_of_lane<kRows>(lane);
   const bool owner = owner_lane_of_row<kRows>(myu) == lane;
-  for (int64_t k = 0; k < nb; ++k) {
-    const int s = (int)(k % kStages);
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t k = 0; k < nb; ++k, s = (s + 1 == kStages) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u) {
     const int cnt = (int)min((int64_t)kRows, len - k * kRows);
-    mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
+    mbar_wait(&full[s], ph);
     const double *st = ring + (size_t)s * kRows * d;
     double a[kRows][NC];
 #pragma unroll
@@ -195,12 +220,12 @@ __global__ void __launch_bounds__(kConsumers + 32, 7) cs_gather_tma_kernel(
 }
 
 template <bool FUSE, int NC>
-void launch_tma_t(size_t smem, const double *A, int64_t n, int d, int m, const int32_t *hist, const int32_t *tile_sums,
-                  int64_t nchunks, const uint32_t *perm, const double *bvec, const double *x, double *SA,
-                  double *gpart, double scale, cudaStream_t st) {
+void launch_tma_t(size_t smem, int nst, const double *A, int64_t n, int d, int m, const int32_t *hist,
+                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec, const double *x,
+                  double *SA, double *gpart, double scale, cudaStream_t st) {
   IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC>), smem);
   cs_gather_tma_kernel<FUSE, NC><<<(unsigned)m, kConsumers + 32, smem, st>>>(A, n, d, m, hist, tile_sums, nchunks,
-                                                                              perm, bvec, x, SA, gpart, scale);
+                                                                              perm, bvec, x, SA, gpart, scale, nst);
 }
 }  // namespace
 
@@ -212,14 +237,16 @@ cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t 
                                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
                                  const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
                                  LaunchCounter lc) {
-  const size_t smem = (size_t)kStages * kRows * d * 8 + (size_t)kStages * kRows * 8 * (1 + kCW) + 2 * kStages * 8 +
-                      kStages * kRows * 4 + 64;
+  // ring depth: ~kRingBytes of rows in flight per CTA, 2..kMaxStages stages
+  const int nst = (int)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, kRingBytes / (kRows * d * 8)));
+  const size_t smem = (size_t)nst * kRows * d * 8 + (size_t)nst * kRows * 8 * (1 + kCW) + 2 * kMaxStages * 8 +
+                      kMaxStages * kRows * 4 + 64;
   const int nc = (int)((d + kConsumers - 1) / kConsumers);
   const bool f = gpart != nullptr;
 #define IHS_TMA(NC)                                                                                           \
-  (f ? launch_tma_t<true, NC>(smem, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart,   \
+  (f ? launch_tma_t<true, NC>(smem, nst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart,   \
                               scale, st)                                                                     \
-     : launch_tma_t<false, NC>(smem, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, nullptr, nullptr, SA,   \
+     : launch_tma_t<false, NC>(smem, nst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, nullptr, nullptr, SA,   \
                                nullptr, scale, st))
   if (nc <= 1) IHS_TMA(1);
   else if (nc == 2) IHS_TMA(2);

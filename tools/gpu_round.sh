@@ -1,0 +1,52 @@
+#!/bin/bash
+# One gpurun call: GPU tests, bench on every config, ncu launch list and one
+# `ncu --set full` capture per dominant kernel.  Outputs under gpurun_out/$TAG/.
+# usage: gpurun -- 'bash tools/gpu_round.sh TAG [parts...]'   parts: tests smoke bench ncu probe
+TAG=${1:-r01}
+shift
+PARTS=${*:-"probe tests smoke bench ncu"}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi > $OUT/nvidia-smi.txt 2>&1
+has() { [[ " $PARTS " == *" $1 "* ]]; }
+if has probe; then
+  nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/probe tools/probe/probe.cu > $OUT/probe_build.txt 2>&1 &&
+    timeout 300 /tmp/probe > $OUT/probe.txt 2>&1
+fi
+if has tests; then
+  timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $OUT/pytest_gpu.txt 2>&1
+  echo "pytest exit $?" >> $OUT/pytest_gpu.txt
+fi
+if has smoke; then
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1
+  echo "smoke exit $?" >> $OUT/smoke.txt
+fi
+if has bench; then
+  timeout 900 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
+  for C in C1 C3 C4 C5; do
+    timeout 600 python bench.py --config $C --steps 10 --warmup 3 --no-cpu > $OUT/bench_$C.json 2> $OUT/bench_$C.err
+  done
+  timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
+fi
+if has ncu; then
+  NCU=/usr/local/cuda/bin/ncu
+  for C in C2 C3 C4 C5; do
+    timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $OUT/launches_$C.csv python bench.py --config $C --steps 3 --warmup 3 --no-e2e --no-cpu --no-ttt \
+      > $OUT/ncu_launch_$C.log 2>&1
+  done
+  # one full capture of each dominant kernel (launch-skip past the warm-up)
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cs_gather_tma -s 3 -c 1 \
+    -o $OUT/full_C2_gather -f python bench.py --config C2 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt \
+    > $OUT/ncu_full_C2.log 2>&1
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:sjlt -s 3 -c 1 \
+    -o $OUT/full_C5_sjlt -f python bench.py --config C5 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt \
+    > $OUT/ncu_full_C5.log 2>&1
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"gram_kernel|csr_sketch|potrf|syrk" -s 12 -c 6 \
+    -o $OUT/full_C3 -f python bench.py --config C3 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt \
+    > $OUT/ncu_full_C3.log 2>&1
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"pg_l1ball|cs_gather_tma" -s 6 -c 2 \
+    -o $OUT/full_C4 -f python bench.py --config C4 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt \
+    > $OUT/ncu_full_C4.log 2>&1
+fi
+ls -la $OUT
