@@ -209,50 +209,75 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
     if (SA && s > 1) IHS_CUDA(launch_scale(SA, m * d, spec_scale(spec), st, lc_of(c)));
     return IHS_OK;
   }
-  // dense.  CountSketch (s = 1) and SJLT (s > 1): per block j of m/s buckets, a
-  // stable counting sort of the rows by bucket and one bucket-ordered gather
-  // (SJLT = s stacked independent CountSketches).  The
-  // gradient rides on block 0's read of A.  IHS_SJLT=tile selects the
-  // single-pass shared-memory tile kernel instead (s > 1).
+  // dense.  CountSketch (s = 1): a stable counting sort of the rows by bucket
+  // and one bucket-ordered gather, with the gradient riding on the same read
+  // of A.  SJLT (s > 1): the same per block j (s stacked
+  // CountSketches; s reads of A, bit-identical to the oracle).  IHS_SJLT=stream
+  // selects one streaming pass of shared-memory tiles over A (sjlt_stream.cu,
+  // plus a separate gradient pass), IHS_SJLT=tile the older per-CTA tile
+  // kernel; both measured slower on B200.
   const int64_t M = m / s;
-  static const bool sjlt_tile = getenv("IHS_SJLT") && !std::strcmp(getenv("IHS_SJLT"), "tile");
-  const bool use_sort = cs_sort_supported(M) && !(s > 1 && sjlt_tile);
+  static const char *sjlt_env = getenv("IHS_SJLT");
+  static const int sjlt_mode = !sjlt_env ? 1 : !std::strcmp(sjlt_env, "stream") ? 0 : !std::strcmp(sjlt_env, "tile") ? 2 : 1;
+  SjltPlan sp;
+  const bool use_stream = s > 1 && sjlt_mode == 0 && sjlt_stream_plan(n, d, m, s, c->num_sms, sp);
+  const bool use_sort = cs_sort_supported(M) && !use_stream && !(s > 1 && sjlt_mode == 2);
   const bool fuse = SA && use_sort && g && d <= 256;
   if (SA) {
     if (use_sort) {
       CsSortPlan p = cs_sort_plan(n, M);
+      // SJLT blocks are gathered nb at a time (one launch, grid.y = block) so
+      // that a launch has about one wave of bucket CTAs (7 per SM) even when
+      // M = m / s is small; each block of a batch has its own sort buffers.
+      const bool tma = c->gather == 1 && cs_gather_tma_supported(d, A->values);
+      const int nb = tma ? (int)std::max<int64_t>(1, std::min<int64_t>(s, (7 * (int64_t)c->num_sms) / std::max<int64_t>(M, 1)))
+                         : 1;
+      const int64_t hs = (int64_t)(p.hist_bytes() / 4 + 63) / 64 * 64, ts = (int64_t)(p.tiles_bytes() / 4 + 63) / 64 * 64;
+      const int64_t ps = (p.n + 63) / 64 * 64;
       int32_t *hist, *tiles;
       uint32_t *perm;
-      IHS_TRY(scratch(c, S_HIST, p.hist_bytes(), &hist));
-      IHS_TRY(scratch(c, S_TILES, p.tiles_bytes(), &tiles));
-      IHS_TRY(scratch(c, S_PERM, p.perm_bytes(), &perm));
+      IHS_TRY(scratch(c, S_HIST, (size_t)hs * 4 * nb, &hist));
+      IHS_TRY(scratch(c, S_TILES, (size_t)ts * 4 * nb, &tiles));
+      IHS_TRY(scratch(c, S_PERM, (size_t)std::max<int64_t>(ps, 1) * 4 * nb, &perm));
       double *gpart = nullptr;
       if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)M * d * 8, &gpart));
       const double scale = spec_scale(spec);
-      for (int j = 0; j < s; ++j) {
-        double *SAj = SA + (int64_t)j * M * d;
-        double *gp = (j == 0) ? gpart : nullptr;
+      for (int j0 = 0; j0 < s; j0 += nb) {
+        const int cnt = std::min(nb, s - j0);
         {
           Prof pr(c, IHS_K_SORT);
-          IHS_CUDA(launch_cs_sort(p, key, A->row_offset, (uint32_t)j, (uint32_t)s, hist, tiles, perm, st, lc_of(c)));
+          for (int jj = 0; jj < cnt; ++jj)
+            IHS_CUDA(launch_cs_sort(p, key, A->row_offset, (uint32_t)(j0 + jj), (uint32_t)s, hist + jj * hs,
+                                    tiles + jj * ts, perm + jj * ps, st, lc_of(c)));
         }
-        {
-          Prof pr(c, IHS_K_SKETCH);
-          if (c->gather == 1 && cs_gather_tma_supported(d, A->values))
-            IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale, st,
-                                          lc_of(c)));
-          else if (c->gather == 2 && cs_gather_async_supported(d, A->values))
-            IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale,
-                                            st, lc_of(c)));
-          else
-            IHS_CUDA(launch_cs_gather(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale, st,
-                                      lc_of(c)));
+        double *SAj = SA + (int64_t)j0 * M * d;
+        double *gp = (j0 == 0) ? gpart : nullptr;
+        Prof pr(c, IHS_K_SKETCH);
+        if (tma) {
+          GatherBatchStrides bst;
+          bst.hist = hs;
+          bst.tiles = ts;
+          bst.perm = ps;
+          bst.sa = M * d;
+          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale, st,
+                                        lc_of(c), cnt, bst));
+        } else if (c->gather == 2 && cs_gather_async_supported(d, A->values)) {
+          IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale,
+                                          st, lc_of(c)));
+        } else {
+          IHS_CUDA(launch_cs_gather(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale, st,
+                                    lc_of(c)));
         }
       }
       if (fuse) {
         Prof pr(c, IHS_K_REDUCE);
         IHS_CUDA(launch_reduce_rows(gpart, M, d, g, st, lc_of(c)));
       }
+    } else if (use_stream) {
+      double *part;
+      IHS_TRY(scratch(c, S_SJLT, sp.partial_bytes(), &part));
+      Prof pr(c, IHS_K_SJLT);
+      IHS_CUDA(launch_sjlt_stream(sp, A->values, key, A->row_offset, part, SA, spec_scale(spec), st, lc_of(c)));
     } else {
       SjltPlan p;
       if (!sjlt_plan(n, d, m, s, c->num_sms, p)) return IHS_ERR_UNSUPPORTED;

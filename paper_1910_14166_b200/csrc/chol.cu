@@ -5,8 +5,8 @@
 // R13) and x_next = x.  Latency-bound: O(d) dependent column steps.
 #include "common.cuh"
 #include "kernels.h"
+#include "chol_blocks.cuh"
 
-#include <utility>
 
 namespace ihs {
 
@@ -14,14 +14,15 @@ namespace {
 // ----------------------------------------------------------------------------
 // Blocked right-looking Cholesky in one CTA for D = ceil(d/32)*32 <= 160 (the
 // matrix is padded with an identity block).  Per 32-column block kb:
-//   1. warp 0 factors the 32x32 diagonal block in registers (lane i holds row
-//      i; one shuffle broadcasts each column), storing L11 and 1/L_jj;
-//   2. the rows below solve X L11^T = A21 (one thread per row, L11 broadcast
-//      from shared memory);
+//   1. warp 0 factors the 32x32 diagonal block in registers (warp_chol32:
+//      lane i holds row i; one shuffle broadcasts each column), storing L11
+//      and 1/L_jj;
+//   2. the rows below solve X L11^T = A21 (thread_trsm32: one thread per row,
+//      L11 broadcast from shared memory);
 //   3. the trailing lower triangle is updated A22 -= L21 L21^T on the DMMA pipe
 //      (mma.sync m8n8k4 f64, 8x8 tiles spread over the 16 warps).
-// Then warp 0 runs both triangular solves with the right-hand side in
-// registers.  Leading dimension D + 4 (== 4 mod 16 doubles) keeps the DMMA
+// g rides along as an augmented row (the forward solve comes out of the
+// factorisation); then warp 0 runs the backward solve in registers.  Leading dimension D + 4 (== 4 mod 16 doubles) keeps the DMMA
 // fragment loads conflict-free.
 __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -30,109 +31,75 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
 }
 
 
-// Compile-time unrolled column steps (template recursion keeps row[] in registers).
-template <int J>
-__device__ __forceinline__ void diag_step(double (&row)[32], int lane, bool &bad, double *rd) {
-  const double piv = __shfl_sync(0xffffffffu, row[J], J);
-  bad |= !(piv > 0.0);
-  const double sq = sqrt(piv);
-  const double r = 1.0 / sq;
-  const double lij = (lane > J) ? row[J] * r : (lane == J ? sq : 0.0);
-  row[J] = lij;
-  if (lane == 0) rd[J] = r;
-#pragma unroll
-  for (int k = J + 1; k < 32; ++k) {
-    const double lkj = __shfl_sync(0xffffffffu, lij, k);
-    if (lane >= k) row[k] -= lij * lkj;
-  }
-}
-template <int... Js>
-__device__ __forceinline__ void diag_steps(double (&row)[32], int lane, bool &bad, double *rd,
-                                           std::integer_sequence<int, Js...>) {
-  (diag_step<Js>(row, lane, bad, rd), ...);
-}
-template <int J>
-__device__ __forceinline__ void trsm_step(double (&xr)[32], const double *rd, const double *L11, int lda) {
-  const double xj = xr[J] * rd[J];
-  xr[J] = xj;
-#pragma unroll
-  for (int k = J + 1; k < 32; ++k) xr[k] -= xj * L11[k * lda + J];
-}
-template <int... Js>
-__device__ __forceinline__ void trsm_steps(double (&xr)[32], const double *rd, const double *L11, int lda,
-                                           std::integer_sequence<int, Js...>) {
-  (trsm_step<Js>(xr, rd, L11, lda), ...);
-}
-
 constexpr int kBThreads = 256;
+// The right-hand side rides along as row D of an augmented matrix [[H, 0], [g^T, 0]]
+// (rows D+1..D+7 are zero so the DMMA trailing update keeps whole 8-row tiles):
+// the panel TRSM and the trailing updates turn row D into y = L^{-1} g, so only
+// the backward solve L^T u = y runs after the factorisation.
 template <int NBLK>
 __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *__restrict__ H,
                                                                 const double *__restrict__ g, int d,
                                                                 const double *__restrict__ x, double *x_next,
                                                                 int *status) {
   constexpr int D = 32 * NBLK;
+  constexpr int DA = D + 8;  // rows incl. the augmented g row and its zero tile padding
   constexpr int lda = D + 4;
   extern __shared__ double sm[];
-  double *Ls = sm;               // D x lda
-  double *rdiag = sm + D * lda;  // D
+  double *Ls = sm;                // DA x lda
+  double *rdiag = sm + DA * lda;  // D
   __shared__ int s_bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = warp; i < D; i += kBThreads / 32)
-    for (int c = lane; c <= i; c += 32)
-      Ls[i * lda + c] = (i < d) ? H[(int64_t)i * d + c] : (c == i ? 1.0 : 0.0);
+  for (int i = warp; i < DA; i += kBThreads / 32) {
+    if (i < D) {
+      for (int c = lane; c <= i; c += 32) Ls[i * lda + c] = (i < d) ? H[(int64_t)i * d + c] : (c == i ? 1.0 : 0.0);
+    } else {
+      for (int c = lane; c < D; c += 32) Ls[i * lda + c] = (i == D && c < d) ? g[c] : 0.0;
+    }
+  }
   if (tid == 0) s_bad = 0;
   __syncthreads();
 #pragma unroll 1
   for (int kb = 0; kb < D; kb += 32) {
     // 1. diagonal block
     if (warp == 0) {
-      double row[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) row[c] = (c <= lane) ? Ls[(kb + lane) * lda + kb + c] : 0.0;
-      bool bad = false;
-      diag_steps(row, lane, bad, rdiag + kb, std::make_integer_sequence<int, 32>{});
+      const bool bad = warp_chol32(Ls + kb * lda + kb, lda, rdiag + kb, 32);
       if (bad && lane == 0) s_bad = 1;
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (c <= lane) Ls[(kb + lane) * lda + kb + c] = row[c];
     }
     __syncthreads();
     if (s_bad) break;
-    // 2. panel: rows below solve X L11^T = A21
+    // 2. panel: rows below (incl. the g row) solve X L11^T = A21
     const int nbelow = D - kb - 32;
-    if (tid < nbelow) {
-      const int i = kb + 32 + tid;
-      double xr[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) xr[c] = Ls[i * lda + kb + c];
-      trsm_steps(xr, rdiag + kb, Ls + kb * lda + kb, lda, std::make_integer_sequence<int, 32>{});
-#pragma unroll
-      for (int c = 0; c < 32; ++c) Ls[i * lda + kb + c] = xr[c];
-    }
+    if (tid < nbelow + 8) thread_trsm32(Ls + (kb + 32 + tid) * lda + kb, Ls + kb * lda + kb, lda, rdiag + kb);
     __syncthreads();
-    // 3. trailing update A22 -= L21 L21^T (lower 8x8 tiles on DMMA)
-    if (nbelow > 0) {
-      const int nt = nbelow / 8;
-      const int ntri = nt * (nt + 1) / 2;
-      for (int t = warp; t < ntri; t += kBThreads / 32) {
-        int ti = 0, rem = t;  // row-major enumeration of {(ti, tj): tj <= ti}
+    // 3. trailing update A22 -= L21 L21^T (lower 8x8 tiles on DMMA), plus the
+    //    g-row tile against every trailing column tile
+    const int nt = nbelow / 8;
+    const int ntri = nt * (nt + 1) / 2;
+    for (int t = warp; t < ntri + nt; t += kBThreads / 32) {
+      int ti, tj;
+      if (t < ntri) {
+        ti = 0;
+        int rem = t;  // row-major enumeration of {(ti, tj): tj <= ti}
         while (rem > ti) {
           rem -= ti + 1;
           ++ti;
         }
-        const int tj = rem;
-        const int I = kb + 32 + 8 * ti, J = kb + 32 + 8 * tj;
-        double c0 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 32; kk += 4) {
-          const double a = Ls[(I + (lane >> 2)) * lda + kb + kk + (lane & 3)];
-          const double b = Ls[(J + (lane >> 2)) * lda + kb + kk + (lane & 3)];
-          dmma884(c0, c1, a, b);
-        }
-        const int r = I + (lane >> 2), c = J + 2 * (lane & 3);
-        Ls[r * lda + c] -= c0;
-        Ls[r * lda + c + 1] -= c1;
+        tj = rem;
+      } else {
+        ti = nt;
+        tj = t - ntri;
       }
+      const int I = kb + 32 + 8 * ti, J = kb + 32 + 8 * tj;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < 32; kk += 4) {
+        const double a = Ls[(I + (lane >> 2)) * lda + kb + kk + (lane & 3)];
+        const double b = Ls[(J + (lane >> 2)) * lda + kb + kk + (lane & 3)];
+        dmma884(c0, c1, a, b);
+      }
+      const int r = I + (lane >> 2), c = J + 2 * (lane & 3);
+      Ls[r * lda + c] -= c0;
+      Ls[r * lda + c + 1] -= c1;
     }
     __syncthreads();
   }
@@ -142,28 +109,10 @@ __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *_
     return;
   }
   if (warp == 0) {
+    // backward: L^T u = y, y = row D
     double z[NBLK];
 #pragma unroll
-    for (int s = 0; s < NBLK; ++s) {
-      const int i = lane + 32 * s;
-      z[s] = i < d ? g[i] : 0.0;
-    }
-    // forward: L y = g
-#pragma unroll
-    for (int s = 0; s < NBLK; ++s) {
-#pragma unroll 4
-      for (int jj = 0; jj < 32; ++jj) {
-        const int j = 32 * s + jj;
-        const double yj = __shfl_sync(0xffffffffu, z[s], jj) * rdiag[j];
-        if (lane == jj) z[s] = yj;
-#pragma unroll
-        for (int q = s; q < NBLK; ++q) {
-          const int i = lane + 32 * q;
-          if (i > j) z[q] -= Ls[i * lda + j] * yj;
-        }
-      }
-    }
-    // backward: L^T u = y
+    for (int s = 0; s < NBLK; ++s) z[s] = Ls[D * lda + lane + 32 * s];
 #pragma unroll
     for (int s = NBLK - 1; s >= 0; --s) {
 #pragma unroll 4
@@ -190,7 +139,7 @@ template <int NBLK>
 void launch_blocked(const double *H, const double *g, int d, const double *x, double *x_next, int *status,
                     cudaStream_t st) {
   constexpr int D = 32 * NBLK;
-  const size_t smem = ((size_t)D * (D + 4) + D) * 8;
+  const size_t smem = ((size_t)(D + 8) * (D + 4) + D) * 8;
   IHS_SMEM_ATTR((chol_blocked_kernel<NBLK>), smem);
   chol_blocked_kernel<NBLK><<<1, kBThreads, smem, st>>>(H, g, d, x, x_next, status);
 }

@@ -7,10 +7,9 @@
 //   syrk   (n CTAs)  trailing lower 64x64 tiles -= L21 L21^T on the DMMA pipe.
 // Then one CTA runs the blocked back substitution L^T u = y and x + u.
 // Eq. (2) with C = R^d; T_solve = O(d^3).
-#include <utility>
-
 #include "common.cuh"
 #include "kernels.h"
+#include "chol_blocks.cuh"
 
 namespace ihs {
 
@@ -22,41 +21,6 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
-}
-
-// 32x32 diagonal block in registers (lane i holds row i); pivots of rows
-// >= jcheck (the augmented row and the identity padding) are not checked.
-template <int J>
-__device__ __forceinline__ void dstep(double (&row)[32], int lane, bool &bad, double *rd, int jcheck) {
-  const double piv = __shfl_sync(0xffffffffu, row[J], J);
-  bad |= (J < jcheck) && !(piv > 0.0);
-  const double sq = sqrt(piv);
-  const double r = 1.0 / sq;
-  const double lij = (lane > J) ? row[J] * r : (lane == J ? sq : 0.0);
-  row[J] = lij;
-  if (lane == 0) rd[J] = r;
-#pragma unroll
-  for (int k = J + 1; k < 32; ++k) {
-    const double lkj = __shfl_sync(0xffffffffu, lij, k);
-    if (lane >= k) row[k] -= lij * lkj;
-  }
-}
-template <int... Js>
-__device__ __forceinline__ void dsteps(double (&row)[32], int lane, bool &bad, double *rd, int jcheck,
-                                       std::integer_sequence<int, Js...>) {
-  (dstep<Js>(row, lane, bad, rd, jcheck), ...);
-}
-template <int N, int J>
-__device__ __forceinline__ void tstep(double (&xr)[N], const double *rd, const double *L11, int lda) {
-  const double xj = xr[J] * rd[J];
-  xr[J] = xj;
-#pragma unroll
-  for (int k = J + 1; k < N; ++k) xr[k] -= xj * L11[k * lda + J];
-}
-template <int N, int... Js>
-__device__ __forceinline__ void tsteps(double (&xr)[N], const double *rd, const double *L11, int lda,
-                                       std::integer_sequence<int, Js...>) {
-  (tstep<N, Js>(xr, rd, L11, lda), ...);
 }
 
 __global__ void aug_fill_kernel(const double *__restrict__ H, const double *__restrict__ g, int d, int Dp,
@@ -89,27 +53,13 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double *__restrict__ M,
   __syncthreads();
   for (int k2 = 0; k2 < PB; k2 += 32) {
     if (warp == 0) {
-      double row[32];
-#pragma unroll
-      for (int c = 0; c < 32; ++c) row[c] = (c <= lane) ? Ls[(k2 + lane) * LDP + k2 + c] : 0.0;
-      bool bad = false;
-      dsteps(row, lane, bad, rd + k2, d - (kb + k2), std::make_integer_sequence<int, 32>{});
+      const bool bad = warp_chol32(Ls + k2 * LDP + k2, LDP, rd + k2, d - (kb + k2));
       if (bad && lane == 0) s_bad = 1;
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        if (c <= lane) Ls[(k2 + lane) * LDP + k2 + c] = row[c];
     }
     __syncthreads();
     if (s_bad) break;
     if (k2 == 0) {
-      if (tid < 32) {  // rows 32..63 solve against the first 32x32 block
-        double xr[32];
-#pragma unroll
-        for (int c = 0; c < 32; ++c) xr[c] = Ls[(32 + tid) * LDP + c];
-        tsteps<32>(xr, rd, Ls, LDP, std::make_integer_sequence<int, 32>{});
-#pragma unroll
-        for (int c = 0; c < 32; ++c) Ls[(32 + tid) * LDP + c] = xr[c];
-      }
+      if (tid < 32) thread_trsm32(Ls + (32 + tid) * LDP, Ls, LDP, rd);  // rows 32..63 against the first block
       __syncthreads();
       // lower 8x8 tiles of the (32,32) block -= L21 L21^T
       for (int t = warp; t < 10; t += 8) {
@@ -142,27 +92,51 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double *__restrict__ M,
   if (tid < PB) rdiag[kb + tid] = rd[tid];
 }
 
-// Rows below the panel: X L11^T = A21 (one thread per row, 64 columns in registers).
-__global__ void __launch_bounds__(128) trsm_panel_kernel(double *__restrict__ M, int Dp, int kb,
-                                                         const double *__restrict__ rdiag, const int *flag) {
-  __shared__ double L11[PB * (PB + 1)];
-  __shared__ double rd[PB];
+// Rows below the panel: X L11^T = A21, one thread per row.  With L11 =
+// [[P, 0], [Q, R]] (32x32 blocks): x1 P^T = a1, then x2 R^T = a2 - x1 Q^T.
+// Each thread stages its 64-wide row in shared memory (stride 65: conflict-free
+// across threads); L11 is read as broadcasts.
+constexpr int kTrsmThreads = 128;
+__global__ void __launch_bounds__(kTrsmThreads) trsm_panel_kernel(double *__restrict__ M, int Dp, int kb,
+                                                                  const double *__restrict__ rdiag, const int *flag) {
+  extern __shared__ double tsm[];
+  double *L11 = tsm;                  // PB x (PB + 1)
+  double *X = L11 + PB * (PB + 1);    // kTrsmThreads x (PB + 1)
+  double *rd = X + kTrsmThreads * (PB + 1);
   if (*flag) return;
   for (int e = threadIdx.x; e < PB * PB; e += blockDim.x) {
     const int i = e / PB, c = e % PB;
     L11[i * (PB + 1) + c] = (c <= i) ? M[(int64_t)(kb + i) * Dp + kb + c] : 0.0;
   }
   if (threadIdx.x < PB) rd[threadIdx.x] = rdiag[kb + threadIdx.x];
+  const int r0 = kb + PB + blockIdx.x * blockDim.x;
+  const int nr = min((int)blockDim.x, Dp - r0);
+  for (int e = threadIdx.x; e < nr * PB; e += blockDim.x) {  // coalesced: consecutive threads, consecutive columns
+    const int r = e / PB, c = e % PB;
+    X[r * (PB + 1) + c] = M[(int64_t)(r0 + r) * Dp + kb + c];
+  }
   __syncthreads();
-  const int i = kb + PB + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= Dp) return;
-  double *row = M + (int64_t)i * Dp + kb;
-  double xr[PB];
+  double *x = X + threadIdx.x * (PB + 1);
+  if (threadIdx.x < nr) {
+    thread_trsm32(x, L11, PB + 1, rd);
+    const double *Q = L11 + 32 * (PB + 1);
+#pragma unroll 1
+    for (int c = 0; c < 32; ++c) {
+      double t0 = 0.0, t1 = 0.0;
 #pragma unroll
-  for (int c = 0; c < PB; ++c) xr[c] = row[c];
-  tsteps<PB>(xr, rd, L11, PB + 1, std::make_integer_sequence<int, PB>{});
-#pragma unroll
-  for (int c = 0; c < PB; ++c) row[c] = xr[c];
+      for (int k = 0; k < 32; k += 2) {
+        t0 = fma(x[k], Q[c * (PB + 1) + k], t0);
+        t1 = fma(x[k + 1], Q[c * (PB + 1) + k + 1], t1);
+      }
+      x[32 + c] -= t0 + t1;
+    }
+    thread_trsm32(x + 32, L11 + 32 * (PB + 1) + 32, PB + 1, rd + 32);
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nr * PB; e += blockDim.x) {
+    const int r = e / PB, c = e % PB;
+    M[(int64_t)(r0 + r) * Dp + kb + c] = X[r * (PB + 1) + c];
+  }
 }
 
 // Trailing update of the lower 64x64 tiles: C_IJ -= P_I P_J^T with P = the
@@ -262,10 +236,22 @@ __global__ void __launch_bounds__(1024) backsolve_kernel(const double *__restric
       if (lane + 32 < w) z[kb + lane + 32] = zr[1];
     }
     __syncthreads();
+    // z[k] -= sum_i L[kb+i][k] u[kb+i] for k < kb: coalesced rows of L from L2,
+    // 16 independent loads in flight per thread (rows >= w of the block are the
+    // identity padding / zero and never read: w == PB except for the top block)
     for (int k = tid; k < kb; k += blockDim.x) {
-      double t = z[k];
-      for (int i = 0; i < w; ++i) t -= M[(int64_t)(kb + i) * Dp + k] * z[kb + i];
-      z[k] = t;
+      const double *col = M + (int64_t)kb * Dp + k;
+      double t0 = 0.0, t1 = 0.0;
+      if (w == PB) {
+#pragma unroll 16
+        for (int i = 0; i < PB; i += 2) {
+          t0 = fma(col[(int64_t)i * Dp], z[kb + i], t0);
+          t1 = fma(col[(int64_t)(i + 1) * Dp], z[kb + i + 1], t1);
+        }
+      } else {
+        for (int i = 0; i < w; ++i) t0 = fma(col[(int64_t)i * Dp], z[kb + i], t0);
+      }
+      z[k] -= t0 + t1;
     }
     __syncthreads();
   }
@@ -290,12 +276,14 @@ cudaError_t launch_chol_large(const double *H, const double *g, int64_t d, const
   int launches = 1;
   const size_t syrk_smem = (size_t)2 * PB * LDP * 8;
   IHS_SMEM_ATTR(syrk_panel_kernel, syrk_smem);
+  const size_t trsm_smem = ((size_t)(PB + kTrsmThreads) * (PB + 1) + PB) * 8;
+  IHS_SMEM_ATTR(trsm_panel_kernel, trsm_smem);
   for (int kb = 0; kb < Dp; kb += PB) {
     potrf_diag_kernel<<<1, 256, 0, st>>>(M, Dp, kb, (int)d, rdiag, flag, status);
     const int below = Dp - kb - PB;
     ++launches;
     if (below > 0) {
-      trsm_panel_kernel<<<(below + 127) / 128, 128, 0, st>>>(M, Dp, kb, rdiag, flag);
+      trsm_panel_kernel<<<(below + kTrsmThreads - 1) / kTrsmThreads, kTrsmThreads, trsm_smem, st>>>(M, Dp, kb, rdiag, flag);
       const int nt = below / PB;
       syrk_panel_kernel<<<nt * (nt + 1) / 2, 128, syrk_smem, st>>>(M, Dp, kb, flag);
       launches += 2;

@@ -48,6 +48,20 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Lanes of the warp whose key equals this lane's key (a match_any built from
+// one ballot per key bit: MATCH.ANY is a long-latency instruction on sm_100a).
+// key < 2^nbits; lanes with valid == false form their own group.
+__device__ __forceinline__ unsigned peers_by_ballot(uint32_t key, int nbits, bool valid) {
+  const unsigned vm = __ballot_sync(0xffffffffu, valid);
+  unsigned peers = valid ? vm : ~vm;
+#pragma unroll 4
+  for (int k = 0; k < nbits; ++k) {
+    const unsigned bk = __ballot_sync(0xffffffffu, (key >> k) & 1u);
+    peers &= ((key >> k) & 1u) ? bk : ~bk;
+  }
+  return peers;
+}
+
 // Transpose-reduce U per-lane partial sums (one per row) across the warp in
 // U-1 + log2(32/U) shuffles instead of U*5.  On return p[0] holds the full sum
 // for row reduced_row_of_lane<U>(lane).
@@ -84,6 +98,14 @@ __device__ __forceinline__ int owner_lane_of_row(int u) {
   for (int w = U / 2; w >= 1; w >>= 1, sh >>= 1)
     if (u & w) lane |= sh;
   return lane;
+}
+
+// Cholesky pivot: r = 1/sqrt(piv) (one MUFU.RSQ64H + Newton, <= 1 ulp) and
+// L_jj = piv * r, instead of an IEEE sqrt followed by an IEEE division: both
+// sit on the factorisation's sequential critical path.
+__device__ __forceinline__ void pivot_rsqrt(double piv, double &ljj, double &r) {
+  r = rsqrt(piv);
+  ljj = piv * r;
 }
 
 // Device-side status word (first error wins).

@@ -63,13 +63,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // is released (one arrival per consumer warp) and issues one bulk copy per row.
 constexpr int kConsumers = 64;
 constexpr int kCW = kConsumers / 32;
-template <bool FUSE, int NC>
+template <bool FUSE, int NC, bool SOLO>
 __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tma_kernel(
     const double *__restrict__ A, int64_t n, int d, int m, const int32_t *__restrict__ hist,
     const int32_t *__restrict__ tile_sums, int64_t nchunks, const uint32_t *__restrict__ perm,
     const double *__restrict__ bvec, const double *__restrict__ x, double *__restrict__ SA,
-    double *__restrict__ gpart, double scale, int kStages) {
+    double *__restrict__ gpart, double scale, int kStages, GatherBatchStrides bst) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  // blockIdx.y selects one SJLT block of a batch (its own sort and SA rows);
+  // the gradient rides on batch entry 0 only
+  hist += blockIdx.y * bst.hist;
+  tile_sums += blockIdx.y * bst.tiles;
+  perm += blockIdx.y * bst.perm;
+  SA += blockIdx.y * bst.sa;
+  const bool fz = FUSE && (SOLO || blockIdx.y == 0);  // SOLO: a one-entry batch (compile-time)
   double *ring = reinterpret_cast<double *>(smem_raw);                                // [kStages][kRows][d]
   double *bs = ring + (size_t)kStages * kRows * d;                                    // [kStages][kRows]
   double *pd = bs + kStages * kRows;                                                  // [kStages][kCW][kRows]
@@ -107,7 +114,7 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
       return (w < nwin && i < len) ? perm[beg + i] : 0u;
     };
     auto b_win = [&](int64_t w, uint32_t e) -> double {
-      return (FUSE && w < nwin && w * 32 + lane < len) ? bvec[e & 0x7fffffffu] : 0.0;
+      return (fz && w < nwin && w * 32 + lane < len) ? bvec[e & 0x7fffffffu] : 0.0;
     };
     uint32_t p_cur = perm_win(0), p_next = perm_win(1);
     int s = 0;
@@ -123,11 +130,11 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
         const int cnt = (int)min((int64_t)kRows, len - k * kRows);
         const int src = ks * kRows + (lane & (kRows - 1));
         const uint32_t e = __shfl_sync(0xffffffffu, p_cur, src);
-        const double bv = FUSE ? __shfl_sync(0xffffffffu, b_cur, src) : 0.0;
+        const double bv = fz ? __shfl_sync(0xffffffffu, b_cur, src) : 0.0;
         if (k >= kStages) mbar_wait(&empty[s], ph ^ 1u);
         if (lane < cnt) {
           rid[s * kRows + lane] = e;
-          if (FUSE) bs[s * kRows + lane] = bv;
+          if (fz) bs[s * kRows + lane] = bv;
         }
         __syncwarp();
         if (lane == 0) {
@@ -159,7 +166,7 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
     cc[q] = cv[q] ? c : d - 1;
     acc[q] = 0.0;
     gac[q] = 0.0;
-    xv[q] = (FUSE && cv[q]) ? x[c] : 0.0;
+    xv[q] = (fz && cv[q]) ? x[c] : 0.0;
   }
   const int myu = reduced_row_of_lane<kRows>(lane);
   const bool owner = owner_lane_of_row<kRows>(myu) == lane;
@@ -177,7 +184,9 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
       for (int q = 0; q < NC; ++q) a[r][q] = st[(size_t)rr * d + cc[q]];
     }
     double res[kRows];
-    if constexpr (FUSE) {
+#pragma unroll
+    for (int r = 0; r < kRows; ++r) res[r] = 0.0;
+    if (fz) {
       double p[kRows];
 #pragma unroll
       for (int r = 0; r < kRows; ++r) {
@@ -203,7 +212,7 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
           acc[q] += neg ? -a[r][q] : a[r][q];
-          if constexpr (FUSE) gac[q] = fma(res[r], a[r][q], gac[q]);
+          if (fz) gac[q] = fma(res[r], a[r][q], gac[q]);
         }
       }
     }
@@ -214,18 +223,24 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
   for (int q = 0; q < NC; ++q) {
     if (cv[q]) {
       SA[(int64_t)b * d + tid + kConsumers * q] = scale == 1.0 ? acc[q] : acc[q] * scale;
-      if constexpr (FUSE) gpart[(int64_t)b * d + tid + kConsumers * q] = gac[q];
+      if (fz) gpart[(int64_t)b * d + tid + kConsumers * q] = gac[q];
     }
   }
 }
 
 template <bool FUSE, int NC>
-void launch_tma_t(size_t smem, int nst, const double *A, int64_t n, int d, int m, const int32_t *hist,
-                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec, const double *x,
-                  double *SA, double *gpart, double scale, cudaStream_t st) {
-  IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC>), smem);
-  cs_gather_tma_kernel<FUSE, NC><<<(unsigned)m, kConsumers + 32, smem, st>>>(A, n, d, m, hist, tile_sums, nchunks,
-                                                                              perm, bvec, x, SA, gpart, scale, nst);
+void launch_tma_t(size_t smem, int nst, int nb, GatherBatchStrides bst, const double *A, int64_t n, int d, int m,
+                  const int32_t *hist, const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm,
+                  const double *bvec, const double *x, double *SA, double *gpart, double scale, cudaStream_t st) {
+  if (nb == 1) {
+    IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC, true>), smem);
+    cs_gather_tma_kernel<FUSE, NC, true><<<dim3((unsigned)m, 1), kConsumers + 32, smem, st>>>(
+        A, n, d, m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, nst, bst);
+  } else {
+    IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC, false>), smem);
+    cs_gather_tma_kernel<FUSE, NC, false><<<dim3((unsigned)m, (unsigned)nb), kConsumers + 32, smem, st>>>(
+        A, n, d, m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, nst, bst);
+  }
 }
 }  // namespace
 
@@ -236,18 +251,18 @@ bool cs_gather_tma_supported(int64_t d, const void *A) {
 cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
                                  const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
-                                 LaunchCounter lc) {
+                                 LaunchCounter lc, int nbatch, GatherBatchStrides bst) {
   // ring depth: ~kRingBytes of rows in flight per CTA, 2..kMaxStages stages
   const int nst = (int)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, kRingBytes / (kRows * d * 8)));
   const size_t smem = (size_t)nst * kRows * d * 8 + (size_t)nst * kRows * 8 * (1 + kCW) + 2 * kMaxStages * 8 +
                       kMaxStages * kRows * 4 + 64;
   const int nc = (int)((d + kConsumers - 1) / kConsumers);
   const bool f = gpart != nullptr;
-#define IHS_TMA(NC)                                                                                           \
-  (f ? launch_tma_t<true, NC>(smem, nst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart,   \
-                              scale, st)                                                                     \
-     : launch_tma_t<false, NC>(smem, nst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, nullptr, nullptr, SA,   \
-                               nullptr, scale, st))
+#define IHS_TMA(NC)                                                                                               \
+  (f ? launch_tma_t<true, NC>(smem, nst, nbatch, bst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, bvec, \
+                              x, SA, gpart, scale, st)                                                           \
+     : launch_tma_t<false, NC>(smem, nst, nbatch, bst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm,      \
+                               nullptr, nullptr, SA, nullptr, scale, st))
   if (nc <= 1) IHS_TMA(1);
   else if (nc == 2) IHS_TMA(2);
   else IHS_TMA(4);

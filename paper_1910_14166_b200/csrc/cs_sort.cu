@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
   const int64_t ws = r0 + warp * sub;
   const int64_t we = min(r1, ws + sub);
   int32_t *my = wcnt + (size_t)warp * m;
+  const int nbits = 32 - __clz((int)max(m - 1, 1u));  // bucket < 2^nbits
   uint32_t bk[kMaxGroups];
 #pragma unroll
   for (int q = 0; q < kMaxGroups; ++q) {
@@ -157,11 +158,13 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
     bool neg = false;
     uint32_t b = 0xffffffffu;
     if (ws + 32 * q < we && r < we) b = hash_bucket(key, (uint64_t)(row_offset + r), jb, sb, m, neg) - jb * m;
+    else b = 0;
     bk[q] = b | (neg ? 0x80000000u : 0u);  // m < 2^31: bit 31 free for the sign
     if (ws + 32 * q < we) {
-      const uint32_t bb = r < we ? (bk[q] & 0x7fffffffu) : 0xffffffffu;
-      const unsigned mask = __match_any_sync(0xffffffffu, bb);
-      if (r < we && lane == __ffs(mask) - 1) atomicAdd(&my[bb], __popc(mask));
+      const bool valid = r < we;
+      const uint32_t bb = bk[q] & 0x7fffffffu;
+      const unsigned mask = peers_by_ballot(bb, nbits, valid);
+      if (valid && lane == __ffs(mask) - 1) atomicAdd(&my[bb], __popc(mask));
     }
   }
   __syncthreads();
@@ -182,8 +185,8 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
     if (ws + 32 * q < we) {
       const int64_t r = ws + 32 * q + lane;
       const bool valid = r < we;
-      const uint32_t bb = valid ? (bk[q] & 0x7fffffffu) : 0xffffffffu;
-      const unsigned mask = __match_any_sync(0xffffffffu, bb);
+      const uint32_t bb = bk[q] & 0x7fffffffu;
+      const unsigned mask = peers_by_ballot(bb, nbits, valid);
       const int leader = __ffs(mask) - 1;
       int32_t old = 0;
       if (valid && lane == leader) old = atomicAdd(&my[bb], __popc(mask));

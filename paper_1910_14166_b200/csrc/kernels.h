@@ -50,12 +50,18 @@ cudaError_t launch_cs_gather_async(const double *A, int64_t n, int64_t d, int64_
                                    const double *bvec, const double *x, double *SA, double *gpart, double scale,
                                    cudaStream_t st, LaunchCounter lc);
 // TMA-fed variant: one CTA per bucket, bulk copies of whole rows into a smem
-// ring.  Requires even d <= 256 and a 16-byte aligned A.
+// ring.  Requires even d <= 256 and a 16-byte aligned A.  A batch of nbatch
+// SJLT blocks runs in one launch (grid.y): entry y uses hist + y*bst.hist,
+// tile_sums + y*bst.tiles, perm + y*bst.perm and SA + y*bst.sa; the fused
+// gradient (gpart != null) rides on entry 0.
+struct GatherBatchStrides {
+  int64_t hist = 0, tiles = 0, perm = 0, sa = 0;
+};
 bool cs_gather_tma_supported(int64_t d, const void *A);
 cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
                                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
                                  const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
-                             LaunchCounter lc);
+                                 LaunchCounter lc, int nbatch = 1, GatherBatchStrides bst = GatherBatchStrides());
 
 // ---- a2 dense SJLT (s > 1): smem-tile accumulation --------------------------
 struct SjltPlan {
@@ -70,6 +76,13 @@ struct SjltPlan {
 bool sjlt_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, SjltPlan &p);
 cudaError_t launch_sjlt_dense(const SjltPlan &p, const double *A, uint64_t key, int64_t row_offset,
                               double *partials, double *SA, double scale, cudaStream_t st, LaunchCounter lc);
+// Single-pass variant: 4-column slices, warp j applies block j (2 <= s <= 16, s | m).
+bool sjlt_stream_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, SjltPlan &p);
+cudaError_t launch_sjlt_stream(const SjltPlan &p, const double *A, uint64_t key, int64_t row_offset,
+                               double *partials, double *SA, double scale, cudaStream_t st, LaunchCounter lc);
+// SA[e] = scale * sum_{k < nsplit} partials[k * count + e], k ascending.
+cudaError_t launch_sum_splits(const double *partials, int64_t count, int nsplit, double scale, double *SA,
+                              cudaStream_t st, LaunchCounter lc);
 
 // ---- CSR sketch and gradient (atomics into L2) ------------------------------
 // SA must be zeroed first when sketching.  g must be zeroed when gradient.

@@ -119,16 +119,6 @@ __global__ void __launch_bounds__(256) sjlt_dense_kernel(const double *__restric
   }
 }
 
-// SA[e] = scale * sum_k partials[k][e], k ascending.
-__global__ void sum_splits_kernel(const double *__restrict__ partials, int64_t count, int nsplit, double scale,
-                                  double *__restrict__ SA) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
-    double t = 0.0;
-    for (int k = 0; k < nsplit; ++k) t += partials[(int64_t)k * count + e];
-    SA[e] = scale == 1.0 ? t : t * scale;
-  }
-}
-
 template <int DC>
 void launch_dc(const SjltPlan &p, const double *A, uint64_t key, int64_t row_offset, double *partials,
                cudaStream_t st) {
@@ -140,6 +130,25 @@ void launch_dc(const SjltPlan &p, const double *A, uint64_t key, int64_t row_off
                                                        std::max<int64_t>(rps, 1), partials);
 }
 }  // namespace
+
+// SA[e] = scale * sum_k partials[k][e], k ascending.
+__global__ void sum_splits_kernel(const double *__restrict__ partials, int64_t count, int nsplit, double scale,
+                                  double *__restrict__ SA) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    double t = 0.0;
+    for (int k = 0; k < nsplit; ++k) t += partials[(int64_t)k * count + e];
+    SA[e] = scale == 1.0 ? t : t * scale;
+  }
+}
+
+cudaError_t launch_sum_splits(const double *partials, int64_t count, int nsplit, double scale, double *SA,
+                              cudaStream_t st, LaunchCounter lc) {
+  if (count <= 0) return cudaSuccess;
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 8);
+  sum_splits_kernel<<<grid, 256, 0, st>>>(partials, count, nsplit, scale, SA);
+  lc.add();
+  return cudaGetLastError();
+}
 
 bool sjlt_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, SjltPlan &p) {
   p.n = n;
@@ -182,11 +191,9 @@ cudaError_t launch_sjlt_dense(const SjltPlan &p, const double *A, uint64_t key, 
     case 2: launch_dc<2>(p, A, key, row_offset, partials, st); break;
     default: launch_dc<1>(p, A, key, row_offset, partials, st); break;
   }
-  const int64_t count = p.m * p.d;
-  int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 8);
-  sum_splits_kernel<<<grid, 256, 0, st>>>(partials, count, p.nsplit, scale, SA);
-  lc.add(2);
-  return cudaGetLastError();
+  lc.add();
+  { cudaError_t e = cudaGetLastError(); if (e != cudaSuccess) return e; }
+  return launch_sum_splits(partials, p.m * p.d, p.nsplit, scale, SA, st, lc);
 }
 
 }  // namespace ihs

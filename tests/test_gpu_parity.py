@@ -80,7 +80,8 @@ def test_countsketch_row_offset_shards(P, oracle_mod):
 
 
 @pytest.mark.parametrize("n,d,m,s", [(65_536 + 11, 96, 4096, 8), (20_000, 10, 200, 4), (30_000, 40, 512, 2),
-                                     (5000, 7, 4096, 8), (257, 3, 64, 64), (0, 4, 16, 2)])
+                                     (5000, 7, 4096, 8), (257, 3, 64, 64), (0, 4, 16, 2), (40_001, 97, 4096, 8),
+                                     (30_000, 13, 256, 16), (1, 5, 16, 8)])
 def test_sjlt_dense(P, oracle_mod, n, d, m, s):
     rng = np.random.default_rng(n + m)
     A = rng.standard_normal((n, d))

@@ -41,6 +41,35 @@ __global__ void gather_rows(const double* __restrict__ A, const int* __restrict_
   for (int k=0;k<NV;k++) out[(size_t)w*d+lane+32*k]=acc[k];
 }
 
+// L2-resident re-reads: each CTA streams the same small buffer reps times
+__global__ void rd_l2(const double2* __restrict__ a, size_t n2, int reps, double* out) {
+  double2 acc = {0,0};
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (int r = 0; r < reps; ++r) {
+    size_t i = (blockIdx.x * (size_t)blockDim.x + threadIdx.x + (size_t)r * 7919 * 32) % n2;
+    #pragma unroll 8
+    for (size_t k = 0; k < n2 / stride; ++k) { double2 v = a[(i + k * stride) % n2]; acc.x += v.x; acc.y += v.y; }
+  }
+  if (acc.x == 12345.0) out[0] = acc.y;
+}
+// smem fp64 read-modify-write throughput: conflict-free (lane-contiguous) vs random rows
+__global__ void smem_rmw(int iters, int random, double* out) {
+  extern __shared__ double tile[];
+  const int n = 16384;  // 128 KB
+  for (int e = threadIdx.x; e < n; e += blockDim.x) tile[e] = 0.0;
+  __syncthreads();
+  unsigned x = threadIdx.x * 2654435761u + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = 0; i < iters; ++i) {
+    int idx;
+    if (random) { x = x * 1664525u + 1013904223u; idx = ((x >> 8) % (n / 4)) * 4 + (lane & 3); }
+    else idx = ((i * 16 + warp) * 32 + lane) % n;
+    tile[idx] += 1.0;
+  }
+  __syncthreads();
+  if (tile[threadIdx.x] == 12345.0) out[0] = 1;
+}
+
 __global__ void dmma_loop(double* out, int iters) {
   double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
   double c0[4]={0,0,0,0}, c1[4]={0,0,0,0};
@@ -81,6 +110,19 @@ int main(){
   { std::vector<int> id(n), of2(m+1); int k=0; for (int b=0;b<m;b++){ of2[b]=k; for (int i=b;i<n;i+=m) id[k++]=i; } of2[m]=n;
     cudaMemcpy(dp,id.data(),n*4,cudaMemcpyHostToDevice); cudaMemcpy(doff,of2.data(),(m+1)*4,cudaMemcpyHostToDevice); }
   printf("strided b+k*m:\n"); G(8) G(16)
+  CK(cudaGetLastError());
+  for (size_t mb : {32, 64, 96}) {
+    size_t nb = mb << 20;
+    for (int r=0;r<3;r++){ cudaEventRecord(e0); rd_l2<<<148*8,256>>>((const double2*)A, nb/16, 20, out); cudaEventRecord(e1); cudaEventSynchronize(e1);} cudaEventElapsedTime(&ms,e0,e1);
+    printf("L2 re-read %zu MB x20: %.3f ms  %.1f GB/s\n", mb, ms, 20.0*nb/ms/1e6);
+  }
+  cudaFuncSetAttribute(smem_rmw, cudaFuncAttributeMaxDynamicSharedMemorySize, 131072);
+  for (int rnd : {0, 1}) {
+    int it = 4096;
+    for (int r=0;r<2;r++){ cudaEventRecord(e0); smem_rmw<<<148,512,131072>>>(it, rnd, out); cudaEventRecord(e1); cudaEventSynchronize(e1);} cudaEventElapsedTime(&ms,e0,e1);
+    double upd = 148.0*512*it;
+    printf("smem fp64 RMW %s: %.3f ms  %.2f G upd/s  (%.2f upd/clk/SM at 1.965 GHz)\n", rnd ? "random 32B rows" : "contiguous", ms, upd/ms/1e6, upd/ms/1e-3/148/1.965e9);
+  }
   CK(cudaGetLastError());
   // dmma
   for (int r=0;r<2;r++){ cudaEventRecord(e0); dmma_loop<<<148*4,256>>>(out, 4096); cudaEventRecord(e1); cudaEventSynchronize(e1);} cudaEventElapsedTime(&ms,e0,e1);
