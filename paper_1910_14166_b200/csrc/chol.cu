@@ -7,6 +7,10 @@
 #include "kernels.h"
 #include "chol_blocks.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+
 
 namespace ihs {
 
@@ -149,11 +153,12 @@ size_t chol_large_scratch_bytes(int64_t d);
 cudaError_t launch_chol_large(const double *H, const double *g, int64_t d, const double *x, double *x_next,
                               double *scratch, int *status, cudaStream_t st, LaunchCounter lc);
 
-size_t chol_scratch_bytes(int64_t d) { return d > 160 ? chol_large_scratch_bytes(d) : 256; }
+size_t chol_scratch_bytes(int64_t d) {
+  return d > 160 ? std::max(chol_large_scratch_bytes(d), ols_cg_scratch_bytes(d)) : 256;
+}
 
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,
                               double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc) {
-  (void)num_sms;
   if (d <= 160) {
     const int nblk = (int)((d + 31) / 32);
     switch (nblk) {
@@ -165,6 +170,13 @@ cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const
     }
     lc.add();
     return cudaGetLastError();
+  }
+  // d > 160: conjugate gradients (ols_cg.cu) unless IHS_OLS=chol
+  static const bool force_chol = getenv("IHS_OLS") && !std::strcmp(getenv("IHS_OLS"), "chol");
+  if (!force_chol && ols_cg_supported(d)) {
+    const cudaError_t e = launch_ols_cg(H, g, d, x, x_next, scratch, status, num_sms, st, lc);
+    if (e != cudaErrorCooperativeLaunchTooLarge) return e;
+    cudaGetLastError();
   }
   return launch_chol_large(H, g, d, x, x_next, scratch, status, st, lc);
 }

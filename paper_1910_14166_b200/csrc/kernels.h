@@ -118,6 +118,12 @@ size_t chol_scratch_bytes(int64_t d);
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,
                               double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc);
 
+// d > 160 default: Jacobi-preconditioned CG in one cooperative launch (ols_cg.cu).
+bool ols_cg_supported(int64_t d);
+size_t ols_cg_scratch_bytes(int64_t d);
+cudaError_t launch_ols_cg(const double *H, const double *g, int64_t d, const double *x, double *x_next,
+                          double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc);
+
 // ---- a6 l1 ball: projected gradient -----------------------------------------
 size_t pg_scratch_bytes(int64_t d);
 bool pg_supported(int64_t d);
