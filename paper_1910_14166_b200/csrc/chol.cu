@@ -44,7 +44,8 @@ template <int NBLK>
 __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *__restrict__ H,
                                                                 const double *__restrict__ g, int d,
                                                                 const double *__restrict__ x, double *x_next,
-                                                                int *status) {
+                                                                int *status, const int *run) {
+  if (run && *run == 0) return;  // the CG solve before it finished
   constexpr int D = 32 * NBLK;
   constexpr int DA = D + 8;  // rows incl. the augmented g row and its zero tile padding
   constexpr int lda = D + 4;
@@ -141,11 +142,11 @@ __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *_
 
 template <int NBLK>
 void launch_blocked(const double *H, const double *g, int d, const double *x, double *x_next, int *status,
-                    cudaStream_t st) {
+                    const int *run, cudaStream_t st) {
   constexpr int D = 32 * NBLK;
   const size_t smem = ((size_t)(D + 8) * (D + 4) + D) * 8;
   IHS_SMEM_ATTR((chol_blocked_kernel<NBLK>), smem);
-  chol_blocked_kernel<NBLK><<<1, kBThreads, smem, st>>>(H, g, d, x, x_next, status);
+  chol_blocked_kernel<NBLK><<<1, kBThreads, smem, st>>>(H, g, d, x, x_next, status, run);
 }
 }  // namespace
 
@@ -160,13 +161,14 @@ size_t chol_scratch_bytes(int64_t d) {
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,
                               double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc) {
   if (d <= 160) {
+    const int *run = nullptr;
     const int nblk = (int)((d + 31) / 32);
     switch (nblk) {
-      case 1: launch_blocked<1>(H, g, (int)d, x, x_next, status, st); break;
-      case 2: launch_blocked<2>(H, g, (int)d, x, x_next, status, st); break;
-      case 3: launch_blocked<3>(H, g, (int)d, x, x_next, status, st); break;
-      case 4: launch_blocked<4>(H, g, (int)d, x, x_next, status, st); break;
-      default: launch_blocked<5>(H, g, (int)d, x, x_next, status, st); break;
+      case 1: launch_blocked<1>(H, g, (int)d, x, x_next, status, run, st); break;
+      case 2: launch_blocked<2>(H, g, (int)d, x, x_next, status, run, st); break;
+      case 3: launch_blocked<3>(H, g, (int)d, x, x_next, status, run, st); break;
+      case 4: launch_blocked<4>(H, g, (int)d, x, x_next, status, run, st); break;
+      default: launch_blocked<5>(H, g, (int)d, x, x_next, status, run, st); break;
     }
     lc.add();
     return cudaGetLastError();

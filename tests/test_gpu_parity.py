@@ -185,6 +185,29 @@ def test_ols_update_not_spd(P):
     assert ctx.status() == P.OK  # status is cleared once read
 
 
+@pytest.mark.parametrize("d", [2, 50, 300])
+def test_ols_update_indefinite_positive_diagonal(P, d):
+    """Reading R13: an indefinite H whose diagonal is positive reports NOT_SPD
+    and leaves x unchanged (Cholesky pivot for d <= 160, non-positive curvature
+    p.Hp on the CG path for d > 160)."""
+    rng = np.random.default_rng(d)
+    if d == 2:
+        H = np.array([[1.0, 2.0], [2.0, 1.0]])
+    else:
+        Q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+        ev = np.geomspace(1.0, 10.0, d)
+        ev[:3] = -0.5  # three negative eigenvalues; the diagonal stays positive
+        H = (Q * ev) @ Q.T
+        H = 0.5 * (H + H.T)
+        assert np.linalg.eigvalsh(H).min() < 0 < np.diag(H).min()
+    ctx = P.Context(0)
+    x = torch.ones(d, dtype=torch.float64, device=DEV)
+    g = torch.from_numpy(rng.standard_normal(d)).to(DEV)
+    xn = P.ihs_ols_update(torch.from_numpy(H).to(DEV), g, x, ctx=ctx)
+    assert ctx.status() == P.ERR_NOT_SPD
+    assert torch.equal(xn, x)
+
+
 @pytest.mark.parametrize("d,tau", [(16, 1.0), (256, 10.0), (64, 1e9), (5, 0.0)])
 def test_l1ball_update(P, oracle_mod, d, tau):
     rng = np.random.default_rng(d)
