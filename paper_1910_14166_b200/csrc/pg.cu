@@ -296,6 +296,179 @@ __global__ void __launch_bounds__(kCT) pg_cluster_kernel(const double *__restric
   }
 }
 
+
+// ----------------------------------------------------------------------------
+// Warp-redundant cluster version for d <= 32 K (K <= 8 per lane): as above, but
+// every WARP holds the whole iterate in registers (element q = lane + 32 k) and
+// runs the projection, the norms and the convergence test on its own with
+// warp shuffles -- all warps of all CTAs compute bitwise-identical values --
+// so an inner step has no CTA barrier, only the one cluster barrier after the
+// z rows are exchanged.  The GEMV interleaves a warp's rows (independent fp64
+// chains) and reduces them with one transpose-reduce.
+template <int K>
+__device__ __forceinline__ double wsum_k(const double (&v)[K]) {
+  double t = 0.0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) t += v[k];
+  return warp_sum(t);
+}
+
+template <int K>
+__global__ void __launch_bounds__(kCT) pg_warp_kernel(const double *__restrict__ H, const double *__restrict__ g,
+                                                      int d, const double *__restrict__ x, double radius,
+                                                      int max_inner, int power_iters, double tol, double safety,
+                                                      double *x_next, int32_t *inner_iters, int *status) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int cs = (int)cluster.num_blocks();
+  const int rank = (int)cluster.block_rank();
+  const int R = (d + cs - 1) / cs;
+  const int r0 = rank * R, r1 = min(d, r0 + R);
+  extern __shared__ double sm[];
+  double *Hs = sm;                   // R x d (my rows)
+  double *gs = Hs + (size_t)R * d;   // R (my rows of g)
+  double *zb = gs + R;               // 2 x d : z (or H v), double-buffered by step parity
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int64_t e = tid; e < (int64_t)(r1 - r0) * d; e += kCT) Hs[e] = H[(int64_t)r0 * d + e];
+  for (int i = tid; i < r1 - r0; i += kCT) gs[i] = g[r0 + i];
+  double xv[K], yv[K], wv[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int q = lane + 32 * k;
+    xv[k] = q < d ? x[q] : 0.0;
+    yv[k] = xv[k];
+    wv[k] = q < d ? 1.0 / sqrt((double)d) : 0.0;
+  }
+  cluster.sync();
+  int par = 0;
+  // rows p of this warp: out_p = pg ? y_p - ((H w)_p - g_p) / L : (H w)_p,
+  // written into every CTA's zb[par]; then the cluster barrier.
+  auto gemv_bcast = [&](bool pg_step, double L) {
+    for (int pb = r0 + 8 * warp; pb < r1; pb += 8 * kCW) {
+      double acc[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int p = pb + u;
+        const double *hr = Hs + (size_t)(min(p, r1 - 1) - r0) * d;
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const int q = lane + 32 * k;
+          if (q < d) a = fma(hr[q], wv[k], a);
+        }
+        acc[u] = a;
+      }
+      transpose_reduce<8>(acc, lane);
+      const int u = reduced_row_of_lane<8>(lane);
+      const int p = pb + u;
+      double val = acc[0];
+      if (pg_step) {  // warp-uniform; the shuffles run in every lane
+        // y_p is held by lane p % 32 as element p / 32 of every warp's copy
+        double yp = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          const double t = __shfl_sync(0xffffffffu, yv[k], p & 31);
+          if ((p >> 5) == k) yp = t;
+        }
+        if (p < r1) val = yp - (val - gs[p - r0]) / L;
+      }
+      // the row's owner lane publishes it to every CTA of the cluster
+      if (owner_lane_of_row<8>(u) == lane && p < r1)
+        for (int r = 0; r < cs; ++r) cluster.map_shared_rank(zb + par * d, r)[p] = val;
+    }
+    cluster.sync();
+  };
+  double lam = 0.0;
+  for (int it = 0; it < power_iters; ++it) {
+    gemv_bcast(false, 1.0);
+    const double *hv = zb + par * d;
+    double hvv[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int q = lane + 32 * k;
+      hvv[k] = q < d ? hv[q] : 0.0;
+    }
+    double sq[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) sq[k] = hvv[k] * hvv[k];
+    lam = sqrt(wsum_k(sq));
+    if (!(lam > 0.0)) break;
+#pragma unroll
+    for (int k = 0; k < K; ++k) wv[k] = hvv[k] / lam;
+    par ^= 1;
+  }
+  const double L = (lam > 0.0) ? safety * lam : 1.0;
+  int kk = 0;
+  bool converged = false;
+  while (kk < max_inner) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) wv[k] = yv[k] - xv[k];
+    gemv_bcast(true, L);
+    const double *z = zb + par * d;
+    double zv[K], av[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int q = lane + 32 * k;
+      zv[k] = q < d ? z[q] : 0.0;
+      av[k] = fabs(zv[k]);
+    }
+    const double n1 = wsum_k(av);
+    double theta = 0.0;
+    const bool proj = n1 > radius;
+    if (proj) {  // Michelot's fixed point (reading R19), warp-local
+      theta = (n1 - radius) / (double)d;
+      double cprev = (double)d;
+      for (int guard = 0; guard <= d; ++guard) {
+        double Sv = 0.0, cv = 0.0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (av[k] > theta) {
+            Sv += av[k];
+            cv += 1.0;
+          }
+        }
+        Sv = warp_sum(Sv);
+        cv = warp_sum(cv);
+        if (cv == cprev || cv == 0.0) break;
+        theta = (Sv - radius) / cv;
+        cprev = cv;
+      }
+    }
+    double dn[K], yy[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double yn = zv[k];
+      if (proj) {
+        const double a = av[k] - theta;
+        yn = a > 0.0 ? (zv[k] < 0.0 ? -a : a) : 0.0;
+      }
+      const double e = yn - yv[k];
+      dn[k] = e * e;
+      yy[k] = yv[k] * yv[k];
+      yv[k] = yn;
+    }
+    const double dnn = wsum_k(dn), yyy = wsum_k(yy);
+    par ^= 1;
+    ++kk;
+    if (sqrt(dnn) <= tol * fmax(1.0, sqrt(yyy))) {
+      converged = true;
+      break;
+    }
+  }
+  cluster.sync();  // no CTA may exit while others can still write into its shared memory
+  if (rank == 0 && warp == 0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int q = lane + 32 * k;
+      if (q < d) x_next[q] = yv[k];
+    }
+    if (lane == 0) {
+      if (inner_iters) *inner_iters = kk;
+      if (!converged) set_status(status, 4 /* IHS_ERR_NOT_CONVERGED */);
+    }
+  }
+}
+
 }  // namespace
 
 int pg_cluster_size(int64_t d) {
@@ -316,16 +489,17 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
                                  LaunchCounter lc) {
   (void)scratch;
   static const bool use_cluster = !getenv("IHS_PG_SINGLE");
+  static const bool warp_version = !getenv("IHS_PG_CTA");
   const int cs = use_cluster ? pg_cluster_size(d) : 0;
   if (cs > 0) {
     const int64_t R = (d + cs - 1) / cs;
-    const size_t smem = (size_t)(R * d + 6 * d) * 8;
-    IHS_SMEM_ATTR(pg_cluster_kernel, smem);
-    static bool nonportable = false;
-    if (cs > 8 && !nonportable) {
-      cudaFuncSetAttribute(pg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      nonportable = true;
-    }
+    const bool wv = warp_version && d <= 256;
+    const size_t smem = wv ? (size_t)(R * d + R + 2 * d) * 8 : (size_t)(R * d + 6 * d) * 8;
+    auto kern = !wv ? pg_cluster_kernel
+              : d <= 64 ? pg_warp_kernel<2> : d <= 128 ? pg_warp_kernel<4> : pg_warp_kernel<8>;
+    if (wv && d <= 32) kern = pg_warp_kernel<1>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(kCT);
@@ -339,8 +513,8 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     lc.add();
-    return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
-                              x_next, inner_iters, status);
+    return cudaLaunchKernelEx(&cfg, kern, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety, x_next,
+                              inner_iters, status);
   }
   const size_t smem = (size_t)5 * d * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
