@@ -55,7 +55,7 @@ constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 
 enum Slot {
   S_PERM, S_HIST, S_TILES, S_GPART, S_GRAM, S_SJLT, S_CHOL, S_PACK, S_H, S_X, S_MISC, S_ERR,
-  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_NSLOTS
+  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_NSLOTS
 };
 }  // namespace
 
@@ -73,6 +73,22 @@ struct ihs_ctx_s {
   // profiling: (group, start, stop) per timed launch; events reused after reset
   bool profiling = false;
   int gather = 1;  // CountSketch gather: 0 = register-staged LDG, 1 = TMA bulk, 2 = cp.async ring (IHS_GATHER)
+  // Speculative sort of the NEXT iteration's buckets on a side stream: the
+  // hash (hence the sort) depends only on (seed, iteration, row), not on x, so
+  // after the gathers of iteration t the sort for t + 1 runs beside the
+  // gradient reduction, Gram and inner solve of t (IHS_PREFETCH=0 disables).
+  bool prefetch = true;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_side = nullptr, ev_main = nullptr;
+  bool side_pending = false;  // side work not yet waited on by the main stream
+  struct SortTag {
+    bool valid = false;
+    uint64_t key = 0;
+    int64_t row_offset = 0, n = 0, M = 0;
+    int s = 0;
+    const void *A = nullptr;
+  } pre;
+  int pre_set = 0;
   struct Rec { int group; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
@@ -114,10 +130,13 @@ ihs_status from_cuda(cudaError_t e) {
   } while (0)
 #define IHS_CUDA(expr) IHS_TRY(from_cuda(expr))
 
+void join_side(ihs_ctx c);
+
 template <typename T>
 ihs_status scratch(ihs_ctx c, Slot s, size_t bytes, T **out) {
   bytes = std::max<size_t>(bytes, 256);
   if (c->cap[s] < bytes) {
+    join_side(c);  // the side stream may still use this slot
     if (c->slot[s]) {
       cudaError_t e = cudaFreeAsync(c->slot[s], c->stream);
       if (e != cudaSuccess) return from_cuda(e);
@@ -144,19 +163,29 @@ LaunchCounter lc_of(ihs_ctx c) { return LaunchCounter{&c->launches}; }
 struct Prof {
   ihs_ctx c;
   int group;
+  cudaStream_t st;
   cudaEvent_t b = nullptr;
-  Prof(ihs_ctx c_, int g) : c(c_), group(g) {
+  Prof(ihs_ctx c_, int g, cudaStream_t s_ = nullptr) : c(c_), group(g), st(s_ ? s_ : c_->stream) {
     if (c->profiling) {
       cudaEvent_t a = c->ev();
       b = c->ev();
-      cudaEventRecord(a, c->stream);
+      cudaEventRecord(a, st);
       c->recs.push_back({group, a, b});
     }
   }
   ~Prof() {
-    if (b) cudaEventRecord(b, c->stream);
+    if (b) cudaEventRecord(b, st);
   }
 };
+
+// The main stream waits for any side-stream work issued earlier (before it
+// touches, frees or regrows the buffers the side stream writes).
+void join_side(ihs_ctx c) {
+  if (c->side_pending) {
+    cudaStreamWaitEvent(c->stream, c->ev_side, 0);
+    c->side_pending = false;
+  }
+}
 
 ihs_status check_spec(const ihs_sketch_spec *spec) {
   if (!spec) return IHS_ERR_INVALID_ARGUMENT;
@@ -228,28 +257,41 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       CsSortPlan p = cs_sort_plan(n, M);
       // SJLT blocks are gathered nb at a time (one launch, grid.y = block) so
       // that a launch has about one wave of bucket CTAs (7 per SM) even when
-      // M = m / s is small; each block of a batch has its own sort buffers.
+      // M = m / s is small.  The sort buffers hold all s blocks; two sets, so
+      // the next iteration's sort can be prefetched into the other set.
       const bool tma = c->gather == 1 && cs_gather_tma_supported(d, A->values);
       const int nb = tma ? (int)std::max<int64_t>(1, std::min<int64_t>(s, (7 * (int64_t)c->num_sms) / std::max<int64_t>(M, 1)))
                          : 1;
       const int64_t hs = (int64_t)(p.hist_bytes() / 4 + 63) / 64 * 64, ts = (int64_t)(p.tiles_bytes() / 4 + 63) / 64 * 64;
       const int64_t ps = (p.n + 63) / 64 * 64;
+      const bool hit = c->pre.valid && c->pre.key == key && c->pre.row_offset == A->row_offset && c->pre.n == n &&
+                       c->pre.M == M && c->pre.s == s && c->pre.A == (const void *)A->values;
+      join_side(c);  // also orders any scratch (re)allocation below after side-stream use
+      const int set = hit ? c->pre_set : (c->pre.valid ? 1 - c->pre_set : 0);
+      c->pre.valid = false;
       int32_t *hist, *tiles;
       uint32_t *perm;
-      IHS_TRY(scratch(c, S_HIST, (size_t)hs * 4 * nb, &hist));
-      IHS_TRY(scratch(c, S_TILES, (size_t)ts * 4 * nb, &tiles));
-      IHS_TRY(scratch(c, S_PERM, (size_t)std::max<int64_t>(ps, 1) * 4 * nb, &perm));
+      auto get_set = [&](int k, int32_t **h, int32_t **t, uint32_t **pm) -> ihs_status {
+        IHS_TRY(scratch(c, k ? S_HIST2 : S_HIST, (size_t)hs * 4 * s, h));
+        IHS_TRY(scratch(c, k ? S_TILES2 : S_TILES, (size_t)ts * 4 * s, t));
+        return scratch(c, k ? S_PERM2 : S_PERM, (size_t)std::max<int64_t>(ps, 1) * 4 * s, pm);
+      };
+      IHS_TRY(get_set(set, &hist, &tiles, &perm));
+      auto sort_all = [&](uint64_t k, int32_t *h, int32_t *t, uint32_t *pm, cudaStream_t sst) -> ihs_status {
+        Prof pr(c, IHS_K_SORT, sst);
+        for (int j = 0; j < s; ++j)
+          IHS_CUDA(launch_cs_sort(p, k, A->row_offset, (uint32_t)j, (uint32_t)s, h + j * hs, t + j * ts, pm + j * ps,
+                                  sst, lc_of(c)));
+        return IHS_OK;
+      };
+      if (!hit) IHS_TRY(sort_all(key, hist, tiles, perm, st));
       double *gpart = nullptr;
       if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)M * d * 8, &gpart));
       const double scale = spec_scale(spec);
       for (int j0 = 0; j0 < s; j0 += nb) {
         const int cnt = std::min(nb, s - j0);
-        {
-          Prof pr(c, IHS_K_SORT);
-          for (int jj = 0; jj < cnt; ++jj)
-            IHS_CUDA(launch_cs_sort(p, key, A->row_offset, (uint32_t)(j0 + jj), (uint32_t)s, hist + jj * hs,
-                                    tiles + jj * ts, perm + jj * ps, st, lc_of(c)));
-        }
+        int32_t *hist_j = hist + j0 * hs, *tiles_j = tiles + j0 * ts;
+        uint32_t *perm_j = perm + j0 * ps;
         double *SAj = SA + (int64_t)j0 * M * d;
         double *gp = (j0 == 0) ? gpart : nullptr;
         Prof pr(c, IHS_K_SKETCH);
@@ -259,15 +301,45 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
           bst.tiles = ts;
           bst.perm = ps;
           bst.sa = M * d;
-          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale, st,
-                                        lc_of(c), cnt, bst));
+          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp, scale,
+                                        st, lc_of(c), cnt, bst));
         } else if (c->gather == 2 && cs_gather_async_supported(d, A->values)) {
-          IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale,
-                                          st, lc_of(c)));
+          IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp,
+                                          scale, st, lc_of(c)));
         } else {
-          IHS_CUDA(launch_cs_gather(A->values, n, d, M, hist, tiles, p.nchunks, perm, b, x, SAj, gp, scale, st,
+          IHS_CUDA(launch_cs_gather(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp, scale, st,
                                     lc_of(c)));
         }
+      }
+      // speculative prefetch of iteration iter + 1 into the other set, on the
+      // side stream, after this iteration's gathers (which it cannot overlap:
+      // they fill every SM) -- it runs beside the reduction, Gram and solve.
+      // CountSketch only: an SJLT sort (s blocks) is longer than everything it
+      // could hide behind (measured: no gain on C5).
+      if (c->prefetch && n > 0 && s == 1) {
+        if (!c->side) {
+          IHS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+          IHS_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+          IHS_CUDA(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
+        }
+        const int nset = 1 - set;
+        int32_t *h2, *t2;
+        uint32_t *p2;
+        IHS_TRY(get_set(nset, &h2, &t2, &p2));  // allocated on the main stream, before ev_main
+        IHS_CUDA(cudaEventRecord(c->ev_main, st));
+        IHS_CUDA(cudaStreamWaitEvent(c->side, c->ev_main, 0));
+        const uint64_t key_next = iter_key(spec->seed, iter + 1);
+        IHS_TRY(sort_all(key_next, h2, t2, p2, c->side));
+        IHS_CUDA(cudaEventRecord(c->ev_side, c->side));
+        c->side_pending = true;
+        c->pre.valid = true;
+        c->pre.key = key_next;
+        c->pre.row_offset = A->row_offset;
+        c->pre.n = n;
+        c->pre.M = M;
+        c->pre.s = s;
+        c->pre.A = A->values;
+        c->pre_set = nset;
       }
       if (fuse) {
         Prof pr(c, IHS_K_REDUCE);
@@ -533,6 +605,7 @@ ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
   cudaMemset(c->d_status, 0, sizeof(int));
   if (const char *e = getenv("IHS_GATHER"))
     c->gather = !std::strcmp(e, "ldg") ? 0 : !std::strcmp(e, "async") ? 2 : 1;
+  if (const char *e = getenv("IHS_PREFETCH")) c->prefetch = std::strcmp(e, "0") != 0;
   *out = c;
   return IHS_OK;
 }
@@ -541,6 +614,12 @@ ihs_status ihs_ctx_destroy(ihs_ctx c) {
   if (!c) return IHS_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+    cudaEventDestroy(c->ev_side);
+    cudaEventDestroy(c->ev_main);
+  }
   for (int s = 0; s < S_NSLOTS; ++s)
     if (c->slot[s]) cudaFree(c->slot[s]);
   if (c->d_status) cudaFree(c->d_status);
