@@ -53,6 +53,7 @@ __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *_
   double *Ls = sm;                // DA x lda
   double *rdiag = sm + DA * lda;  // D
   __shared__ int s_bad;
+  __shared__ double colbuf[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int i = warp; i < DA; i += kBThreads / 32) {
     if (i < D) {
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *_
   for (int kb = 0; kb < D; kb += 32) {
     // 1. diagonal block
     if (warp == 0) {
-      const bool bad = warp_chol32(Ls + kb * lda + kb, lda, rdiag + kb, 32);
+      const bool bad = warp_chol32(Ls + kb * lda + kb, lda, rdiag + kb, 32, colbuf);
       if (bad && lane == 0) s_bad = 1;
     }
     __syncthreads();

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double *__restrict__ M,
   __shared__ double Ls[PB * LDP];
   __shared__ double rd[PB];
   __shared__ int s_bad;
+  __shared__ double colbuf[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (*flag) return;  // an earlier panel failed: nothing left to do
   for (int i = warp; i < PB; i += 8)
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) potrf_diag_kernel(double *__restrict__ M,
   __syncthreads();
   for (int k2 = 0; k2 < PB; k2 += 32) {
     if (warp == 0) {
-      const bool bad = warp_chol32(Ls + k2 * LDP + k2, LDP, rd + k2, d - (kb + k2));
+      const bool bad = warp_chol32(Ls + k2 * LDP + k2, LDP, rd + k2, d - (kb + k2), colbuf);
       if (bad && lane == 0) s_bad = 1;
     }
     __syncthreads();

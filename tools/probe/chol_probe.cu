@@ -64,6 +64,43 @@ __device__ __forceinline__ void v4_diag(double (&row)[32], int lane, bool &bad, 
   (v4_step<Js>(row, lane, bad, rd, pnext), ...);
 }
 
+// v5: unconditional updates (entries right of the diagonal pick up unused values)
+template <int J>
+__device__ __forceinline__ void v5_step(double (&row)[32], int lane, bool &bad, double *rd) {
+  const double piv = __shfl_sync(0xffffffffu, row[J], J);
+  bad |= !(piv > 0.0);
+  double sq, r;
+  pivot_rsqrt(piv, sq, r);
+  const double lij = (lane > J) ? row[J] * r : (lane == J ? sq : 0.0);
+  row[J] = lij;
+  if (lane == 0) rd[J] = r;
+#pragma unroll
+  for (int k = J + 1; k < 32; ++k) row[k] = fma(-lij, __shfl_sync(0xffffffffu, lij, k), row[k]);
+}
+template <int... Js>
+__device__ __forceinline__ void v5_diag(double (&row)[32], int lane, bool &bad, double *rd, std::integer_sequence<int, Js...>) {
+  (v5_step<Js>(row, lane, bad, rd), ...);
+}
+// v6: lkj broadcast through shared memory (one STS of the column, LDS broadcasts)
+template <int J>
+__device__ __forceinline__ void v6_step(double (&row)[32], int lane, bool &bad, double *rd, double *col) {
+  const double piv = __shfl_sync(0xffffffffu, row[J], J);
+  bad |= !(piv > 0.0);
+  double sq, r;
+  pivot_rsqrt(piv, sq, r);
+  const double lij = (lane > J) ? row[J] * r : (lane == J ? sq : 0.0);
+  row[J] = lij;
+  if (lane == 0) rd[J] = r;
+  col[(J & 1) * 32 + lane] = lij;
+  __syncwarp();
+#pragma unroll
+  for (int k = J + 1; k < 32; ++k) row[k] = fma(-lij, col[(J & 1) * 32 + k], row[k]);
+}
+template <int... Js>
+__device__ __forceinline__ void v6_diag(double (&row)[32], int lane, bool &bad, double *rd, double *col, std::integer_sequence<int, Js...>) {
+  (v6_step<Js>(row, lane, bad, rd, col), ...);
+}
+
 __device__ void load_spd(double *B) {
   // B = I*40 + ones (SPD), lower part
   for (int e = threadIdx.x; e < 32 * LD; e += blockDim.x) {
@@ -84,7 +121,8 @@ __global__ void k_chol(int variant, int reps, long long *out, double *sink) {
     __syncthreads();
     long long t0 = clock64();
     if (variant == 0 && threadIdx.x < 32) {
-      warp_chol32(B, LD, rd, 32);
+      __shared__ double cb[64];
+      warp_chol32(B, LD, rd, 32, cb);
     } else if (variant == 1 && threadIdx.x < 32) {
       double row[32];
 #pragma unroll
@@ -100,6 +138,17 @@ __global__ void k_chol(int variant, int reps, long long *out, double *sink) {
       for (int c = 0; c < 32; ++c) row[c] = (c <= lane) ? B[lane * LD + c] : 0.0;
       bool bad = false;
       v4_diag(row, lane, bad, rd, std::make_integer_sequence<int, 32>{});
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        if (c <= lane) B[lane * LD + c] = row[c];
+    } else if ((variant == 5 || variant == 6) && threadIdx.x < 32) {
+      __shared__ double colbuf[64];
+      double row[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) row[c] = (c <= lane) ? B[lane * LD + c] : 0.0;
+      bool bad = false;
+      if (variant == 5) v5_diag(row, lane, bad, rd, std::make_integer_sequence<int, 32>{});
+      else v6_diag(row, lane, bad, rd, colbuf, std::make_integer_sequence<int, 32>{});
 #pragma unroll
       for (int c = 0; c < 32; ++c)
         if (c <= lane) B[lane * LD + c] = row[c];
@@ -155,9 +204,10 @@ int main() {
   cudaMalloc(&d_out, 64);
   cudaMalloc(&sink, 64);
   const char *names[] = {"warp_chol32 (rotated)", "diag unrolled", "thread_trsm32 x128 thr (rotated)",
-                         "trsm unrolled x128 thr", "diag unrolled, local next pivot"};
-  for (int v = 0; v < 5; ++v) {
-    int threads = (v < 2 || v == 4) ? 32 : 128;
+                         "trsm unrolled x128 thr", "diag unrolled, local next pivot", "diag unconditional fma",
+                         "diag smem column broadcast"};
+  for (int v = 0; v < 7; ++v) {
+    int threads = (v < 2 || v >= 4) ? 32 : 128;
     k_chol<<<1, threads>>>(v, 20, d_out, sink);  // warm (i-cache)
     k_chol<<<1, threads>>>(v, 20, d_out, sink);
     cudaMemcpy(h, d_out, 64, cudaMemcpyDeviceToHost);
