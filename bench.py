@@ -128,58 +128,73 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(kernel: str):
-    """dram read+write bytes per launch from the committed ncu --set full summary."""
+def ncu_traffic(cfg_name: str, group: str):
+    """DRAM read+write bytes per launch of the group's dominant kernel, from the
+    committed `ncu --set full` summary (profiles/ncu_traffic.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             d = json.load(f)
-        return d.get(kernel)
+        return d.get(cfg_name, {}).get(group)
     except Exception:
         return None
 
 
-DMMA_TFLOPS = 36.7  # fp64 DMMA peak measured on this pool's B200 (tools/probe/probe.cu, profiles/r01_probe.txt)
+DMMA_TFLOPS = 36.8  # fp64 DMMA peak measured on this pool's B200 (tools/probe/probe.cu, profiles/r01/probe.txt)
 
 
-def roofline(prof, cfg, n_loc, nnz_loc, ms_step):
-    """Achieved vs peak for the dominant kernel group of the step, from the
-    library's CUDA events (algorithmic bytes / flops per launch)."""
+def algorithmic(cfg, group, n_loc, nnz_loc, steps_launches):
+    """(bytes or flops per step, kind, kernel label) of one kernel group, from
+    SURVEY.md 8(d)'s per-unit figures."""
+    d, m, s = cfg.d, cfg.m, cfg.s
+    M = m // s
+    if group == "sketch":  # s bucket-ordered gathers over A; gradient fused into block 0
+        b = s * (8 * n_loc * d + 4 * n_loc) + 8 * n_loc + 8 * M * d + 8 * m * d
+        return b, "hbm", "cs_gather_tma_kernel (bucket-ordered sketch, gradient fused into block 0)"
+    if group == "sjlt":
+        return 8 * n_loc * d + 8 * m * d, "hbm", "sjlt_stream_kernel"
+    if group == "grad":
+        return 8 * n_loc * d + 8 * n_loc, "hbm", "grad_dense_kernel"
+    if group == "csr":
+        return 8 * (n_loc + 1) + 12 * nnz_loc + 8 * n_loc + 8 * m * d, "hbm", "csr_sketch_grad_kernel"
+    if group == "gram":
+        return float(m) * d * d, "tensor", "gram_kernel (DMMA m8n8k4 f64, symmetric half)"
+    return None, "latency", group
+
+
+def roofline(prof, cfg, n_loc, nnz_loc, steps):
+    """Achieved vs peak for the dominant kernel group of the step: algorithmic
+    bytes (flops) per launch / the group's average launch time from the
+    library's CUDA events on its stream."""
     peaks, peak_src = measured_peaks()
-    d, m = cfg.d, cfg.m
     groups = {k: v for k, v in prof.items() if v[1] > 0}
     if not groups:
         return None
     name = max(groups, key=lambda k: groups[k][0])
     tot, k = groups[name]
+    per_step = tot / steps
     avg = tot / k
-    out = {"kernel_group": name, "avg_launch_ms": avg, "share_of_step": tot / ms_step if ms_step else None}
-    if name in ("sketch", "sjlt", "csr", "grad"):
-        if name == "sketch":
-            alg = 8 * n_loc * d + 12 * n_loc + 16 * m * d  # A once, b + perm per row, SA + g partials
-            out["kernel"] = "cs_gather_tma_kernel<fused> (CountSketch sketch + gradient, one read of A)"
-        elif name == "sjlt":
-            alg = 8 * n_loc * d + 8 * m * d  # A once + SA
-            out["kernel"] = "sjlt_dense_kernel (smem-tile SJLT sketch; shared-memory bound, DESIGN.md 9)"
-        elif name == "grad":
-            alg = 8 * n_loc * d + 8 * n_loc
-            out["kernel"] = "grad_dense_kernel"
-        else:
-            alg = 8 * (n_loc + 1) + 12 * nnz_loc + 8 * n_loc + 8 * m * d
-            out["kernel"] = "csr_sketch_grad_kernel (CSR sketch + gradient)"
-        ach = alg / (avg / 1e3) / 1e9
+    launches_per_step = k / steps
+    alg, kind, label = algorithmic(cfg, name, n_loc, nnz_loc, launches_per_step)
+    out = {"kernel_group": name, "kernel": label, "avg_launch_ms": avg, "launches_per_step": launches_per_step,
+           "ms_per_step": per_step}
+    if alg is None:
+        out.update({"bound": "latency", "achieved": None, "peak": None, "unit": None, "frac": None})
+    elif kind == "hbm":
+        per_launch = alg / launches_per_step
+        ach = per_launch / (avg / 1e3) / 1e9
         out.update({"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": ach / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": alg,
+                    "frac": ach / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": per_launch,
                     "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"})
-    elif name == "gram":
-        fl = 2.0 * m * d * d / 2  # symmetric half: m d^2 FMA-pairs
-        ach = fl / (avg / 1e3) / 1e12
-        out.update({"kernel": "gram_kernel (DMMA m8n8k4 f64)", "bound": "tensor", "achieved": ach,
-                    "peak": DMMA_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_TFLOPS,
-                    "algorithmic_flops_per_launch": fl, "peak_source": "measured fp64 DMMA (probe)"})
     else:
-        out.update({"kernel": name, "bound": "latency", "achieved": None, "peak": None, "unit": None,
-                    "frac": None})
-    out["traffic"] = ncu_traffic(name)
+        per_launch = alg / launches_per_step
+        ach = per_launch / (avg / 1e3) / 1e12
+        out.update({"bound": "tensor", "achieved": ach, "peak": DMMA_TFLOPS, "unit": "TFLOP/s",
+                    "frac": ach / DMMA_TFLOPS, "algorithmic_flops_per_launch": per_launch,
+                    "peak_source": "measured fp64 DMMA m8n8k4 throughput (tools/probe/probe.cu)"})
+    tr = ncu_traffic(cfg.name, name)
+    out["traffic"] = tr.get("dram_bytes_per_launch") if isinstance(tr, dict) else tr
+    if isinstance(tr, dict):
+        out["traffic_source"] = tr.get("source")
     return out
 
 
@@ -307,7 +322,7 @@ def main():
     ctx.set_profiling(False)
     # ---- roofline of the dominant kernel group (C2: the fused sketch+gradient gather)
     n_loc = r1 - r0
-    roof = roofline(prof, cfg, n_loc, n_loc_nnz, ms_local)
+    roof = roofline(prof, cfg, n_loc, n_loc_nnz, args.steps)
     breakdown = {name: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for name, v in prof.items() if v[1]}
     # ---- time to 1e-10 (IHS solve from x^0 = 0; errors post hoc, outside the timing)
     ttt = None

@@ -36,8 +36,10 @@ typedef enum {
     IHS_OK = 0,
     IHS_ERR_INVALID_ARGUMENT = 1,   /* null pointer, negative size, bad spec */
     IHS_ERR_DIMENSION_MISMATCH = 2, /* e.g. m not divisible by s */
-    IHS_ERR_NOT_SPD = 3,            /* Cholesky pivot <= 0 (reading R13) */
-    IHS_ERR_NOT_CONVERGED = 4,      /* inner PG hit max_inner; best iterate written */
+    IHS_ERR_NOT_SPD = 3,            /* H not positive definite: Cholesky pivot <= 0, or (CG path,
+                                       d > 160) a non-positive diagonal / curvature p.Hp <= 0 (R13, R22) */
+    IHS_ERR_NOT_CONVERGED = 4,      /* inner PG hit max_inner (best iterate written), or the
+                                       OLS CG hit its cap (x_next = x + last u) */
     IHS_ERR_CUDA = 5,               /* CUDA runtime / launch / async fault */
     IHS_ERR_COMM = 6,               /* NCCL failure or communicator missing */
     IHS_ERR_OUT_OF_MEMORY = 7,      /* scratch allocation failed */
@@ -164,9 +166,12 @@ ihs_status ihs_sketch_grad(ihs_ctx ctx, const ihs_matrix *A, const ihs_sketch_sp
 ihs_status ihs_gram(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, double scale,
                     double *H);
 
-/* a6, OLS: x_next = x + H^{-1} g by Cholesky (Eq. (2) with C = R^d).  A
- * non-positive pivot sets IHS_ERR_NOT_SPD (device status) and writes x_next = x.
- * H is not modified.  x_next may alias x. */
+/* a6, OLS: x_next = x + H^{-1} g (Eq. (2) with C = R^d).
+ * d <= 160: blocked Cholesky in one CTA; d > 160: Jacobi-preconditioned
+ * conjugate gradients to a relative residual of 1e-15 in one cooperative
+ * launch (reading R22; IHS_OLS=chol selects the multi-CTA Cholesky).  H not
+ * positive definite sets IHS_ERR_NOT_SPD (device status) and writes
+ * x_next = x.  H is not modified.  x_next may alias x. */
 ihs_status ihs_ols_update(ihs_ctx ctx, const double *H, const double *g, int64_t d,
                           const double *x, double *x_next);
 

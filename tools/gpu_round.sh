@@ -1,10 +1,11 @@
 #!/bin/bash
-# One gpurun call: GPU tests, bench on every config, ncu launch list and one
-# `ncu --set full` capture per dominant kernel.  Outputs under gpurun_out/$TAG/.
-# usage: gpurun -- 'bash tools/gpu_round.sh TAG [parts...]'   parts: tests smoke bench ncu probe
+# One gpurun call: GPU tests, smoke, bench on every config, the reference arm,
+# ncu launch lists and one `ncu --set full` capture per dominant kernel.
+# Outputs under gpurun_out/$TAG/ (summarised into profiles/ by tools/ncu_summary.py).
+# usage: gpurun -- 'bash tools/gpu_round.sh TAG [parts...]'   parts: probe tests smoke bench ncu
 TAG=${1:-r01}
 shift
-PARTS=${*:-"probe tests smoke bench ncu"}
+PARTS=${*:-"tests smoke bench ncu"}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
@@ -31,22 +32,23 @@ fi
 if has ncu; then
   NCU=/usr/local/cuda/bin/ncu
   for C in C2 C3 C4 C5; do
+    python bench.py --config $C --steps 3 --warmup 3 --no-e2e --no-cpu --no-ttt > $OUT/plain_$C.log 2>&1 &&
     timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $OUT/launches_$C.csv python bench.py --config $C --steps 3 --warmup 3 --no-e2e --no-cpu --no-ttt \
       > $OUT/ncu_launch_$C.log 2>&1
   done
-  # one full capture of each dominant kernel (launch-skip past the warm-up)
+  B="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt"
+  $B --config C2 > $OUT/plain1_C2.log 2>&1 &&
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cs_gather_tma -s 3 -c 1 \
-    -o $OUT/full_C2_gather -f python bench.py --config C2 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt \
-    > $OUT/ncu_full_C2.log 2>&1
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:sjlt -s 3 -c 1 \
-    -o $OUT/full_C5_sjlt -f python bench.py --config C5 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt \
-    > $OUT/ncu_full_C5.log 2>&1
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"gram_kernel|csr_sketch|potrf|syrk" -s 12 -c 6 \
-    -o $OUT/full_C3 -f python bench.py --config C3 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt \
-    > $OUT/ncu_full_C3.log 2>&1
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"pg_l1ball|cs_gather_tma" -s 6 -c 2 \
-    -o $OUT/full_C4 -f python bench.py --config C4 --steps 1 --warmup 3 --no-e2e --no-cpu --no-ttt \
-    > $OUT/ncu_full_C4.log 2>&1
+    -o $OUT/full_C2 -f $B --config C2 > $OUT/ncu_full_C2.log 2>&1
+  $B --config C3 > $OUT/plain1_C3.log 2>&1 &&
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"gram_kernel|csr_sketch|ols_cg" -s 9 -c 3 \
+    -o $OUT/full_C3 -f $B --config C3 > $OUT/ncu_full_C3.log 2>&1
+  $B --config C4 > $OUT/plain1_C4.log 2>&1 &&
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"pg_warp|cs_gather_tma" -s 6 -c 2 \
+    -o $OUT/full_C4 -f $B --config C4 > $OUT/ncu_full_C4.log 2>&1
+  $B --config C5 > $OUT/plain1_C5.log 2>&1 &&
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cs_gather_tma -s 12 -c 1 \
+    -o $OUT/full_C5 -f $B --config C5 > $OUT/ncu_full_C5.log 2>&1
 fi
 ls -la $OUT
