@@ -288,35 +288,13 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       double *gpart = nullptr;
       if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)M * d * 8, &gpart));
       const double scale = spec_scale(spec);
-      for (int j0 = 0; j0 < s; j0 += nb) {
-        const int cnt = std::min(nb, s - j0);
-        int32_t *hist_j = hist + j0 * hs, *tiles_j = tiles + j0 * ts;
-        uint32_t *perm_j = perm + j0 * ps;
-        double *SAj = SA + (int64_t)j0 * M * d;
-        double *gp = (j0 == 0) ? gpart : nullptr;
-        Prof pr(c, IHS_K_SKETCH);
-        if (tma) {
-          GatherBatchStrides bst;
-          bst.hist = hs;
-          bst.tiles = ts;
-          bst.perm = ps;
-          bst.sa = M * d;
-          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp, scale,
-                                        st, lc_of(c), cnt, bst));
-        } else if (c->gather == 2 && cs_gather_async_supported(d, A->values)) {
-          IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp,
-                                          scale, st, lc_of(c)));
-        } else {
-          IHS_CUDA(launch_cs_gather(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp, scale, st,
-                                    lc_of(c)));
-        }
-      }
-      // speculative prefetch of iteration iter + 1 into the other set, on the
-      // side stream, after this iteration's gathers (which it cannot overlap:
-      // they fill every SM) -- it runs beside the reduction, Gram and solve.
-      // CountSketch only: an SJLT sort (s blocks) is longer than everything it
-      // could hide behind (measured: no gain on C5).
-      if (c->prefetch && n > 0 && s == 1) {
+      // Speculative prefetch of iteration iter + 1 into the other set, on the
+      // side stream, issued BEFORE this iteration's gathers: the sort kernels
+      // (hash + smem histogram + scatter, compute/L2-bound) co-reside with the
+      // HBM-bound gather CTAs, so the next sort is hidden behind this
+      // iteration's read of A.  The other set was last read by the gathers of
+      // iter - 1, which precede ev_main on the main stream.
+      if (c->prefetch && n > 0) {
         if (!c->side) {
           IHS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
           IHS_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
@@ -340,6 +318,29 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
         c->pre.s = s;
         c->pre.A = A->values;
         c->pre_set = nset;
+      }
+      for (int j0 = 0; j0 < s; j0 += nb) {
+        const int cnt = std::min(nb, s - j0);
+        int32_t *hist_j = hist + j0 * hs, *tiles_j = tiles + j0 * ts;
+        uint32_t *perm_j = perm + j0 * ps;
+        double *SAj = SA + (int64_t)j0 * M * d;
+        double *gp = (j0 == 0) ? gpart : nullptr;
+        Prof pr(c, IHS_K_SKETCH);
+        if (tma) {
+          GatherBatchStrides bst;
+          bst.hist = hs;
+          bst.tiles = ts;
+          bst.perm = ps;
+          bst.sa = M * d;
+          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp, scale,
+                                        st, lc_of(c), cnt, bst));
+        } else if (c->gather == 2 && cs_gather_async_supported(d, A->values)) {
+          IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp,
+                                          scale, st, lc_of(c)));
+        } else {
+          IHS_CUDA(launch_cs_gather(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp, scale, st,
+                                    lc_of(c)));
+        }
       }
       if (fuse) {
         Prof pr(c, IHS_K_REDUCE);

@@ -145,7 +145,7 @@ template <int NBLK>
 void launch_blocked(const double *H, const double *g, int d, const double *x, double *x_next, int *status,
                     const int *run, cudaStream_t st) {
   constexpr int D = 32 * NBLK;
-  const size_t smem = ((size_t)(D + 8) * (D + 4) + D) * 8;
+  const size_t smem = std::max(((size_t)(D + 8) * (D + 4) + D) * 8, kExclusiveSmem);
   IHS_SMEM_ATTR((chol_blocked_kernel<NBLK>), smem);
   chol_blocked_kernel<NBLK><<<1, kBThreads, smem, st>>>(H, g, d, x, x_next, status, run);
 }

@@ -113,6 +113,12 @@ __device__ __forceinline__ void set_status(int *status, int code) {
   if (status) atomicCAS(status, 0, code);
 }
 
+// Latency-bound single-CTA / single-cluster kernels (the inner solves) ask for
+// this much dynamic shared memory so that no other CTA can share their SM:
+// the next iteration's sort, prefetched on a side stream, would otherwise
+// co-reside and steal issue slots on the critical path.
+constexpr size_t kExclusiveSmem = 200 * 1024;
+
 // Opt a kernel into large dynamic shared memory once per call site and size
 // (raised only when a launch needs more): cudaFuncSetAttribute must not run on
 // every launch.

@@ -7,6 +7,7 @@
 // outer iteration); H stays L2-resident.  The projection threshold is found by
 // Michelot's fixed-point iteration, which reaches the same theta as the sorted
 // rule of the oracle (R8) in exact arithmetic.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -494,7 +495,8 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
   if (cs > 0) {
     const int64_t R = (d + cs - 1) / cs;
     const bool wv = warp_version && d <= 256;
-    const size_t smem = wv ? (size_t)(R * d + R + 2 * d) * 8 : (size_t)(R * d + 6 * d) * 8;
+    const size_t smem =
+        std::max(wv ? (size_t)(R * d + R + 2 * d) * 8 : (size_t)(R * d + 6 * d) * 8, kExclusiveSmem);
     auto kern = !wv ? pg_cluster_kernel
               : d <= 64 ? pg_warp_kernel<2> : d <= 128 ? pg_warp_kernel<4> : pg_warp_kernel<8>;
     if (wv && d <= 32) kern = pg_warp_kernel<1>;
