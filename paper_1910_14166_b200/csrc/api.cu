@@ -55,7 +55,7 @@ constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 
 enum Slot {
   S_PERM, S_HIST, S_TILES, S_GPART, S_GRAM, S_SJLT, S_CHOL, S_PACK, S_H, S_X, S_MISC, S_ERR,
-  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_NSLOTS
+  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_PG, S_NSLOTS
 };
 }  // namespace
 
@@ -89,6 +89,7 @@ struct ihs_ctx_s {
     const void *A = nullptr;
   } pre;
   int pre_set = 0;
+  int64_t pg_warm_d = -1;  // S_PG holds a power-iteration vector for this d
   struct Rec { int group; cudaEvent_t a, b; };
   std::vector<Rec> recs;
   std::vector<cudaEvent_t> pool;
@@ -411,9 +412,16 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
   if (k.max_inner < 1 || k.power_iters < 1 || !(k.inner_tol >= 0.0) || !(k.lip_safety > 0.0))
     return IHS_ERR_INVALID_ARGUMENT;
   if (!pg_supported(d)) return IHS_ERR_UNSUPPORTED;
+  // warm-started power iteration across calls with the same d (IHS_PG_WARM=0 off)
+  static const bool warm_env = !getenv("IHS_PG_WARM") || std::strcmp(getenv("IHS_PG_WARM"), "0") != 0;
+  double *ev = nullptr;
+  if (warm_env && c->cap[S_PG] < std::max<size_t>(pg_scratch_bytes(d), 256)) c->pg_warm_d = -1;  // (re)allocation loses it
+  if (warm_env) IHS_TRY(scratch(c, S_PG, pg_scratch_bytes(d), &ev));
+  const bool warm = warm_env && c->pg_warm_d == d;
   Prof pr(c, IHS_K_PG);
   IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.inner_tol, k.lip_safety, xn, inner,
-                                nullptr, c->d_status, c->stream, lc_of(c)));
+                                ev, c->d_status, c->stream, lc_of(c), warm));
+  if (warm_env) c->pg_warm_d = d;
   return IHS_OK;
 }
 

@@ -9,6 +9,7 @@
 // rule of the oracle (R8) in exact arithmetic.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -315,10 +316,11 @@ __device__ __forceinline__ double wsum_k(const double (&v)[K]) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(kCT) pg_warp_kernel(const double *__restrict__ H, const double *__restrict__ g,
+__global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restrict__ H, const double *__restrict__ g,
                                                       int d, const double *__restrict__ x, double radius,
                                                       int max_inner, int power_iters, double tol, double safety,
-                                                      double *x_next, int32_t *inner_iters, int *status) {
+                                                      double *x_next, int32_t *inner_iters, int *status, int accel,
+                                                      double *evec, int warm) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = (int)cluster.num_blocks();
@@ -332,13 +334,16 @@ __global__ void __launch_bounds__(kCT) pg_warp_kernel(const double *__restrict__
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int64_t e = tid; e < (int64_t)(r1 - r0) * d; e += kCT) Hs[e] = H[(int64_t)r0 * d + e];
   for (int i = tid; i < r1 - r0; i += kCT) gs[i] = g[r0 + i];
-  double xv[K], yv[K], wv[K];
+  double xv[K], yv[K], vv[K], wv[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int q = lane + 32 * k;
     xv[k] = q < d ? x[q] : 0.0;
     yv[k] = xv[k];
-    wv[k] = q < d ? 1.0 / sqrt((double)d) : 0.0;
+    vv[k] = yv[k];
+    // power iteration start: 1/sqrt(d) (reading R10), or, warm, the previous
+    // call's final vector (consecutive IHS Hessian sketches are close)
+    wv[k] = q < d ? (warm ? evec[q] : 1.0 / sqrt((double)d)) : 0.0;
   }
   cluster.sync();
   int par = 0;
@@ -368,7 +373,7 @@ __global__ void __launch_bounds__(kCT) pg_warp_kernel(const double *__restrict__
         double yp = 0.0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          const double t = __shfl_sync(0xffffffffu, yv[k], p & 31);
+          const double t = __shfl_sync(0xffffffffu, vv[k], p & 31);
           if ((p >> 5) == k) yp = t;
         }
         if (p < r1) val = yp - (val - gs[p - r0]) / L;
@@ -399,11 +404,19 @@ __global__ void __launch_bounds__(kCT) pg_warp_kernel(const double *__restrict__
     par ^= 1;
   }
   const double L = (lam > 0.0) ? safety * lam : 1.0;
+  if (evec && rank == 0 && warp == 0 && lam > 0.0) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int q = lane + 32 * k;
+      if (q < d) evec[q] = wv[k];
+    }
+  }
   int kk = 0;
   bool converged = false;
+  double tk = 1.0;  // FISTA momentum parameter (accel) -- plain PG keeps vv = yv
   while (kk < max_inner) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) wv[k] = yv[k] - xv[k];
+    for (int k = 0; k < K; ++k) wv[k] = vv[k] - xv[k];
     gemv_bcast(true, L);
     const double *z = zb + par * d;
     double zv[K], av[K];
@@ -435,7 +448,7 @@ __global__ void __launch_bounds__(kCT) pg_warp_kernel(const double *__restrict__
         cprev = cv;
       }
     }
-    double dn[K], yy[K];
+    double dn[K], yy[K], rs[K], ynv[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       double yn = zv[k];
@@ -446,9 +459,28 @@ __global__ void __launch_bounds__(kCT) pg_warp_kernel(const double *__restrict__
       const double e = yn - yv[k];
       dn[k] = e * e;
       yy[k] = yv[k] * yv[k];
-      yv[k] = yn;
+      rs[k] = (vv[k] - yn) * e;  // gradient-based restart test (O'Donoghue & Candes)
+      ynv[k] = yn;
     }
     const double dnn = wsum_k(dn), yyy = wsum_k(yy);
+    if (accel) {
+      const double rsum = wsum_k(rs);
+      double coef = 0.0;
+      if (rsum > 0.0) {
+        tk = 1.0;  // restart: the next step is a plain projected-gradient step
+      } else {
+        const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * tk * tk));
+        coef = (tk - 1.0) / tn;
+        tk = tn;
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) vv[k] = ynv[k] + coef * (ynv[k] - yv[k]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) vv[k] = ynv[k];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) yv[k] = ynv[k];
     par ^= 1;
     ++kk;
     if (sqrt(dnn) <= tol * fmax(1.0, sqrt(yyy))) {
@@ -482,13 +514,12 @@ int pg_cluster_size(int64_t d) {
 
 bool pg_supported(int64_t d) { return pg_cluster_size(d) > 0 || (size_t)5 * d * 8 <= 200 * 1024; }
 
-size_t pg_scratch_bytes(int64_t) { return 0; }
+size_t pg_scratch_bytes(int64_t d) { return (size_t)d * 8; }
 
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
                                  int max_inner, int power_iters, double tol, double safety, double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
-                                 LaunchCounter lc) {
-  (void)scratch;
+                                 LaunchCounter lc, bool warm_start) {
   static const bool use_cluster = !getenv("IHS_PG_SINGLE");
   static const bool warp_version = !getenv("IHS_PG_CTA");
   const int cs = use_cluster ? pg_cluster_size(d) : 0;
@@ -497,9 +528,9 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     const bool wv = warp_version && d <= 256;
     const size_t smem =
         std::max(wv ? (size_t)(R * d + R + 2 * d) * 8 : (size_t)(R * d + 6 * d) * 8, kExclusiveSmem);
-    auto kern = !wv ? pg_cluster_kernel
-              : d <= 64 ? pg_warp_kernel<2> : d <= 128 ? pg_warp_kernel<4> : pg_warp_kernel<8>;
-    if (wv && d <= 32) kern = pg_warp_kernel<1>;
+    auto wkern = d <= 32 ? pg_warp_kernel<1> : d <= 64 ? pg_warp_kernel<2> : d <= 128 ? pg_warp_kernel<4>
+                                                                             : pg_warp_kernel<8>;
+    const void *kern = wv ? (const void *)wkern : (const void *)pg_cluster_kernel;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
@@ -515,8 +546,16 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     lc.add();
-    return cudaLaunchKernelEx(&cfg, kern, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety, x_next,
-                              inner_iters, status);
+    if (!wv)
+      return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
+                                x_next, inner_iters, status);
+    static const int accel = (getenv("IHS_PG_PLAIN") && std::strcmp(getenv("IHS_PG_PLAIN"), "0") != 0) ? 0 : 1;
+    // warm start (scratch = d doubles holding the last eigenvector estimate):
+    // a dozen power steps from it instead of power_iters from 1/sqrt(d)
+    const bool warm_ok = warm_start && scratch;
+    const int piters = warm_ok ? std::min(power_iters, 12) : power_iters;
+    return cudaLaunchKernelEx(&cfg, wkern, H, g, (int)d, x, radius, max_inner, piters, tol, safety, x_next,
+                              inner_iters, status, accel, scratch, warm_ok ? 1 : 0);
   }
   const size_t smem = (size_t)5 * d * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
