@@ -65,11 +65,13 @@ def lib():
                 "or_project_l1": (None, [i64, p, dbl, p]),
                 "or_power_lmax": (dbl, [i64, p, i32]),
                 "or_l1ball_step": (C.c_int, [i64, p, p, p, dbl, i32, dbl, i32, dbl, p, p]),
+                "or_lasso_step": (C.c_int, [i64, p, p, p, dbl, i32, dbl, i32, dbl, p, p]),
                 "or_ihs_solve": (C.c_int, [i32, i64, i64, p, p, p, p, u64, i64, i32, i32, u64,
                                            i32, dbl, i32, dbl, i32, dbl, p, p, p]),
                 "or_normal_dense": (None, [i64, i64, p, p, p, p]),
                 "or_exact_ols": (C.c_int, [i32, i64, i64, p, p, p, p, p]),
                 "or_exact_l1ball": (C.c_int, [i32, i64, i64, p, p, p, p, dbl, i32, i32, dbl, p]),
+                "or_exact_lasso": (C.c_int, [i64, i64, p, p, dbl, i32, i32, dbl, p]),
                 "or_pred_rel_err": (dbl, [i32, i64, i64, p, p, p, p, p]),
             }
             for name, (res, args) in sig.items():
@@ -253,6 +255,17 @@ def l1ball_step(H, g, x, tau, max_inner=20000, tol=1e-14, power_iters=50, safety
     return xn, int(it.value), int(st)
 
 
+def lasso_step(H, g, x, lam, max_inner=20000, tol=1e-14, power_iters=50, safety=1.05):
+    """NEXT-2: proximal-gradient solve of Eq. (2) + lambda ||x||_1 (readings R10, R23).
+    Returns (x_next, inner_iterations, status)."""
+    H, g, x = _f64(H), _f64(g), _f64(x)
+    xn = np.empty_like(x)
+    it = C.c_int32(0)
+    st = lib().or_lasso_step(H.shape[0], _ptr(H), _ptr(g), _ptr(x), float(lam), max_inner, tol,
+                             power_iters, safety, _ptr(xn), C.byref(it))
+    return xn, int(it.value), int(st)
+
+
 # ------------------------------------------------------------ IHS (a1-a7)
 def ihs_solve(A=None, b=None, *, csr=None, d=None, seed=0, m, s=1, T, iter0=0,
               constraint="ols", tau=0.0, max_inner=20000, tol=1e-14, power_iters=50,
@@ -273,7 +286,8 @@ def ihs_solve(A=None, b=None, *, csr=None, d=None, seed=0, m, s=1, T, iter0=0,
     inner = np.zeros(max(T, 1), np.int32)
     x0a = None if x0 is None else _f64(x0)
     st = lib().or_ihs_solve(layout, n, d, _ptr(vals), _ptr(rp), _ptr(cl), _ptr(b), seed, m, s, T, iter0,
-                            0 if constraint == "ols" else 1, float(tau), max_inner, tol, power_iters,
+                            {"ols": 0, "l1ball": 1, "lasso": 2}[constraint], float(tau), max_inner, tol,
+                            power_iters,
                             safety, _ptr(x0a), _ptr(xh), _ptr(inner))
     if st != OK:
         raise OracleError(st, "ihs_solve")
@@ -307,6 +321,17 @@ def exact_l1ball(A, b, tau, outer=8, max_inner=200000, tol=1e-15):
     st = lib().or_exact_l1ball(0, n, d, _ptr(A), None, None, _ptr(b), float(tau), outer, max_inner, tol, _ptr(x))
     if st != OK:
         raise OracleError(st, "exact_l1ball")
+    return x
+
+
+def exact_lasso(A, b, lam, outer=8, max_inner=200000, tol=1e-15):
+    """NEXT-2: x_OPT of 1/2||Ax - b||^2 + lam ||x||_1: IHS with A^T A."""
+    A, b = _f64(A), _f64(b)
+    n, d = A.shape
+    x = np.empty(d)
+    st = lib().or_exact_lasso(n, d, _ptr(A), _ptr(b), float(lam), outer, max_inner, tol, _ptr(x))
+    if st != OK:
+        raise OracleError(st, "exact_lasso")
     return x
 
 

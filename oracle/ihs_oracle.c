@@ -382,10 +382,50 @@ int or_l1ball_step(int64_t d, const double *H, const double *g, const double *x,
     return st;
 }
 
+/* NEXT-2, penalised LASSO (section 3: x_OPT = argmin
+ * 1/2||Ax - b||^2 + lambda ||x||_1; the IHS step keeps the penalty, reading
+ * R23): proximal gradient on q(y) + lambda ||y||_1, q as in or_l1ball_step,
+ * with the l1 prox (soft-thresholding at lambda / L) in place of the ball
+ * projection; same L, start, stopping rule and cap as R10. */
+int or_lasso_step(int64_t d, const double *H, const double *g, const double *x,
+                  double lambda, int32_t max_inner, double tol, int32_t power_iters,
+                  double safety, double *x_next, int32_t *iters_out)
+{
+    double L = safety * or_power_lmax(d, H, power_iters);
+    double *y = (double *)malloc(sizeof(double) * (size_t)d);
+    double *yn = (double *)malloc(sizeof(double) * (size_t)d);
+    int st = OR_ERR_NOT_CONVERGED;
+    int32_t k = 0;
+    for (int64_t c = 0; c < d; ++c) y[c] = x[c];
+    while (k < max_inner) {
+        for (int64_t p = 0; p < d; ++p) {
+            double acc = 0.0;
+            for (int64_t q = 0; q < d; ++q) acc += H[p * d + q] * (y[q] - x[q]);
+            double z = y[p] - (acc - g[p]) / L;
+            double a = fabs(z) - lambda / L;                  /* soft threshold */
+            yn[p] = a > 0.0 ? (z < 0.0 ? -a : a) : 0.0;
+        }
+        ++k;
+        double dn = 0.0, yy = 0.0;
+        for (int64_t c = 0; c < d; ++c) {
+            double e = yn[c] - y[c];
+            dn += e * e;
+            yy += y[c] * y[c];
+        }
+        for (int64_t c = 0; c < d; ++c) y[c] = yn[c];
+        if (sqrt(dn) <= tol * fmax(1.0, sqrt(yy))) { st = OR_OK; break; }
+    }
+    for (int64_t c = 0; c < d; ++c) x_next[c] = y[c];
+    if (iters_out) *iters_out = k;
+    free(y); free(yn);
+    return st;
+}
+
 /* ------------------------------------------------------------------------ */
 /* a1-a7 loop (Eq. (2); x^0 = 0 unless given, R11).         */
 /* layout: 0 = dense (A = values, n x d), 1 = CSR.  constraint: 0 = OLS,     */
-/* 1 = l1 ball of radius tau.  x_hist is (T+1) x d and receives x^0..x^T.    */
+/* 1 = l1 ball of radius tau, 2 = l1 penalty lambda = tau (NEXT-2).          */
+/* x_hist is (T+1) x d and receives x^0..x^T.                                 */
 /* inner_iters (optional, T entries) receives the PG step counts.             */
 /* ------------------------------------------------------------------------ */
 int or_ihs_solve(int32_t layout, int64_t n, int64_t d, const double *values,
@@ -415,7 +455,10 @@ int or_ihs_solve(int32_t layout, int64_t n, int64_t d, const double *values,
             st = or_ols_step(d, H, g, x, xn);
         } else {
             int32_t it = 0;
-            st = or_l1ball_step(d, H, g, x, tau, max_inner, tol, power_iters, safety, xn, &it);
+            if (constraint == 1)
+                st = or_l1ball_step(d, H, g, x, tau, max_inner, tol, power_iters, safety, xn, &it);
+            else
+                st = or_lasso_step(d, H, g, x, tau, max_inner, tol, power_iters, safety, xn, &it);
             if (inner_iters) inner_iters[t] = it;
             if (st == OR_ERR_NOT_CONVERGED) st = OR_OK; /* best iterate kept */
         }
@@ -507,6 +550,33 @@ int or_exact_l1ball(int32_t layout, int64_t n, int64_t d, const double *values,
         else or_grad_csr(n, d, row_ptr, col, values, b, x, g);
         int32_t it = 0;
         st = or_l1ball_step(d, G, g, x, tau, max_inner, tol, 50, 1.05, xn, &it);
+        double dn = 0.0, xx = 0.0;
+        for (int64_t k = 0; k < d; ++k) {
+            dn += (xn[k] - x[k]) * (xn[k] - x[k]);
+            xx += xn[k] * xn[k];
+            x[k] = xn[k];
+        }
+        if (sqrt(dn) <= 1e-15 * fmax(1.0, sqrt(xx))) break;
+    }
+    free(G); free(c); free(g); free(xn);
+    return st == OR_ERR_NOT_CONVERGED ? OR_OK : st;
+}
+
+/* NEXT-2: x_OPT of the penalised LASSO, IHS with the exact Hessian A^T A. */
+int or_exact_lasso(int64_t n, int64_t d, const double *A, const double *b, double lambda,
+                   int32_t outer, int32_t max_inner, double tol, double *x)
+{
+    double *G = (double *)malloc(sizeof(double) * (size_t)(d * d));
+    double *c = (double *)malloc(sizeof(double) * (size_t)d);
+    double *g = (double *)malloc(sizeof(double) * (size_t)d);
+    double *xn = (double *)malloc(sizeof(double) * (size_t)d);
+    or_normal_dense(n, d, A, b, G, c);
+    int st = OR_OK;
+    for (int64_t k = 0; k < d; ++k) x[k] = 0.0;
+    for (int32_t t = 0; t < outer; ++t) {
+        or_grad_dense(n, d, A, b, x, g);
+        int32_t it = 0;
+        st = or_lasso_step(d, G, g, x, lambda, max_inner, tol, 50, 1.05, xn, &it);
         double dn = 0.0, xx = 0.0;
         for (int64_t k = 0; k < d; ++k) {
             dn += (xn[k] - x[k]) * (xn[k] - x[k]);

@@ -226,3 +226,81 @@ def test_ihs_csr_matches_dense(oracle_mod):
     np.testing.assert_allclose(xa, xb, rtol=1e-11, atol=1e-12)
     xo = oracle_mod.exact_ols(b=b, csr=csr, d=12)
     np.testing.assert_allclose(xo, np.linalg.lstsq(M.toarray(), b, rcond=None)[0], rtol=1e-10)
+
+
+# ---------------------------------------------------------------- NEXT-2: penalised LASSO
+def lasso_kkt(H, g, y, xt, lam):
+    """Optimality of min 1/2 (y-xt)^T H (y-xt) - g^T (y-xt) + lam ||y||_1:
+    r = H(y - xt) - g must equal -lam sign(y_i) where y_i != 0 and satisfy
+    |r_i| <= lam where y_i = 0.  Returns the largest violation."""
+    r = H @ (y - xt) - g
+    on = y != 0
+    v_on = np.abs(r[on] + lam * np.sign(y[on])).max(initial=0.0)
+    v_off = np.maximum(np.abs(r[~on]) - lam, 0.0).max(initial=0.0)
+    return max(v_on, v_off)
+
+
+def test_lasso_spec_worked_example(oracle_mod):
+    """A = I, b = (3, -1), lambda = 1 -> x = (2, 0) (soft threshold)."""
+    x = oracle_mod.exact_lasso(np.eye(2), np.array([3.0, -1.0]), 1.0)
+    np.testing.assert_allclose(x, [2.0, 0.0], atol=1e-12)
+
+
+def test_lasso_step_identity_is_soft_threshold(oracle_mod):
+    """H = I: the step's minimiser is the l1 prox S_lam(x + g) in closed form
+    (SPEC.md:237), a formula independent of the iteration."""
+    rng = np.random.default_rng(3)
+    d = 40
+    g, xt = rng.standard_normal(d) * 3, rng.standard_normal(d)
+    lam = 1.3
+    y, _, st = oracle_mod.lasso_step(np.eye(d), g, xt, lam)
+    v = xt + g
+    ref = np.sign(v) * np.maximum(np.abs(v) - lam, 0.0)
+    assert st == oracle_mod.OK
+    np.testing.assert_allclose(y, ref, atol=1e-13)
+
+
+def test_lasso_step_kkt_and_special_cases(oracle_mod):
+    rng = np.random.default_rng(4)
+    d = 30
+    Q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    H = (Q * np.geomspace(1.0, 20.0, d)) @ Q.T
+    g, xt = rng.standard_normal(d) * 5, rng.standard_normal(d) * 0.1
+    lam = 2.0
+    y, it, st = oracle_mod.lasso_step(H, g, xt, lam)
+    assert st == oracle_mod.OK and it > 1
+    assert lasso_kkt(H, g, y, xt, lam) <= 1e-9 * max(1.0, np.abs(g).max())
+    assert (y == 0).sum() > 0  # the penalty is active
+    # lambda = 0: the Newton step of OLS
+    y0, _, st0 = oracle_mod.lasso_step(H, g, xt, 0.0)
+    np.testing.assert_allclose(y0, xt + np.linalg.solve(H, g), rtol=1e-9, atol=1e-11)
+    # lambda >= ||H xt + g||_inf: y = 0 satisfies the optimality conditions
+    big = 1.01 * np.abs(H @ xt + g).max()
+    yb, _, stb = oracle_mod.lasso_step(H, g, xt, big)
+    assert stb == oracle_mod.OK and np.abs(yb).max() == 0.0
+    # the cap reports NOT_CONVERGED with the last iterate
+    _, it3, st3 = oracle_mod.lasso_step(H, g, xt, lam, max_inner=3)
+    assert st3 == oracle_mod.ERR_NOT_CONVERGED and it3 == 3
+
+
+def test_exact_lasso_kkt(oracle_mod):
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((300, 12))
+    b = A @ np.r_[np.ones(3), np.zeros(9)] + 0.5 * rng.standard_normal(300)
+    lam = 5.0  # the paper's value (PAPER.md:334)
+    x = oracle_mod.exact_lasso(A, b, lam)
+    G, c = A.T @ A, A.T @ b
+    assert lasso_kkt(G, c, x, np.zeros(12), lam) <= 1e-9 * np.abs(c).max()
+
+
+def test_ihs_lasso_converges(oracle_mod):
+    """Theorem 1 on the penalised form."""
+    rng = np.random.default_rng(6)
+    n, d = 2048, 16
+    A = rng.standard_normal((n, d))
+    b = A @ rng.standard_normal(d) + rng.standard_normal(n)
+    xo = oracle_mod.exact_lasso(A, b, 5.0)
+    xh, inner = oracle_mod.ihs_solve(A, b, m=160, s=1, T=30, constraint="lasso", tau=5.0)
+    errs = [oracle_mod.pred_rel_err(x, xo, A) for x in xh]
+    assert errs[-1] <= 1e-10
+    assert sum(e <= 0.5 ** t for t, e in enumerate(errs) if e > 1e-12) >= 0.8 * sum(e > 1e-12 for e in errs)
