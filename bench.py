@@ -257,7 +257,7 @@ def main():
     r0, r1 = shard_rows(cfg.n, rank, world)
     # ---- inputs, resident in HBM before timing
     xs = synthetic.x_star(cfg, dev)
-    radius = float(xs.abs().sum()) if cfg.constraint == "l1ball" else 0.0
+    radius = float(xs.abs().sum()) if cfg.constraint == "l1ball" else (cfg.lam if cfg.constraint == "lasso" else 0.0)
     if cfg.layout == "dense":
         A = synthetic.dense_A(cfg, dev, rows=(r0, r1))
         b = (A @ xs + synthetic.noise(cfg, dev)[r0:r1]).contiguous()
@@ -399,7 +399,7 @@ def main():
         x = torch.zeros(d, dtype=torch.float64).numpy()
         it = 0
         t0 = time.perf_counter()
-        kw = dict(constraint="l1ball", tau=radius) if cfg.constraint == "l1ball" else {}
+        kw = dict(constraint=cfg.constraint, tau=radius) if cfg.constraint in ("l1ball", "lasso") else {}
         while True:
             xh_o, _ = oracle.ihs_solve(A_np, b_np, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=it, x0=x, **kw)
             x = xh_o[-1]

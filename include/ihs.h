@@ -183,6 +183,17 @@ ihs_status ihs_l1ball_update(ihs_ctx ctx, const double *H, const double *g, int6
                              const double *x, double radius, const ihs_inner_cfg *cfg,
                              double *x_next, int32_t *inner_iters);
 
+/* NEXT-2, penalised LASSO (section 3: 1/2||Ax-b||^2 +
+ * lambda ||x||_1; the penalty is carried into every IHS step, reading R23):
+ * x_next = argmin_y 1/2 (y-x)^T H (y-x) - g^T (y-x) + lambda ||y||_1 by
+ * accelerated proximal gradient (soft threshold at lambda / L; L, start,
+ * stopping rule and cap as for the ball, reading R10).  lambda >= 0;
+ * d <= 256 (else IHS_ERR_UNSUPPORTED).  inner_iters / statuses as for
+ * ihs_l1ball_update. */
+ihs_status ihs_lasso_update(ihs_ctx ctx, const double *H, const double *g, int64_t d,
+                            const double *x, double lambda, const ihs_inner_cfg *cfg,
+                            double *x_next, int32_t *inner_iters);
+
 /* a1-a7: n_iters IHS steps from x0 (NULL = 0), hash iterations iter0.. .
  * A/b/x0/x/x_hist may be HOST or DEVICE pointers (detected per pointer); host
  * inputs are copied in and results copied out inside the call.  x_hist
@@ -200,6 +211,12 @@ ihs_status ihs_solve_l1ball(ihs_ctx ctx, const ihs_matrix *A, const double *b, d
                             const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0,
                             const ihs_inner_cfg *cfg, const double *x0, double *x,
                             double *x_hist, ihs_iter_record *trace);
+
+/* NEXT-2: the same loop for the penalised LASSO (ihs_lasso_update inner step). */
+ihs_status ihs_solve_lasso(ihs_ctx ctx, const ihs_matrix *A, const double *b, double lambda,
+                           const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0,
+                           const ihs_inner_cfg *cfg, const double *x0, double *x,
+                           double *x_hist, ihs_iter_record *trace);
 
 /* a7 bookkeeping: err2[k] = ||A_local (X[k] - xref)||^2 and ref2 = ||A_local xref||^2
  * for k < count (X is count x d, device).  One pass over A.  Summed across

@@ -9,7 +9,8 @@ cannot run, every call raises.
 
 Names follow the C ABI: ``ihs_hash``, ``ihs_sketch``, ``ihs_grad``,
 ``ihs_sketch_grad``, ``ihs_gram``, ``ihs_ols_update``, ``ihs_l1ball_update``,
-``ihs_solve_ols``, ``ihs_solve_l1ball``, ``ihs_pred_err2``.
+``ihs_solve_ols``, ``ihs_solve_l1ball``, ``ihs_pred_err2``; NEXT-2 (penalised LASSO):
+``ihs_lasso_update``, ``ihs_solve_lasso``.
 """
 from __future__ import annotations
 
@@ -83,6 +84,11 @@ _EXPORTS = {
     "ihs_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "ihs_l1ball_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_double,
                                     C.POINTER(InnerCfg), C.c_void_p, C.c_void_p]),
+    "ihs_lasso_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_double,
+                                   C.POINTER(InnerCfg), C.c_void_p, C.c_void_p]),
+    "ihs_solve_lasso": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.c_void_p, C.c_double, C.POINTER(SketchSpec),
+                                  C.c_int32, C.c_uint64, C.POINTER(InnerCfg), C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.POINTER(IterRecord)]),
     "ihs_solve_ols": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.c_void_p, C.POINTER(SketchSpec), C.c_int32,
                                 C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(IterRecord)]),
     "ihs_solve_l1ball": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.c_void_p, C.c_double, C.POINTER(SketchSpec),
@@ -338,6 +344,17 @@ def ihs_l1ball_update(H, g, x, radius, cfg: InnerCfg | None = None, out=None, in
     return xn
 
 
+def ihs_lasso_update(H, g, x, lam, cfg: InnerCfg | None = None, out=None, inner=None,
+                     ctx: Context | None = None):
+    """NEXT-2: argmin_y 1/2 (y-x)^T H (y-x) - g^T (y-x) + lam ||y||_1."""
+    ctx = ctx or default_context(H.device)
+    xn = out if out is not None else torch.empty_like(x)
+    cfg = cfg or inner_cfg()
+    _check(lib().ihs_lasso_update(ctx._bind(), _p(H), _p(g), x.numel(), _p(x), float(lam), C.byref(cfg),
+                                  _p(xn), _p(inner)), "ihs_lasso_update")
+    return xn
+
+
 # ------------------------------------------------------------------ a1-a7
 def _solve(kind, A, b, spec, n_iters, iter0, x0, radius, cfg, trace, ctx, x_out, x_hist):
     A = A if isinstance(A, (Dense, Csr)) else as_matrix(A)
@@ -357,8 +374,9 @@ def _solve(kind, A, b, spec, n_iters, iter0, x0, radius, cfg, trace, ctx, x_out,
                                  _p(x_hist), rp)
     else:
         c = cfg or inner_cfg()
-        st = lib().ihs_solve_l1ball(ctx._bind(), C.byref(mc), _p(b), float(radius), C.byref(sp), n_iters, iter0,
-                                    C.byref(c), _p(x0), _p(x_out), _p(x_hist), rp)
+        fn = lib().ihs_solve_lasso if kind == "lasso" else lib().ihs_solve_l1ball
+        st = fn(ctx._bind(), C.byref(mc), _p(b), float(radius), C.byref(sp), n_iters, iter0, C.byref(c), _p(x0),
+                _p(x_out), _p(x_hist), rp)
     if st not in (OK, ERR_NOT_CONVERGED):
         raise IhsError(st, f"ihs_solve_{kind}")
     out = {"x": x_out, "x_hist": x_hist, "status": st}
@@ -379,6 +397,12 @@ def ihs_solve_l1ball(A, b, radius: float, spec: Spec, n_iters: int, iter0: int =
                      trace=False, ctx=None, x_out=None, x_hist=None):
     """T IHS steps over {||x||_1 <= radius} with the PG inner solver."""
     return _solve("l1", A, b, spec, n_iters, iter0, x0, radius, cfg, trace, ctx, x_out, x_hist)
+
+
+def ihs_solve_lasso(A, b, lam: float, spec: Spec, n_iters: int, iter0: int = 0, cfg=None, x0=None,
+                    trace=False, ctx=None, x_out=None, x_hist=None):
+    """NEXT-2: T IHS steps for 1/2||Ax-b||^2 + lam ||x||_1 (penalty kept in every step)."""
+    return _solve("lasso", A, b, spec, n_iters, iter0, x0, lam, cfg, trace, ctx, x_out, x_hist)
 
 
 def ihs_pred_err2(A, X: torch.Tensor, xref: torch.Tensor, ctx: Context | None = None):

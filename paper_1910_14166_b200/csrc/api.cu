@@ -406,12 +406,13 @@ ihs_inner_cfg default_inner() {
   return k;
 }
 
+// prox = 0: l1 ball of radius `radius`; prox = 1: penalty lambda = `radius` (NEXT-2)
 ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const double *x, double radius,
-                   const ihs_inner_cfg *cfg, double *xn, int32_t *inner) {
+                   const ihs_inner_cfg *cfg, double *xn, int32_t *inner, int prox = 0) {
   ihs_inner_cfg k = cfg ? *cfg : default_inner();
   if (k.max_inner < 1 || k.power_iters < 1 || !(k.inner_tol >= 0.0) || !(k.lip_safety > 0.0))
     return IHS_ERR_INVALID_ARGUMENT;
-  if (!pg_supported(d)) return IHS_ERR_UNSUPPORTED;
+  if (!pg_supported(d) || (prox && !lasso_supported(d))) return IHS_ERR_UNSUPPORTED;
   // warm-started power iteration across calls with the same d (IHS_PG_WARM=0 off)
   static const bool warm_env = !getenv("IHS_PG_WARM") || std::strcmp(getenv("IHS_PG_WARM"), "0") != 0;
   double *ev = nullptr;
@@ -420,7 +421,7 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
   const bool warm = warm_env && c->pg_warm_d == d;
   Prof pr(c, IHS_K_PG);
   IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.inner_tol, k.lip_safety, xn, inner,
-                                ev, c->d_status, c->stream, lc_of(c), warm));
+                                ev, c->d_status, c->stream, lc_of(c), warm, prox));
   if (warm_env) c->pg_warm_d = d;
   return IHS_OK;
 }
@@ -456,7 +457,7 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
   IHS_TRY(check_matrix(A_in));
   IHS_TRY(check_spec(spec));
   if (T < 0 || !b_in || !x_out) return IHS_ERR_INVALID_ARGUMENT;
-  if (constraint == 1 && !(radius >= 0.0)) return IHS_ERR_INVALID_ARGUMENT;
+  if (constraint >= 1 && !(radius >= 0.0)) return IHS_ERR_INVALID_ARGUMENT;
   const int64_t n = A_in->n_rows, d = A_in->n_cols, m = spec->m;
   cudaStream_t st = c->stream;
   ihs_matrix A = *A_in;
@@ -506,7 +507,7 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
     IHS_TRY(scratch(c, S_XH, (size_t)(T + 1) * d * 8, &xh));
   }
   int32_t *inner_dev = nullptr;
-  if (constraint == 1) IHS_TRY(scratch(c, S_MISC, (size_t)std::max(T, 1) * 4, &inner_dev));
+  if (constraint >= 1) IHS_TRY(scratch(c, S_MISC, (size_t)std::max(T, 1) * 4, &inner_dev));
   if (x0_in) {
     IHS_CUDA(cudaMemcpyAsync(xh, x0_in, (size_t)d * 8, is_host_ptr(x0_in) ? cudaMemcpyHostToDevice
                                                                            : cudaMemcpyDeviceToDevice, st));
@@ -534,7 +535,7 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
     IHS_TRY(gram_impl(c, SA, m, d, scale, H));
     if (trace) cudaEventRecord(ev[3], st);
     if (constraint == 0) IHS_TRY(ols_impl(c, H, g, d, x, xn));
-    else IHS_TRY(l1_impl(c, H, g, d, x, radius, cfg, xn, inner_dev + t));
+    else IHS_TRY(l1_impl(c, H, g, d, x, radius, cfg, xn, inner_dev + t, constraint == 2 ? 1 : 0));
     if (trace) {
       cudaEventRecord(ev[4], st);
       IHS_CUDA(cudaEventSynchronize(ev[4]));
@@ -546,7 +547,7 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
       r.t_gram = ms[2];
       r.t_solve = ms[3];
       r.inner_iters = 0;
-      if (constraint == 1) cudaMemcpy(&r.inner_iters, inner_dev + t, 4, cudaMemcpyDeviceToHost);
+      if (constraint >= 1) cudaMemcpy(&r.inner_iters, inner_dev + t, 4, cudaMemcpyDeviceToHost);
       ihs_status s = sync_status(c);
       r.status = s;
       if (s == IHS_ERR_NOT_SPD || (s != IHS_OK && s != IHS_ERR_NOT_CONVERGED)) {
@@ -772,6 +773,21 @@ ihs_status ihs_l1ball_update(ihs_ctx c, const double *H, const double *gv, int64
   if (!c || !H || !gv || !x || !xn || d < 1 || !(radius >= 0.0)) return IHS_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
   return l1_impl(c, H, gv, d, x, radius, cfg, xn, inner);
+}
+
+ihs_status ihs_lasso_update(ihs_ctx c, const double *H, const double *gv, int64_t d, const double *x, double lambda,
+                            const ihs_inner_cfg *cfg, double *xn, int32_t *inner) {
+  if (!c || !H || !gv || !x || !xn || d < 1 || !(lambda >= 0.0)) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return l1_impl(c, H, gv, d, x, lambda, cfg, xn, inner, 1);
+}
+
+ihs_status ihs_solve_lasso(ihs_ctx c, const ihs_matrix *A, const double *b, double lambda,
+                           const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0, const ihs_inner_cfg *cfg,
+                           const double *x0, double *x, double *x_hist, ihs_iter_record *trace) {
+  if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return solve_impl(c, 2, A, b, lambda, spec, n_iters, iter0, cfg, x0, x, x_hist, trace);
 }
 
 ihs_status ihs_solve_ols(ihs_ctx c, const ihs_matrix *A, const double *b, const ihs_sketch_spec *spec, int32_t n_iters,

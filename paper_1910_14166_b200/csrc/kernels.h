@@ -127,13 +127,16 @@ cudaError_t launch_ols_cg(const double *H, const double *g, int64_t d, const dou
 // ---- a6 l1 ball: projected gradient -----------------------------------------
 size_t pg_scratch_bytes(int64_t d);
 bool pg_supported(int64_t d);
+bool lasso_supported(int64_t d);
 int pg_cluster_size(int64_t d);
 // scratch (d doubles, may be null) keeps the power iteration's last vector;
-// warm_start = it holds one from an earlier call with the same d.
+// warm_start = it holds one from an earlier call with the same d.  prox = 1:
+// the penalised form (NEXT-2), radius is lambda and the projection becomes the
+// soft threshold at lambda / L (d <= 256 only: cudaErrorNotSupported beyond).
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
                                  int max_inner, int power_iters, double tol, double safety, double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
-                                 LaunchCounter lc, bool warm_start = false);
+                                 LaunchCounter lc, bool warm_start = false, int prox = 0);
 
 // ---- a7 error norms ----------------------------------------------------------
 cudaError_t launch_pred_err2(int layout, int64_t n, int64_t d, const double *values, const int64_t *row_ptr,

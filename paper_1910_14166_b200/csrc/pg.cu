@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
                                                       int d, const double *__restrict__ x, double radius,
                                                       int max_inner, int power_iters, double tol, double safety,
                                                       double *x_next, int32_t *inner_iters, int *status, int accel,
-                                                      double *evec, int warm) {
+                                                      double *evec, int warm, int prox) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = (int)cluster.num_blocks();
@@ -426,10 +426,12 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
       zv[k] = q < d ? z[q] : 0.0;
       av[k] = fabs(zv[k]);
     }
-    const double n1 = wsum_k(av);
-    double theta = 0.0;
-    const bool proj = n1 > radius;
-    if (proj) {  // Michelot's fixed point (reading R19), warp-local
+    // prox (NEXT-2, reading R23): soft threshold at lambda / L, lambda = radius;
+    // else the projection onto the ball of that radius
+    const double n1 = prox ? 0.0 : wsum_k(av);
+    double theta = prox ? radius / L : 0.0;
+    const bool proj = prox || n1 > radius;
+    if (!prox && proj) {  // Michelot's fixed point (reading R19), warp-local
       theta = (n1 - radius) / (double)d;
       double cprev = (double)d;
       for (int guard = 0; guard <= d; ++guard) {
@@ -512,6 +514,8 @@ int pg_cluster_size(int64_t d) {
   return 0;
 }
 
+bool lasso_supported(int64_t d) { return d <= 256 && pg_cluster_size(d) > 0; }
+
 bool pg_supported(int64_t d) { return pg_cluster_size(d) > 0 || (size_t)5 * d * 8 <= 200 * 1024; }
 
 size_t pg_scratch_bytes(int64_t d) { return (size_t)d * 8; }
@@ -519,7 +523,7 @@ size_t pg_scratch_bytes(int64_t d) { return (size_t)d * 8; }
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
                                  int max_inner, int power_iters, double tol, double safety, double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
-                                 LaunchCounter lc, bool warm_start) {
+                                 LaunchCounter lc, bool warm_start, int prox) {
   static const bool use_cluster = !getenv("IHS_PG_SINGLE");
   static const bool warp_version = !getenv("IHS_PG_CTA");
   const int cs = use_cluster ? pg_cluster_size(d) : 0;
@@ -546,17 +550,20 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     lc.add();
-    if (!wv)
+    if (!wv) {
+      if (prox) return cudaErrorNotSupported;
       return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
                                 x_next, inner_iters, status);
+    }
     static const int accel = (getenv("IHS_PG_PLAIN") && std::strcmp(getenv("IHS_PG_PLAIN"), "0") != 0) ? 0 : 1;
     // warm start (scratch = d doubles holding the last eigenvector estimate):
     // a dozen power steps from it instead of power_iters from 1/sqrt(d)
     const bool warm_ok = warm_start && scratch;
     const int piters = warm_ok ? std::min(power_iters, 12) : power_iters;
     return cudaLaunchKernelEx(&cfg, wkern, H, g, (int)d, x, radius, max_inner, piters, tol, safety, x_next,
-                              inner_iters, status, accel, scratch, warm_ok ? 1 : 0);
+                              inner_iters, status, accel, scratch, warm_ok ? 1 : 0, prox);
   }
+  if (prox) return cudaErrorNotSupported;
   const size_t smem = (size_t)5 * d * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
   IHS_SMEM_ATTR(pg_l1ball_kernel, smem);

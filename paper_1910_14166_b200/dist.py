@@ -51,6 +51,9 @@ class CudaOps:
     def l1(self, H, g, x, tau, cfg, xn, inner):
         P.ihs_l1ball_update(H, g, x, tau, cfg=cfg, out=xn, inner=inner, ctx=self.ctx)
 
+    def lasso(self, H, g, x, lam, cfg, xn, inner):
+        P.ihs_lasso_update(H, g, x, lam, cfg=cfg, out=xn, inner=inner, ctx=self.ctx)
+
     def err2(self, A, X, xref):
         return P.ihs_pred_err2(A, X, xref, ctx=self.ctx)
 
@@ -85,6 +88,8 @@ class ShardedIHS:
         self.ops.gram(self.SA, self.H)
         if self.constraint == "ols":
             self.ops.ols(self.H, self.g, x, xn)
+        elif self.constraint == "lasso":  # NEXT-2: radius carries lambda
+            self.ops.lasso(self.H, self.g, x, self.radius, self.cfg, xn, self.inner)
         else:
             self.ops.l1(self.H, self.g, x, self.radius, self.cfg, xn, self.inner)
         return xn

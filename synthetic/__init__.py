@@ -9,6 +9,7 @@ configs (DESIGN.md section 5 states the recipe):
   C3 sparse    CSR 2^23 x 1024, iid Bernoulli(1e-3) mask, values N(0,1)
   C4 lasso     dense 2^21 x 256, iid Student-t(3); x* 10-sparse +-1; tau = ||x*||_1
   C5 large     dense 2^25 x 96, iid N(0,1)
+  C4P          C4's data with the penalised LASSO, lambda = 5 (NEXT-2)
 
 Every draw comes from a torch.Generator seeded by (config seed, substream), on
 the device the caller names.  The same bytes are handed to both the oracle and
@@ -36,12 +37,13 @@ class Config:
     m: int
     s: int
     T: int               # IHS iterations named by BASELINE.json
-    constraint: str      # "ols" | "l1ball"
+    constraint: str      # "ols" | "l1ball" | "lasso" (NEXT-2)
     density: float = 1.0
     sigma: float = 1.0
     sparse_xstar: int = 0
     hash_seed: int = 0
     data_seed: int = 0
+    lam: float = 0.0     # l1 penalty of the "lasso" constraint
 
     def scaled(self, n: int, **kw) -> "Config":
         """Same recipe at a reduced row count (parity-test sizes)."""
@@ -63,6 +65,10 @@ CONFIGS = {
     "C4": Config("C4", 1 << 21, 256, "dense", "student_t3", "countsketch", 2048, 1, 25, "l1ball",
                  sparse_xstar=10, data_seed=4),
     "C5": Config("C5", 1 << 25, 96, "dense", "normal", "sjlt", 4096, 8, 20, "ols", data_seed=5),
+    # NEXT-2: the paper's penalised objective with lambda = 5.0
+    # on C4's data (not a BASELINE.json config)
+    "C4P": Config("C4P", 1 << 21, 256, "dense", "student_t3", "countsketch", 2048, 1, 25, "lasso",
+                  sparse_xstar=10, data_seed=4, lam=5.0),
 }
 
 
@@ -191,4 +197,5 @@ def problem(cfg: Config, device="cpu"):
         out["csr"] = (rp, cl, vl)
         out["b"] = csr_matvec(rp, cl, vl, xs) + w
     out["tau"] = float(xs.abs().sum()) if cfg.constraint == "l1ball" else 0.0
+    out["lam"] = cfg.lam
     return out

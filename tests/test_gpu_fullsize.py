@@ -54,7 +54,7 @@ def check_hash(P, oracle_mod, cfg, t, windows):
         np.testing.assert_array_equal(sg.cpu().numpy(), so)
 
 
-@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C4", "C5", "C4P"])
 def test_dense_full_size(P, oracle_mod, name):
     from paper_1910_14166_b200.dist import CudaOps, ShardedIHS
     cfg, prob = dense_full(name)
@@ -64,7 +64,7 @@ def test_dense_full_size(P, oracle_mod, name):
     ctx = P.Context(0)
     spec = P.Spec(m=cfg.m, s=cfg.s)
     S = ShardedIHS(P.Dense(prob["A"]), prob["b"], spec, ops=CudaOps(ctx), constraint=cfg.constraint,
-                   radius=prob["tau"])
+                   radius=prob["lam"] if cfg.constraint == "lasso" else prob["tau"])
     rng = np.random.default_rng(0)
     x = torch.from_numpy(rng.standard_normal(d) * 0.1).to(DEV)
     xn = torch.empty_like(x)
@@ -88,12 +88,16 @@ def test_dense_full_size(P, oracle_mod, name):
     assert rel_fro(H, oracle_mod.gram(SA)) <= 1e-12
     if cfg.constraint == "ols":
         xo = oracle_mod.ols_step(H, g, xh)
+    elif cfg.constraint == "lasso":
+        xo, _, st = oracle_mod.lasso_step(H, g, xh, prob["lam"])
+        assert st == oracle_mod.OK
     else:
         xo, _, st = oracle_mod.l1ball_step(H, g, xh, prob["tau"])
         assert st == oracle_mod.OK
     assert np.linalg.norm(xn.cpu().numpy() - xo) <= 1e-10 * np.linalg.norm(xo - xh) + 1e-14 * np.linalg.norm(xo)
-    if name in ("C2", "C4"):  # one whole oracle IHS step at full size (seconds)
-        kw = dict(constraint="l1ball", tau=prob["tau"]) if cfg.constraint == "l1ball" else {}
+    if name in ("C2", "C4", "C4P"):  # one whole oracle IHS step at full size (seconds)
+        kw = {"l1ball": dict(constraint="l1ball", tau=prob["tau"]),
+              "lasso": dict(constraint="lasso", tau=prob["lam"])}.get(cfg.constraint, {})
         xh_o, _ = oracle_mod.ihs_solve(A, b, m=cfg.m, s=cfg.s, T=1, iter0=t, x0=xh, **kw)
         assert oracle_mod.pred_rel_err(xn.cpu().numpy(), xh_o[1], A) <= 1e-9
 

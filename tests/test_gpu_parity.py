@@ -276,6 +276,43 @@ def test_ihs_l1ball_scaled_C4(P, oracle_mod):
     assert all(i >= 1 for i in its)
 
 
+@pytest.mark.parametrize("d,lam", [(16, 0.5), (256, 5.0), (64, 50.0), (5, 0.0), (100, 1e6)])
+def test_lasso_update(P, oracle_mod, d, lam):
+    """NEXT-2 inner step (reading R23) against the oracle's proximal gradient."""
+    rng = np.random.default_rng(d + 1)
+    H = spd(rng, d)
+    g = rng.standard_normal(d) * 10
+    x = rng.standard_normal(d) * 0.1
+    inner = torch.zeros(1, dtype=torch.int32, device=DEV)
+    xn = P.ihs_lasso_update(torch.from_numpy(H).to(DEV), torch.from_numpy(g).to(DEV), torch.from_numpy(x).to(DEV),
+                            lam, inner=inner).cpu().numpy()
+    xo, it, st = oracle_mod.lasso_step(H, g, x, lam)
+    assert st == oracle_mod.OK
+    assert np.linalg.norm(xn - xo) <= 1e-10 * max(1.0, np.linalg.norm(xo))
+    assert ((xn == 0) == (xo == 0)).all()  # the same support (exact zeros from the soft threshold)
+    assert int(inner.item()) >= 1
+
+
+def test_lasso_update_unsupported_d(P):
+    d = 300
+    H = torch.eye(d, dtype=torch.float64, device=DEV)
+    v = torch.zeros(d, dtype=torch.float64, device=DEV)
+    with pytest.raises(P.IhsError):
+        P.ihs_lasso_update(H, v, v, 1.0)
+
+
+def test_ihs_lasso_scaled_C4P(P, oracle_mod):
+    """NEXT-2: the penalised LASSO loop (lambda = 5) against the oracle."""
+    cfg = synthetic.CONFIGS["C4P"].scaled(1 << 15)
+    prob = synthetic.problem(cfg, "cpu")
+    A, b = prob["A"].numpy(), prob["b"].numpy()
+    T = 8
+    out = P.ihs_solve_lasso(prob["A"].to(DEV), prob["b"].to(DEV), cfg.lam, P.Spec(m=cfg.m), T, trace=True)
+    xo, _ = oracle_mod.ihs_solve(A, b, m=cfg.m, s=1, T=T, constraint="lasso", tau=cfg.lam)
+    assert iterate_parity(A, out["x_hist"].cpu().numpy(), xo, oracle_mod) <= 1e-9
+    assert all(r["inner_iters"] >= 1 for r in out["trace"])
+
+
 def test_solve_with_host_buffers(P, oracle_mod):
     """e2e path: host A/b/x, copies inside the call."""
     cfg = synthetic.CONFIGS["C1"]
