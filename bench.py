@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-10 solve")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: host-staged all-reduce, for testing the "
+                         "sharded path with IHS_BENCH_SHARE_GPU=1 on one GPU)")
     return ap.parse_args()
 
 
@@ -249,10 +252,16 @@ def main():
     from paper_1910_14166_b200.dist import CudaOps, ShardedIHS, shard_rows
 
     rank, world, local = dist_env()
+    if os.environ.get("IHS_BENCH_SHARE_GPU") == "1":  # test mode: every rank on cuda:0
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    nccl = args.dist_backend == "nccl"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if nccl:
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     cfg = synthetic.CONFIGS[args.config]
     r0, r1 = shard_rows(cfg.n, rank, world)
     # ---- inputs, resident in HBM before timing
@@ -282,8 +291,12 @@ def main():
     xb = torch.empty_like(xa)
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if nccl:
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize()
 
     t = 0
@@ -353,7 +366,9 @@ def main():
         del xh
     # ---- e2e: the public solve call with HOST (pinned) buffers, copies inside
     e2e = None
-    if not args.no_e2e and cfg.layout == "dense" and cfg.constraint == "ols":
+    if not args.no_e2e and world > 1 and not nccl:
+        e2e = {"value": None, "unit": UNIT, "error": "the e2e solve all-reduces through NCCL; skipped with gloo"}
+    elif not args.no_e2e and cfg.layout == "dense" and cfg.constraint == "ols":
         try:
             T_e2e = (ttt or {}).get("iterations") or 30
             A_h = torch.empty(A.shape, dtype=torch.float64, pin_memory=True)

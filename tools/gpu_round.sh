@@ -2,7 +2,7 @@
 # One gpurun call: GPU tests, smoke, bench on every config, the reference arm,
 # ncu launch lists and one `ncu --set full` capture per dominant kernel.
 # Outputs under gpurun_out/$TAG/ (summarised into profiles/ by tools/ncu_summary.py).
-# usage: gpurun -- 'bash tools/gpu_round.sh TAG [parts...]'   parts: probe tests smoke bench ncu
+# usage: gpurun -- 'bash tools/gpu_round.sh TAG [parts...]'   parts: probe tests smoke bench dist ncu
 TAG=${1:-r01}
 shift
 PARTS=${*:-"tests smoke bench ncu"}
@@ -28,6 +28,10 @@ if has bench; then
     timeout 600 python bench.py --config $C --steps 10 --warmup 3 --no-cpu > $OUT/bench_$C.json 2> $OUT/bench_$C.err
   done
   timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
+fi
+if has dist; then  # the N > 1 bench path on ONE GPU: 2 ranks share cuda:0, gloo all-reduce (no kernel waits on another rank)
+  IHS_BENCH_SHARE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 \
+    --master-port 29511 bench.py --gpus 2 --steps 5 --warmup 3 --dist-backend gloo --no-cpu > $OUT/bench_2ranks_gloo.json 2> $OUT/bench_2ranks_gloo.err
 fi
 if has ncu; then
   NCU=/usr/local/cuda/bin/ncu
