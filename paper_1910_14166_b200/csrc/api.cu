@@ -286,8 +286,18 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
         return IHS_OK;
       };
       if (!hit) IHS_TRY(sort_all(key, hist, tiles, perm, st));
+      // few buckets with long row lists (small m): split every bucket's rows
+      // into nseg segments (grid.z) so a launch still fills the GPU; the
+      // segment partials are summed in order afterwards (SA then agrees with
+      // the oracle to rounding instead of bit for bit, R3)
+      int nseg = 1;
+      if (tma && M * nb < 4 * (int64_t)c->num_sms && n / std::max<int64_t>(M, 1) >= 1024)
+        nseg = (int)std::max<int64_t>(1, std::min<int64_t>((7 * (int64_t)c->num_sms + M * nb - 1) / (M * nb),
+                                                           n / (M * 512)));
       double *gpart = nullptr;
-      if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)M * d * 8, &gpart));
+      if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)M * d * 8 * nseg, &gpart));
+      double *sapart = nullptr;
+      if (nseg > 1) IHS_TRY(scratch(c, S_SJLT, (size_t)nseg * nb * M * d * 8, &sapart));
       const double scale = spec_scale(spec);
       // Speculative prefetch of iteration iter + 1 into the other set, on the
       // side stream, issued BEFORE this iteration's gathers: the sort kernels
@@ -333,8 +343,12 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
           bst.tiles = ts;
           bst.perm = ps;
           bst.sa = M * d;
-          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp, scale,
-                                        st, lc_of(c), cnt, bst));
+          bst.nseg = nseg;
+          bst.seg_sa = (int64_t)cnt * M * d;
+          IHS_CUDA(launch_cs_gather_tma(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x,
+                                        nseg > 1 ? sapart : SAj, gp, nseg > 1 ? 1.0 : scale, st, lc_of(c), cnt, bst));
+          if (nseg > 1)
+            IHS_CUDA(launch_sum_splits(sapart, (int64_t)cnt * M * d, nseg, scale, SAj, st, lc_of(c)));
         } else if (c->gather == 2 && cs_gather_async_supported(d, A->values)) {
           IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp,
                                           scale, st, lc_of(c)));
@@ -345,7 +359,7 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       }
       if (fuse) {
         Prof pr(c, IHS_K_REDUCE);
-        IHS_CUDA(launch_reduce_rows(gpart, M, d, g, st, lc_of(c)));
+        IHS_CUDA(launch_reduce_rows(gpart, M * nseg, d, g, st, lc_of(c)));
       }
     } else if (use_stream) {
       double *part;

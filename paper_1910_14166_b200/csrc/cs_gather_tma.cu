@@ -85,8 +85,17 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
   uint32_t *rid = reinterpret_cast<uint32_t *>(empty + kMaxStages);                   // [kStages][kRows]
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t beg = scanned_at(hist, tile_sums, (int64_t)b * nchunks);
-  const int64_t end = (b + 1 < m) ? scanned_at(hist, tile_sums, (int64_t)(b + 1) * nchunks) : n;
+  int64_t beg = scanned_at(hist, tile_sums, (int64_t)b * nchunks);
+  int64_t end = (b + 1 < m) ? scanned_at(hist, tile_sums, (int64_t)(b + 1) * nchunks) : n;
+  if (gridDim.z > 1) {
+    // few buckets: segment z of the bucket's (ascending) rows -> partial sums
+    // in SA + z * bst.seg_sa / gpart + z * m * d, summed in segment order after
+    const int64_t L = end - beg, z = blockIdx.z, nz = gridDim.z;
+    end = beg + L * (z + 1) / nz;
+    beg = beg + L * z / nz;
+    SA += z * bst.seg_sa;
+    if (gpart) gpart += z * (int64_t)m * d;
+  }
   const int64_t len = end - beg;
   const int64_t nb = (len + kRows - 1) / kRows;
   const uint32_t row_bytes = (uint32_t)d * 8u;
@@ -234,11 +243,12 @@ void launch_tma_t(size_t smem, int nst, int nb, GatherBatchStrides bst, const do
                   const double *bvec, const double *x, double *SA, double *gpart, double scale, cudaStream_t st) {
   if (nb == 1) {
     IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC, true>), smem);
-    cs_gather_tma_kernel<FUSE, NC, true><<<dim3((unsigned)m, 1), kConsumers + 32, smem, st>>>(
+    cs_gather_tma_kernel<FUSE, NC, true><<<dim3((unsigned)m, 1, (unsigned)bst.nseg), kConsumers + 32, smem, st>>>(
         A, n, d, m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, nst, bst);
   } else {
     IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC, false>), smem);
-    cs_gather_tma_kernel<FUSE, NC, false><<<dim3((unsigned)m, (unsigned)nb), kConsumers + 32, smem, st>>>(
+    cs_gather_tma_kernel<FUSE, NC, false><<<dim3((unsigned)m, (unsigned)nb, (unsigned)bst.nseg), kConsumers + 32, smem,
+                                            st>>>(
         A, n, d, m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, nst, bst);
   }
 }

@@ -56,6 +56,11 @@ cudaError_t launch_cs_gather_async(const double *A, int64_t n, int64_t d, int64_
 // gradient (gpart != null) rides on entry 0.
 struct GatherBatchStrides {
   int64_t hist = 0, tiles = 0, perm = 0, sa = 0;
+  // nseg > 1 (few buckets, long rows lists): grid.z splits every bucket's rows
+  // into nseg contiguous segments; segment z writes SA + z * seg_sa and
+  // gpart + z * m * d (partials, reduced by the caller in segment order).
+  int nseg = 1;
+  int64_t seg_sa = 0;
 };
 bool cs_gather_tma_supported(int64_t d, const void *A);
 cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,

@@ -90,6 +90,22 @@ def test_sjlt_dense(P, oracle_mod, n, d, m, s):
     assert rel_fro(SA, ref) <= 1e-12
 
 
+@pytest.mark.parametrize("n,d,m,s", [(1 << 20, 32, 64, 1), (1 << 20, 24, 64, 4), ((1 << 19) + 333, 90, 90, 1)])
+def test_gather_segmented_small_m(P, oracle_mod, n, d, m, s):
+    """Few buckets with long row lists: each bucket's rows are split into
+    segments summed in order (not bit-exact, R3); sketch and fused gradient."""
+    rng = np.random.default_rng(n + d)
+    A = rng.standard_normal((n, d))
+    b = rng.standard_normal(n)
+    x = rng.standard_normal(d) * 0.1
+    Ad = torch.from_numpy(A).to(DEV)
+    _, SA, g = P.ihs_sketch_grad(Ad, P.Spec(m=m, s=s, seed=0), 2, torch.from_numpy(b).to(DEV),
+                                 torch.from_numpy(x).to(DEV))
+    ref = oracle_mod.sketch_dense(A, 0, 2, m, s)
+    assert rel_fro(SA.cpu().numpy(), ref) <= 1e-12
+    assert (np.abs(g.cpu().numpy() - oracle_mod.grad_dense(A, b, x)) <= grad_bound(A, b, x)).all()
+
+
 def csr_case(n, d, p, seed):
     cfg = synthetic.Config("csr", n, d, "csr", "normal", "sjlt", 64, 4, 1, "ols", density=p, data_seed=seed)
     rp, cl, vl = synthetic.csr_A(cfg, "cpu")
