@@ -12,6 +12,43 @@
 namespace ihs {
 
 namespace {
+// L2 eviction-priority policies: the CSR arrays and b stream through L2 once
+// (evict_first); the reductions into SA keep its lines resident (evict_last),
+// so the 34 M REDs of C3 do not re-fetch SA lines the stream pushed out.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+template <typename T>
+__device__ __forceinline__ T ld_stream(const T *p, uint64_t pol);
+template <>
+__device__ __forceinline__ double ld_stream<double>(const double *p, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <>
+__device__ __forceinline__ int32_t ld_stream<int32_t>(const int32_t *p, uint64_t pol) {
+  int32_t v;
+  asm volatile("ld.global.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+template <>
+__device__ __forceinline__ int64_t ld_stream<int64_t>(const int64_t *p, uint64_t pol) {
+  int64_t v;
+  asm volatile("ld.global.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void red_keep(double *p, double v, uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
+
 template <bool SKETCH, bool GRAD, bool GSMEM>
 __global__ void __launch_bounds__(256) csr_sketch_grad_kernel(int64_t n, int d, const int64_t *__restrict__ row_ptr,
                                                               const int32_t *__restrict__ col,
@@ -24,13 +61,14 @@ __global__ void __launch_bounds__(256) csr_sketch_grad_kernel(int64_t n, int d, 
     for (int c = threadIdx.x; c < d; c += blockDim.x) gs[c] = 0.0;
     __syncthreads();
   }
+  const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+    const int64_t e0 = ld_stream(row_ptr + i, pf), e1 = ld_stream(row_ptr + i + 1, pf);
     if (e1 == e0) continue;
     if (GRAD) {
       double dot = 0.0;
-      for (int64_t e = e0; e < e1; ++e) dot = fma(val[e], x[col[e]], dot);
-      const double res = bvec[i] - dot;
+      for (int64_t e = e0; e < e1; ++e) dot = fma(ld_stream(val + e, pf), x[ld_stream(col + e, pf)], dot);
+      const double res = ld_stream(bvec + i, pf) - dot;
       for (int64_t e = e0; e < e1; ++e) {
         if (GSMEM) atomicAdd(&gs[col[e]], val[e] * res);
         else atomicAdd(&g[col[e]], val[e] * res);
@@ -42,8 +80,8 @@ __global__ void __launch_bounds__(256) csr_sketch_grad_kernel(int64_t n, int d, 
         const uint32_t b = hash_bucket(key, (uint64_t)(row_offset + i), (uint32_t)j, (uint32_t)s, M, neg);
         double *row = SA + (int64_t)b * d;
         for (int64_t e = e0; e < e1; ++e) {
-          const double v = val[e];
-          atomicAdd(row + col[e], neg ? -v : v);
+          const double v = GRAD ? val[e] : ld_stream(val + e, pf);
+          red_keep(row + (GRAD ? col[e] : ld_stream(col + e, pf)), neg ? -v : v, pl);
         }
       }
     }
