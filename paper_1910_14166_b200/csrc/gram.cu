@@ -135,6 +135,135 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double *__restri
   H[(int64_t)p * d + q] = s;
   H[(int64_t)q * d + p] = s;
 }
+// ---------------------------------------------------------------------------
+// Stream-K variant for many tiles (d >= 384; C3: 136 upper tiles, m = 8192):
+// the (tile, k-chunk) items, tile-major, are dealt out in equal contiguous
+// ranges to a persistent grid of 2 CTAs per SM, so every SM does the same
+// number of DMMAs (the split-K grid left ~8% of the SMs half idle).  A CTA
+// keeps its accumulators while consecutive items belong to the same tile and
+// flushes a partial tile (at most two per CTA: a range is shorter than a
+// tile's chunk count) with its tile id; the reduction sums, per tile, the
+// partials of the CTAs that covered it in CTA order (fixed, deterministic).
+// Stages are loaded with 16-byte cp.async (d even, 16-byte aligned SA).
+__device__ __forceinline__ void cp_async16(double *smem, const double *gmem, bool pred) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+
+__global__ void __launch_bounds__(128) gram_streamk_kernel(const double *__restrict__ SA, int64_t m, int d,
+                                                           int tiles, int ntri, int kch, int ipc,
+                                                           double *__restrict__ partials, int *__restrict__ slot_tile) {
+  extern __shared__ double sm[];
+  double *Xp = sm;                 // [2][KC][LDS]
+  double *Xq = sm + 2 * KC * LDS;  // [2][KC][LDS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int64_t total = (int64_t)ntri * kch;
+  const int64_t i0 = (int64_t)blockIdx.x * ipc, i1 = min(total, i0 + ipc);
+  if (tid == 0) slot_tile[2 * blockIdx.x] = slot_tile[2 * blockIdx.x + 1] = -1;
+  double acc[4][4][2];
+  int cur = -1, slot = 0;
+  auto flush = [&]() {
+    double *out = partials + ((int64_t)blockIdx.x * 2 + slot) * (GT * GT);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = 32 * wm + 8 * i + (lane >> 2);
+        const int c = 32 * wn + 8 * j + 2 * (lane & 3);
+        out[r * GT + c] = acc[i][j][0];
+        out[r * GT + c + 1] = acc[i][j][1];
+      }
+    if (tid == 0) slot_tile[2 * blockIdx.x + slot] = cur;
+    ++slot;
+  };
+  for (int64_t it = i0; it < i1; ++it) {
+    const int tile = (int)(it / kch), kc = (int)(it % kch);
+    if (tile != cur) {
+      if (cur >= 0) flush();
+      cur = tile;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    int P, Q;
+    tri_decode(tile, tiles, P, Q);
+    const bool diag = (P == Q);
+    const int64_t k0 = m * kc / kch, k1 = m * (kc + 1) / kch;
+    auto load_stage = [&](int buf, int64_t kb) {
+      // KC x 64 doubles per matrix in 16-byte pieces: 1024 / 128 threads = 8 each
+#pragma unroll
+      for (int t2 = 0; t2 < (KC * GT / 2) / 128; ++t2) {
+        const int e = t2 * 128 + tid;
+        const int r = e / (GT / 2), c = 2 * (e % (GT / 2));
+        const int64_t row = kb + r;
+        const bool rin = row < k1;
+        const int cp = P * GT + c, cq = Q * GT + c;
+        cp_async16(&Xp[(buf * KC + r) * LDS + c], SA + (rin ? row : 0) * d + (cp < d ? cp : 0), rin && cp < d);
+        if (!diag)
+          cp_async16(&Xq[(buf * KC + r) * LDS + c], SA + (rin ? row : 0) * d + (cq < d ? cq : 0), rin && cq < d);
+      }
+      cp_async_commit();
+    };
+    const int nstages = (int)((k1 - k0 + KC - 1) / KC);
+    if (nstages > 0) load_stage(0, k0);
+    for (int s2 = 0; s2 < nstages; ++s2) {
+      const int buf = s2 & 1;
+      if (s2 + 1 < nstages) {
+        load_stage(buf ^ 1, k0 + (int64_t)(s2 + 1) * KC);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncthreads();
+      const double *xp = Xp + buf * KC * LDS;
+      const double *xq = (diag ? Xp : Xq) + buf * KC * LDS;
+#pragma unroll
+      for (int kk = 0; kk < KC; kk += 4) {
+        const int kr = kk + (lane & 3);
+        double a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = xp[kr * LDS + 32 * wm + 8 * i + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = xq[kr * LDS + 32 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+      __syncthreads();
+    }
+  }
+  if (cur >= 0) flush();
+}
+
+// Per tile: sum the partials of the CTAs whose item range covered it (CTA
+// order), scale^2, mirror.  grid: tile x 16 chunks of 256 elements.
+__global__ void __launch_bounds__(256) gram_streamk_reduce_kernel(const double *__restrict__ partials,
+                                                                  const int *__restrict__ slot_tile, int d, int tiles,
+                                                                  int kch, int ipc, double scale2,
+                                                                  double *__restrict__ H) {
+  const int t = blockIdx.x;
+  int P, Q;
+  tri_decode(t, tiles, P, Q);
+  const int e = blockIdx.y * 256 + threadIdx.x;
+  const int r = e / GT, c = e % GT;
+  const int p = P * GT + r, q = Q * GT + c;
+  if (p >= d || q >= d) return;
+  if (P == Q && q < p) return;
+  const int64_t c0 = ((int64_t)t * kch) / ipc, c1 = ((int64_t)t * kch + kch - 1) / ipc;
+  double s = 0.0;
+  for (int64_t cta = c0; cta <= c1; ++cta) {
+    const int sl = slot_tile[2 * cta] == t ? 0 : 1;
+    s += partials[((int64_t)cta * 2 + sl) * (GT * GT) + e];
+  }
+  s *= scale2;
+  H[(int64_t)p * d + q] = s;
+  H[(int64_t)q * d + p] = s;
+}
+
 }  // namespace
 
 GramPlan gram_plan(int64_t m, int64_t d, int num_sms) {
@@ -151,12 +280,43 @@ GramPlan gram_plan(int64_t m, int64_t d, int num_sms) {
   kc = (kc + KC - 1) / KC * KC;
   p.kchunk = std::max<int64_t>(kc, KC);
   p.nsplit = (int)std::max<int64_t>(1, (m + p.kchunk - 1) / p.kchunk);
+  // stream-K for many tiles: 2 CTAs per SM, k-chunks per tile chosen so that
+  // the items divide as evenly as possible over the CTAs (>= 64 rows a chunk)
+  if (p.ntri >= 16 && d % 2 == 0 && m >= 256) {
+    const int64_t ncta = 2 * (int64_t)num_sms;
+    const int64_t kmin = std::max<int64_t>(1, (2 * ncta + p.ntri - 1) / p.ntri);
+    const int64_t kmax = std::max<int64_t>(kmin, m / 64);
+    int64_t best = kmin;
+    double best_waste = 1e30;
+    for (int64_t k = kmin; k <= kmax && k <= 8 * kmin; ++k) {
+      const int64_t tot = p.ntri * k, ipc = (tot + ncta - 1) / ncta;
+      const double waste = (double)(ipc * ncta - tot) / (double)tot;
+      if (waste < best_waste - 1e-9) {
+        best_waste = waste;
+        best = k;
+      }
+    }
+    p.kch = (int)best;
+    p.ipc = (int)((p.ntri * best + ncta - 1) / ncta);
+    p.ncta = (int)((p.ntri * best + p.ipc - 1) / p.ipc);
+    if (p.ipc > p.kch) p.ncta = 0;  // a CTA would span three tiles: keep split-K
+  }
   return p;
 }
 
 cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
                         cudaStream_t st, LaunchCounter lc) {
   const size_t smem = (size_t)4 * KC * LDS * 8;
+  if (p.ncta > 0 && (reinterpret_cast<uintptr_t>(SA) % 16) == 0) {
+    IHS_SMEM_ATTR(gram_streamk_kernel, smem);
+    int *slot_tile = reinterpret_cast<int *>(partials + (size_t)p.ncta * 2 * GT * GT);
+    gram_streamk_kernel<<<p.ncta, 128, smem, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kch, p.ipc, partials,
+                                                   slot_tile);
+    gram_streamk_reduce_kernel<<<dim3(p.ntri, (GT * GT) / 256), 256, 0, st>>>(partials, slot_tile, (int)p.d, p.tiles,
+                                                                               p.kch, p.ipc, scale * scale, H);
+    lc.add(2);
+    return cudaGetLastError();
+  }
   IHS_SMEM_ATTR(gram_kernel, smem);
   dim3 grid(p.ntri, p.nsplit);
   gram_kernel<<<grid, 128, smem, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kchunk, partials);

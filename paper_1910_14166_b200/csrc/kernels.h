@@ -1,5 +1,6 @@
 // Host-side launchers of the sm_100a kernels (internal to libihs.so).
 #pragma once
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -112,7 +113,11 @@ struct GramPlan {
   int ntri = 0;     // upper-triangular tiles
   int nsplit = 0;   // split-K
   int64_t kchunk = 0;
-  size_t partial_bytes() const { return (size_t)nsplit * ntri * 64 * 64 * 8; }
+  int ncta = 0, kch = 0, ipc = 0;  // stream-K (ncta > 0): CTAs, k-chunks per tile, items per CTA
+  size_t partial_bytes() const {
+    const size_t sk = (size_t)ncta * 2 * 64 * 64 * 8 + (size_t)ncta * 2 * 4 + 64;
+    return std::max((size_t)nsplit * ntri * 64 * 64 * 8, sk);
+  }
 };
 GramPlan gram_plan(int64_t m, int64_t d, int num_sms);
 cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,

@@ -161,7 +161,7 @@ def test_fused_sketch_grad(P, oracle_mod, n, d, m):
 
 # ---------------------------------------------------------------- a4 Gram
 @pytest.mark.parametrize("m,d", [(200, 10), (1024, 128), (2048, 256), (4096, 96), (777, 130), (64, 1), (3, 70),
-                                 (8192, 1024)])
+                                 (8192, 1024), (3000, 400), (2048, 1000), (513, 2000)])
 def test_gram(P, oracle_mod, m, d):
     rng = np.random.default_rng(m * d)
     SA = rng.standard_normal((m, d))
