@@ -143,6 +143,7 @@ def ncu_traffic(cfg_name: str, group: str):
 
 
 DMMA_TFLOPS = 36.8  # fp64 DMMA peak measured on this pool's B200 (tools/probe/probe.cu, profiles/r01/probe.txt)
+RED_GPS = 179.5  # fp64 RED.ADD throughput into an L2-resident 64 MB array, G/s (same probe)
 
 
 def algorithmic(cfg, group, n_loc, nnz_loc, steps_launches):
@@ -157,8 +158,8 @@ def algorithmic(cfg, group, n_loc, nnz_loc, steps_launches):
         return 8 * n_loc * d + 8 * m * d, "hbm", "sjlt_stream_kernel"
     if group == "grad":
         return 8 * n_loc * d + 8 * n_loc, "hbm", "grad_dense_kernel"
-    if group == "csr":
-        return 8 * (n_loc + 1) + 12 * nnz_loc + 8 * n_loc + 8 * m * d, "hbm", "csr_sketch_grad_kernel"
+    if group == "csr":  # bound by the s fp64 reductions per nonzero into the L2-resident SA
+        return float(s) * nnz_loc, "l2_red", "csr_sketch_grad_kernel (REDG.ADD.F64 into L2-resident SA)"
     if group == "gram":
         return float(m) * d * d, "tensor", "gram_kernel (DMMA m8n8k4 f64, symmetric half)"
     return None, "latency", group
@@ -188,6 +189,12 @@ def roofline(prof, cfg, n_loc, nnz_loc, steps):
         out.update({"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": ach / peaks["hbm_gbs"], "algorithmic_bytes_per_launch": per_launch,
                     "peak_source": f"{peak_src} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"})
+    elif kind == "l2_red":
+        per_launch = alg / launches_per_step
+        ach = per_launch / (avg / 1e3) / 1e9
+        out.update({"bound": "l2_red", "achieved": ach, "peak": RED_GPS, "unit": "G red/s",
+                    "frac": ach / RED_GPS, "algorithmic_reds_per_launch": per_launch,
+                    "peak_source": "measured fp64 RED.ADD throughput, random addresses in 64 MB (tools/probe/probe.cu)"})
     else:
         per_launch = alg / launches_per_step
         ach = per_launch / (avg / 1e3) / 1e12

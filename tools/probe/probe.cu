@@ -70,6 +70,17 @@ __global__ void smem_rmw(int iters, int random, double* out) {
   if (tile[threadIdx.x] == 12345.0) out[0] = 1;
 }
 
+// fp64 RED.ADD throughput into a large array (random 8-byte addresses), the
+// CSR sketch's bound
+__global__ void red_random(double* buf, size_t n, int iters) {
+  unsigned x = (blockIdx.x * blockDim.x + threadIdx.x) * 2654435761u + 12345u;
+  for (int i = 0; i < iters; ++i) {
+    x = x * 1664525u + 1013904223u;
+    size_t idx = ((size_t)x * 2654435761ull) % n;
+    atomicAdd(buf + idx, 1.0);
+  }
+}
+
 __global__ void dmma_loop(double* out, int iters) {
   double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
   double c0[4]={0,0,0,0}, c1[4]={0,0,0,0};
@@ -122,6 +133,13 @@ int main(){
     for (int r=0;r<2;r++){ cudaEventRecord(e0); smem_rmw<<<148,512,131072>>>(it, rnd, out); cudaEventRecord(e1); cudaEventSynchronize(e1);} cudaEventElapsedTime(&ms,e0,e1);
     double upd = 148.0*512*it;
     printf("smem fp64 RMW %s: %.3f ms  %.2f G upd/s  (%.2f upd/clk/SM at 1.965 GHz)\n", rnd ? "random 32B rows" : "contiguous", ms, upd/ms/1e6, upd/ms/1e-3/148/1.965e9);
+  }
+  for (size_t mb : {64, 512}) {
+    size_t nel = (mb << 20) / 8;
+    int it = 256;
+    for (int r=0;r<2;r++){ cudaEventRecord(e0); red_random<<<148*8,256>>>(A, nel, it); cudaEventRecord(e1); cudaEventSynchronize(e1);} cudaEventElapsedTime(&ms,e0,e1);
+    double ops = 148.0*8*256*it;
+    printf("RED.ADD.F64 random over %zu MB: %.3f ms  %.1f G red/s\n", mb, ms, ops/ms/1e6);
   }
   CK(cudaGetLastError());
   // dmma
