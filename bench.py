@@ -312,8 +312,6 @@ def main():
         xa, xb = xb, xa
         t += 1
     barrier()
-    ctx.set_profiling(True)
-    ctx.profile_reset()
     l0 = ctx.kernel_launches
     clocks = ClockSampler(local)
     clocks.start()
@@ -338,6 +336,16 @@ def main():
     ms = float(mt.item())
     ms_step = ms / args.steps
     value = cfg.n * args.steps / (ms / 1e3)
+    # ---- per-kernel-group breakdown: the same K steps again with the library's
+    # CUDA events around every group (kept out of the timed loop above)
+    ctx.set_profiling(True)
+    ctx.profile_reset()
+    barrier()
+    for _ in range(args.steps):
+        S.step(t, xa, xb)
+        xa, xb = xb, xa
+        t += 1
+    barrier()
     prof = {name: ctx.profile(k) for k, name in enumerate(P.KERNEL_GROUPS)}
     ctx.set_profiling(False)
     # ---- roofline of the dominant kernel group (C2: the fused sketch+gradient gather)
