@@ -312,6 +312,7 @@ def main():
         xa, xb = xb, xa
         t += 1
     barrier()
+    x_start, t_start = xa.clone(), t  # the profiled pass below replays these steps
     l0 = ctx.kernel_launches
     clocks = ClockSampler(local)
     clocks.start()
@@ -336,10 +337,13 @@ def main():
     ms = float(mt.item())
     ms_step = ms / args.steps
     value = cfg.n * args.steps / (ms / 1e3)
-    # ---- per-kernel-group breakdown: the same K steps again with the library's
-    # CUDA events around every group (kept out of the timed loop above)
+    # ---- per-kernel-group breakdown: the same K steps (same iterations, same
+    # starting x) replayed with the library's CUDA events around every group,
+    # kept out of the timed loop above
     ctx.set_profiling(True)
     ctx.profile_reset()
+    xa.copy_(x_start)
+    t = t_start
     barrier()
     for _ in range(args.steps):
         S.step(t, xa, xb)
