@@ -146,9 +146,20 @@ __global__ void __launch_bounds__(1024) reduce_rows_kernel(const double *__restr
   __shared__ double sm[32][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int c = blockIdx.x * 32 + lane;
-  double s = 0.0;
-  if (c < d)
-    for (int64_t r = warp; r < rows; r += 32) s += part[r * d + c];
+  // 4 interleaved partial sums per thread (independent L2 loads in flight),
+  // combined in a fixed order: deterministic
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if (c < d) {
+    int64_t r = warp;
+    for (; r + 96 < rows; r += 128) {
+      s0 += part[r * d + c];
+      s1 += part[(r + 32) * d + c];
+      s2 += part[(r + 64) * d + c];
+      s3 += part[(r + 96) * d + c];
+    }
+    for (; r < rows; r += 32) s0 += part[r * d + c];
+  }
+  const double s = (s0 + s1) + (s2 + s3);
   sm[warp][lane] = s;
   __syncthreads();
   if (warp == 0 && c < d) {
