@@ -5,7 +5,7 @@
 # usage: gpurun -- 'bash tools/gpu_round.sh TAG [parts...]'   parts: probe tests smoke bench dist ncu
 TAG=${1:-r01}
 shift
-PARTS=${*:-"tests smoke bench ncu"}
+PARTS=${*:-"tests smoke bench dist ncu"}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
@@ -24,7 +24,7 @@ if has smoke; then
 fi
 if has bench; then
   timeout 900 python bench.py > $OUT/bench_default.json 2> $OUT/bench_default.err
-  for C in C1 C3 C4 C5; do
+  for C in C1 C3 C4 C4P C5; do
     timeout 600 python bench.py --config $C --steps 10 --warmup 3 --no-cpu > $OUT/bench_$C.json 2> $OUT/bench_$C.err
   done
   timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_reference.json 2> $OUT/bench_reference.err
@@ -46,7 +46,7 @@ if has ncu; then
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cs_gather_tma -s 3 -c 1 \
     -o $OUT/full_C2 -f $B --config C2 > $OUT/ncu_full_C2.log 2>&1
   $B --config C3 > $OUT/plain1_C3.log 2>&1 &&
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"gram_kernel|csr_sketch|ols_cg" -s 9 -c 3 \
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"gram_streamk|csr_sketch|ols_cg" -s 9 -c 3 \
     -o $OUT/full_C3 -f $B --config C3 > $OUT/ncu_full_C3.log 2>&1
   $B --config C4 > $OUT/plain1_C4.log 2>&1 &&
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"pg_warp|cs_gather_tma" -s 6 -c 2 \
