@@ -151,9 +151,17 @@ def algorithmic(cfg, group, n_loc, nnz_loc, steps_launches):
     SURVEY.md 8(d)'s per-unit figures."""
     d, m, s = cfg.d, cfg.m, cfg.s
     M = m // s
-    if group == "sketch":  # s bucket-ordered gathers over A; gradient fused into block 0
-        b = s * (8 * n_loc * d + 4 * n_loc) + 8 * n_loc + 8 * M * d + 8 * m * d
-        return b, "hbm", "cs_gather_tma_kernel (bucket-ordered sketch, gradient fused into block 0)"
+    if group == "sketch":
+        # SURVEY 8(d): A read ONCE per iteration (8d B per row) + b and the
+        # perm entry per row + the SA / gradient-partial writes.  For an SJLT
+        # (s > 1) the design reads A s times (one bucket-ordered pass per
+        # block; DESIGN.md section 9), which shows up as DRAM traffic ~s x
+        # the algorithmic bytes, not as algorithmic work.
+        b = 8 * n_loc * d + 12 * n_loc + 8 * M * d + 8 * m * d
+        label = "cs_gather_tma_kernel (bucket-ordered sketch, gradient fused)"
+        if s > 1:
+            label += f"; SJLT: {s} bucket-ordered passes over A (A read {s}x)"
+        return b, "hbm", label
     if group == "sjlt":
         return 8 * n_loc * d + 8 * m * d, "hbm", "sjlt_stream_kernel"
     if group == "grad":
