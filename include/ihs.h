@@ -166,6 +166,14 @@ ihs_status ihs_sketch_grad(ihs_ctx ctx, const ihs_matrix *A, const ihs_sketch_sp
 ihs_status ihs_gram(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, double scale,
                     double *H);
 
+/* a4 + a6 for OLS in one call: H = scale^2 SA^T SA (written to H, d x d) and
+ * x_next = x + H^{-1} g.  d <= 64 (IHS_FUSE=1: d <= 128): one thread-block-
+ * cluster launch (Gram partials on DMMA, reduced through distributed shared
+ * memory straight into the Cholesky CTA); otherwise ihs_gram followed by
+ * ihs_ols_update.  Statuses as for ihs_ols_update. */
+ihs_status ihs_gram_ols_update(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, double scale,
+                               const double *g, const double *x, double *x_next, double *H);
+
 /* a6, OLS: x_next = x + H^{-1} g (Eq. (2) with C = R^d).
  * d <= 160: blocked Cholesky in one CTA; d > 160: Jacobi-preconditioned
  * conjugate gradients to a relative residual of 1e-15 in one cooperative

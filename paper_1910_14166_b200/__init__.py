@@ -82,6 +82,8 @@ _EXPORTS = {
                                   C.c_void_p, C.c_void_p, C.c_void_p]),
     "ihs_gram": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p]),
     "ihs_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "ihs_gram_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]),
     "ihs_l1ball_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_double,
                                     C.POINTER(InnerCfg), C.c_void_p, C.c_void_p]),
     "ihs_lasso_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_double,
@@ -323,6 +325,17 @@ def ihs_gram(SA: torch.Tensor, scale: float = 1.0, out=None, ctx: Context | None
 
 
 # ------------------------------------------------------------------ a6
+def ihs_gram_ols_update(SA: torch.Tensor, g, x, scale: float = 1.0, out=None, H=None, ctx: Context | None = None):
+    """a4 + a6 for OLS: H = scale^2 SA^T SA, x_next = x + H^{-1} g; returns (x_next, H)."""
+    ctx = ctx or default_context(SA.device)
+    m, d = SA.shape
+    xn = out if out is not None else torch.empty_like(x)
+    H = H if H is not None else _f64((d, d), SA.device)
+    _check(lib().ihs_gram_ols_update(ctx._bind(), _p(SA), m, d, float(scale), _p(g), _p(x), _p(xn), _p(H)),
+           "ihs_gram_ols_update")
+    return xn, H
+
+
 def ihs_ols_update(H, g, x, out=None, ctx: Context | None = None):
     ctx = ctx or default_context(H.device)
     xn = out if out is not None else torch.empty_like(x)

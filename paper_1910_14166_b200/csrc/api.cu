@@ -411,6 +411,24 @@ ihs_status ols_impl(ihs_ctx c, const double *H, const double *g, int64_t d, cons
   return IHS_OK;
 }
 
+// a4 + a6 (OLS) in one cluster launch.  Measured on B200: a win while launch
+// latency dominates (C1, d = 10: 31 -> 21 us) but not at d = 96..128 (C2: 69 ->
+// 73 us, C5: 67 -> 97 us: the DSMEM reduction runs at 14-30 GB/s per SM), so
+// the default fuses only d <= 64; IHS_FUSE=1 forces it for d <= 128, 0 never.
+ihs_status gram_ols_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, const double *g,
+                         const double *x, double *xn, double *H) {
+  static const char *fe = getenv("IHS_FUSE");
+  static const int64_t fuse_max = !fe ? 64 : (!std::strcmp(fe, "0") ? 0 : 128);
+  if (d <= fuse_max && gram_ols_supported(d) && m >= 1) {
+    Prof pr(c, IHS_K_CHOL);
+    const cudaError_t e = launch_gram_ols(SA, m, d, scale, g, x, xn, H, c->d_status, c->stream, lc_of(c));
+    if (e == cudaSuccess) return IHS_OK;
+    cudaGetLastError();  // cluster launch refused: the two-call path below
+  }
+  IHS_TRY(gram_impl(c, SA, m, d, scale, H));
+  return ols_impl(c, H, g, d, x, xn);
+}
+
 ihs_inner_cfg default_inner() {
   ihs_inner_cfg k;
   k.max_inner = 20000;
@@ -546,10 +564,14 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
         return IHS_ERR_COMM;
     }
     if (trace) cudaEventRecord(ev[2], st);
-    IHS_TRY(gram_impl(c, SA, m, d, scale, H));
-    if (trace) cudaEventRecord(ev[3], st);
-    if (constraint == 0) IHS_TRY(ols_impl(c, H, g, d, x, xn));
-    else IHS_TRY(l1_impl(c, H, g, d, x, radius, cfg, xn, inner_dev + t, constraint == 2 ? 1 : 0));
+    if (constraint == 0) {
+      if (trace) cudaEventRecord(ev[3], st);  // a4 + a6 are one fused launch for d <= 128
+      IHS_TRY(gram_ols_impl(c, SA, m, d, scale, g, x, xn, H));
+    } else {
+      IHS_TRY(gram_impl(c, SA, m, d, scale, H));
+      if (trace) cudaEventRecord(ev[3], st);
+      IHS_TRY(l1_impl(c, H, g, d, x, radius, cfg, xn, inner_dev + t, constraint == 2 ? 1 : 0));
+    }
     if (trace) {
       cudaEventRecord(ev[4], st);
       IHS_CUDA(cudaEventSynchronize(ev[4]));
@@ -774,6 +796,13 @@ ihs_status ihs_gram(ihs_ctx c, const double *SA, int64_t m, int64_t d, double sc
   if (!c || !SA || !H || m < 1 || d < 1 || !std::isfinite(scale)) return IHS_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
   return gram_impl(c, SA, m, d, scale, H);
+}
+
+ihs_status ihs_gram_ols_update(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, const double *gv,
+                               const double *x, double *xn, double *H) {
+  if (!c || !SA || !gv || !x || !xn || !H || d < 1 || m < 0) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return gram_ols_impl(c, SA, m, d, scale, gv, x, xn, H);
 }
 
 ihs_status ihs_ols_update(ihs_ctx c, const double *H, const double *gv, int64_t d, const double *x, double *xn) {

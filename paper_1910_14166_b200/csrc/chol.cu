@@ -7,6 +7,8 @@
 #include "kernels.h"
 #include "chol_blocks.cuh"
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -40,28 +42,15 @@ constexpr int kBThreads = 256;
 // (rows D+1..D+7 are zero so the DMMA trailing update keeps whole 8-row tiles):
 // the panel TRSM and the trailing updates turn row D into y = L^{-1} g, so only
 // the backward solve L^T u = y runs after the factorisation.
+// The factorisation and solves on the loaded augmented Ls (shared memory), by
+// the whole CTA of kBThreads threads: shared by chol_blocked_kernel (H from
+// global) and gram_ols_kernel (H reduced from a cluster's Gram partials).
 template <int NBLK>
-__global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *__restrict__ H,
-                                                                const double *__restrict__ g, int d,
-                                                                const double *__restrict__ x, double *x_next,
-                                                                int *status, const int *run) {
-  if (run && *run == 0) return;  // the CG solve before it finished
+__device__ __forceinline__ void chol_blocked_body(double *Ls, double *rdiag, double *colbuf, int &s_bad, int d,
+                                                  const double *__restrict__ x, double *x_next, int *status) {
   constexpr int D = 32 * NBLK;
-  constexpr int DA = D + 8;  // rows incl. the augmented g row and its zero tile padding
   constexpr int lda = D + 4;
-  extern __shared__ double sm[];
-  double *Ls = sm;                // DA x lda
-  double *rdiag = sm + DA * lda;  // D
-  __shared__ int s_bad;
-  __shared__ double colbuf[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = warp; i < DA; i += kBThreads / 32) {
-    if (i < D) {
-      for (int c = lane; c <= i; c += 32) Ls[i * lda + c] = (i < d) ? H[(int64_t)i * d + c] : (c == i ? 1.0 : 0.0);
-    } else {
-      for (int c = lane; c < D; c += 32) Ls[i * lda + c] = (i == D && c < d) ? g[c] : 0.0;
-    }
-  }
   if (tid == 0) s_bad = 0;
   __syncthreads();
 #pragma unroll 1
@@ -142,6 +131,179 @@ __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *_
 }
 
 template <int NBLK>
+__global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *__restrict__ H,
+                                                                const double *__restrict__ g, int d,
+                                                                const double *__restrict__ x, double *x_next,
+                                                                int *status, const int *run) {
+  if (run && *run == 0) return;  // the CG solve before it finished
+  constexpr int D = 32 * NBLK;
+  constexpr int DA = D + 8;  // rows incl. the augmented g row and its zero tile padding
+  constexpr int lda = D + 4;
+  extern __shared__ double sm[];
+  double *Ls = sm;                // DA x lda
+  double *rdiag = sm + DA * lda;  // D
+  __shared__ int s_bad;
+  __shared__ double colbuf[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = warp; i < DA; i += kBThreads / 32) {
+    if (i < D) {
+      for (int c = lane; c <= i; c += 32) Ls[i * lda + c] = (i < d) ? H[(int64_t)i * d + c] : (c == i ? 1.0 : 0.0);
+    } else {
+      for (int c = lane; c < D; c += 32) Ls[i * lda + c] = (i == D && c < d) ? g[c] : 0.0;
+    }
+  }
+  chol_blocked_body<NBLK>(Ls, rdiag, colbuf, s_bad, d, x, x_next, status);
+}
+
+// ---------------------------------------------------------------------------
+// a4 + a6 fused for d <= 128 (OLS): one thread-block cluster.  CTAs 1..CL-1
+// form Gram partials of row ranges of SA on DMMA (mma.sync m8n8k4 f64, 32x32
+// warp tiles over the full D x D); after a cluster barrier each of them sums a
+// slice of the lower triangle over all partials in CTA order (DSMEM reads) and
+// stores it straight into CTA 0's augmented Cholesky matrix (DSMEM writes);
+// after a second barrier CTA 0 factorises and solves (chol_blocked_body).
+// Replaces the Gram launch pair + the Cholesky launch (one launch, H never
+// round-trips through L2 on the critical path; H_out, if given, gets a copy).
+constexpr int kGoRows = 64;  // SA rows per staging chunk
+template <int NBLK>
+__global__ void __launch_bounds__(kBThreads, 1) gram_ols_kernel(const double *__restrict__ SA, int64_t m, int d,
+                                                               double scale2, const double *__restrict__ g,
+                                                               const double *__restrict__ x, double *x_next,
+                                                               double *H_out, int *status) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  constexpr int D = 32 * NBLK;
+  constexpr int DA = D + 8;
+  constexpr int lda = D + 4;      // Cholesky layout (CTA 0)
+  constexpr int lds = D + 4;      // staging stride (== 4 mod 16: conflict-free fragments)
+  constexpr int NT = NBLK * NBLK;  // 32x32 warp tiles of the full D x D
+  extern __shared__ double sm[];
+  __shared__ int s_bad;
+  __shared__ double colbuf[64];
+  const int rank = (int)cluster.block_rank(), cs = (int)cluster.num_blocks();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (rank == 0) {
+    double *Ls = sm;
+    for (int i = warp; i < DA; i += kBThreads / 32) {
+      if (i < D) {
+        if (i >= d)  // identity padding; the lower triangle of H arrives from the reducers
+          for (int c = lane; c <= i; c += 32) Ls[i * lda + c] = (c == i ? 1.0 : 0.0);
+      } else {
+        for (int c = lane; c < D; c += 32) Ls[i * lda + c] = (i == D && c < d) ? g[c] : 0.0;
+      }
+    }
+  } else {
+    double *S = sm;                          // kGoRows x lds
+    double *Hp = sm + kGoRows * lds;         // D x D partial
+    const int64_t nw = cs - 1, w0 = rank - 1;
+    const int64_t r0 = m * w0 / nw, r1 = m * (w0 + 1) / nw;
+    double acc[2][4][4][2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[t][i][j][0] = acc[t][i][j][1] = 0.0;
+    for (int64_t rb = r0; rb < r1; rb += kGoRows) {
+      const int rows = (int)min((int64_t)kGoRows, r1 - rb);
+      __syncthreads();  // the previous chunk's fragments are consumed
+      for (int e = tid; e < kGoRows * D; e += kBThreads) {
+        const int r = e / D, c = e % D;
+        S[r * lds + c] = (r < rows && c < d) ? SA[(rb + r) * d + c] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int tile = warp + 8 * t;
+        if (tile < NT) {
+          const int I = 32 * (tile / NBLK), J = 32 * (tile % NBLK);
+#pragma unroll 4
+          for (int kk = 0; kk < kGoRows; kk += 4) {
+            const int kr = kk + (lane & 3);
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = S[kr * lds + I + 8 * i + (lane >> 2)];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = S[kr * lds + J + 8 * j + (lane >> 2)];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) dmma884(acc[t][i][j][0], acc[t][i][j][1], a[i], b[j]);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int tile = warp + 8 * t;
+      if (tile < NT) {
+        const int I = 32 * (tile / NBLK), J = 32 * (tile % NBLK);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = I + 8 * i + (lane >> 2), c = J + 8 * j + 2 * (lane & 3);
+            Hp[r * D + c] = acc[t][i][j][0];
+            Hp[r * D + c + 1] = acc[t][i][j][1];
+          }
+      }
+    }
+  }
+  cluster.sync();
+  if (rank > 0) {
+    // reduce a slice of the lower triangle over the partials (CTA order) into CTA 0
+    double *Ls0 = cluster.map_shared_rank(sm, 0);
+    const int nw = cs - 1;
+    for (int e = (rank - 1) * kBThreads + tid; e < D * D; e += nw * kBThreads) {
+      const int i = e / D, j = e % D;
+      if (j > i || i >= d) continue;
+      double v = 0.0;
+      for (int r = 1; r < cs; ++r) v += cluster.map_shared_rank(sm + kGoRows * lds, r)[e];
+      v *= scale2;
+      Ls0[i * lda + j] = v;
+      if (H_out) {
+        H_out[(int64_t)i * d + j] = v;
+        H_out[(int64_t)j * d + i] = v;
+      }
+    }
+  }
+  cluster.sync();
+  if (rank != 0) return;
+  chol_blocked_body<NBLK>(sm, sm + DA * lda, colbuf, s_bad, d, x, x_next, status);
+}
+
+template <int NBLK>
+cudaError_t launch_gram_ols_t(const double *SA, int64_t m, int d, double scale, const double *g, const double *x,
+                              double *x_next, double *H_out, int *status, cudaStream_t st) {
+  constexpr int D = 32 * NBLK;
+  const size_t smem_chol = ((size_t)(D + 8) * (D + 4) + D) * 8;
+  const size_t smem_gram = ((size_t)kGoRows * (D + 4) + (size_t)D * D) * 8;
+  const size_t smem = std::max(smem_chol, smem_gram);
+  auto kern = gram_ols_kernel<NBLK>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaError_t e = cudaErrorUnknown;
+  for (int cs : {16, 8}) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kBThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, SA, m, d, scale * scale, g, x, x_next, H_out, status);
+    if (e == cudaSuccess) return e;
+    cudaGetLastError();
+  }
+  return e;
+}
+
+template <int NBLK>
 void launch_blocked(const double *H, const double *g, int d, const double *x, double *x_next, int *status,
                     const int *run, cudaStream_t st) {
   constexpr int D = 32 * NBLK;
@@ -157,6 +319,21 @@ cudaError_t launch_chol_large(const double *H, const double *g, int64_t d, const
 
 size_t chol_scratch_bytes(int64_t d) {
   return d > 160 ? std::max(chol_large_scratch_bytes(d), ols_cg_scratch_bytes(d)) : 256;
+}
+
+bool gram_ols_supported(int64_t d) { return d >= 1 && d <= 128; }
+
+cudaError_t launch_gram_ols(const double *SA, int64_t m, int64_t d, double scale, const double *g, const double *x,
+                            double *x_next, double *H_out, int *status, cudaStream_t st, LaunchCounter lc) {
+  cudaError_t e;
+  switch ((d + 31) / 32) {
+    case 1: e = launch_gram_ols_t<1>(SA, m, (int)d, scale, g, x, x_next, H_out, status, st); break;
+    case 2: e = launch_gram_ols_t<2>(SA, m, (int)d, scale, g, x, x_next, H_out, status, st); break;
+    case 3: e = launch_gram_ols_t<3>(SA, m, (int)d, scale, g, x, x_next, H_out, status, st); break;
+    default: e = launch_gram_ols_t<4>(SA, m, (int)d, scale, g, x, x_next, H_out, status, st); break;
+  }
+  lc.add();
+  return e;
 }
 
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,

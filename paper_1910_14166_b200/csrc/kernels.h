@@ -128,6 +128,11 @@ size_t chol_scratch_bytes(int64_t d);
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,
                               double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc);
 
+// a4 + a6 fused (d <= 128): H = scale^2 SA^T SA and x_next = x + H^{-1} g in one
+// cluster launch; H_out (optional) receives H.
+bool gram_ols_supported(int64_t d);
+cudaError_t launch_gram_ols(const double *SA, int64_t m, int64_t d, double scale, const double *g, const double *x,
+                            double *x_next, double *H_out, int *status, cudaStream_t st, LaunchCounter lc);
 // d > 160 default: Jacobi-preconditioned CG in one cooperative launch (ols_cg.cu).
 bool ols_cg_supported(int64_t d);
 size_t ols_cg_scratch_bytes(int64_t d);

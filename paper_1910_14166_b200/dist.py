@@ -48,6 +48,9 @@ class CudaOps:
     def ols(self, H, g, x, xn):
         P.ihs_ols_update(H, g, x, out=xn, ctx=self.ctx)
 
+    def gram_ols(self, SA, g, x, xn, H):
+        P.ihs_gram_ols_update(SA, g, x, out=xn, H=H, ctx=self.ctx)
+
     def l1(self, H, g, x, tau, cfg, xn, inner):
         P.ihs_l1ball_update(H, g, x, tau, cfg=cfg, out=xn, inner=inner, ctx=self.ctx)
 
@@ -85,6 +88,9 @@ class ShardedIHS:
         """x^{t+1} from x^t: a1-a2+a5 (local), a3 (all-reduce), a4, a6 (replicated)."""
         self.ops.sketch_grad(self.A, self.spec, t, self.b, x, self.SA, self.g)
         self.allreduce(self.pack)
+        if self.constraint == "ols" and hasattr(self.ops, "gram_ols"):  # a4 + a6 fused (one launch)
+            self.ops.gram_ols(self.SA, self.g, x, xn, self.H)
+            return xn
         self.ops.gram(self.SA, self.H)
         if self.constraint == "ols":
             self.ops.ols(self.H, self.g, x, xn)

@@ -60,6 +60,16 @@ def main():
         xo = oracle.ols_step(H, gv, xv)
         err = np.linalg.norm((xn.cpu().numpy() - xv) - (xo - xv)) / np.linalg.norm(xo - xv)
         check(f"ols update d={d}", err <= 1e-12, f"{err:.2e}")
+    # a4 + a6 fused (IHS_FUSE=1 forces the cluster kernel up to d = 128)
+    for m, d in ((1024, 128), (4096, 96)):
+        SAm = rng.standard_normal((m, d))
+        gv, xv = rng.standard_normal(d), rng.standard_normal(d)
+        xn, Hg = P.ihs_gram_ols_update(torch.from_numpy(SAm).to(DEV), torch.from_numpy(gv).to(DEV),
+                                       torch.from_numpy(xv).to(DEV))
+        Ho = oracle.gram(SAm)
+        xo = oracle.ols_step(Ho, gv, xv)
+        err = np.linalg.norm((xn.cpu().numpy() - xv) - (xo - xv)) / np.linalg.norm(xo - xv)
+        check(f"gram+ols d={d}", rel_fro(Hg.cpu().numpy(), Ho) <= 1e-12 and err <= 1e-11, f"{err:.2e}")
     # a6 l1 ball
     for d, tau in [(256, 10.0), (64, 2.0)]:
         H = spd(rng, d)

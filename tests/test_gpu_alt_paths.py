@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SETS = {
     "stream_ldg_chol_plain": {"IHS_SJLT": "stream", "IHS_GATHER": "ldg", "IHS_OLS": "chol", "IHS_PG_PLAIN": "1",
                               "IHS_PG_WARM": "0", "IHS_PREFETCH": "0"},
-    "tile_async_pgcta": {"IHS_SJLT": "tile", "IHS_GATHER": "async", "IHS_PG_CTA": "1"},
+    "tile_async_pgcta": {"IHS_SJLT": "tile", "IHS_GATHER": "async", "IHS_PG_CTA": "1", "IHS_FUSE": "1"},
     "pg_single": {"IHS_PG_SINGLE": "1"},
 }
 

@@ -191,6 +191,23 @@ def test_ols_update(P, oracle_mod, d):
     assert np.linalg.norm(u - uo) <= 1e-12 * np.linalg.norm(uo)
 
 
+@pytest.mark.parametrize("m,d", [(200, 10), (1024, 128), (4096, 96), (40, 5), (777, 100), (64, 1), (2048, 33),
+                                 (1000, 200)])
+def test_gram_ols_fused(P, oracle_mod, m, d):
+    """a4 + a6 in one cluster launch (d <= 128; d = 200 takes the two-call path)."""
+    rng = np.random.default_rng(m + d)
+    SA = rng.standard_normal((m, d))
+    g = rng.standard_normal(d)
+    x = rng.standard_normal(d)
+    xn, H = P.ihs_gram_ols_update(torch.from_numpy(SA).to(DEV), torch.from_numpy(g).to(DEV),
+                                  torch.from_numpy(x).to(DEV), scale=0.5)
+    Ho = 0.25 * oracle_mod.gram(SA)
+    assert rel_fro(H.cpu().numpy(), Ho) <= 1e-12
+    xo = oracle_mod.ols_step(Ho, g, x)
+    u, uo = xn.cpu().numpy() - x, xo - x
+    assert np.linalg.norm(u - uo) <= 1e-11 * np.linalg.norm(uo)
+
+
 def test_ols_update_not_spd(P):
     ctx = P.Context(0)
     H = torch.diag(torch.tensor([1.0, -1.0, 2.0], dtype=torch.float64, device=DEV))
