@@ -348,10 +348,11 @@ def main():
     # ---- per-kernel-group breakdown: the same K steps (same iterations, same
     # starting x) replayed with the library's CUDA events around every group,
     # kept out of the timed loop above
-    ctx.set_profiling(True)
-    ctx.profile_reset()
     xa.copy_(x_start)
     t = t_start
+    S.prime(t)  # the look-ahead prologue (a no-op otherwise), outside the profiled steps
+    ctx.set_profiling(True)
+    ctx.profile_reset()
     barrier()
     for _ in range(args.steps):
         S.step(t, xa, xb)
@@ -457,7 +458,9 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
-               "config": config_obj(cfg, world, {"per_gpu_rows": n_loc}),
+               "config": config_obj(cfg, world, {"per_gpu_rows": n_loc, "ols_schedule": (
+                   "look-ahead (H^-1 of the next sketch beside the pass; DESIGN.md section 9)" if S.lookahead
+                   else "plain") if cfg.constraint == "ols" else None}),
                "hbm_GBps_step": (cfg.a_bytes / world) / (ms_step / 1e3) / 1e9,
                "roofline": roof, "breakdown_ms": breakdown, "time_to_1e-10": ttt, "e2e": e2e,
                "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,

@@ -123,7 +123,9 @@ typedef enum {
     IHS_K_GRAM = 6,        /* a4 DMMA Gram + reduction */
     IHS_K_CHOL = 7,        /* a6 Cholesky update */
     IHS_K_PG = 8,          /* a6 projected gradient */
-    IHS_K_COUNT = 9
+    IHS_K_FACTOR = 9,      /* look-ahead a4 + a6: Gram + Cholesky + inverse (factor stream) */
+    IHS_K_APPLY = 10,      /* look-ahead a6: x + H^{-1} g */
+    IHS_K_COUNT = 11
 } ihs_kernel_group;
 ihs_status ihs_ctx_set_profiling(ihs_ctx ctx, int enable);
 ihs_status ihs_ctx_profile(ihs_ctx ctx, int group, double *total_ms, int64_t *launches);
@@ -173,6 +175,41 @@ ihs_status ihs_gram(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, double 
  * ihs_ols_update.  Statuses as for ihs_ols_update. */
 ihs_status ihs_gram_ols_update(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, double scale,
                                const double *g, const double *x, double *x_next, double *H);
+
+/* Look-ahead OLS.  S^{t+1} does not depend on x
+ * (Eq. (2): a fresh sketch per iteration, hashed from
+ * (seed, iteration, row) -- reading R1), so H_{t+1} = (S^{t+1}A)^T S^{t+1}A can
+ * be formed and factorised while the pass over A for g^{t+1} runs.
+ * ihs_ols_factor: Hinv = (scale^2 SA^T SA)^{-1}, d x d row-major (full,
+ * symmetric), through the Cholesky factor (Hinv = L^{-T} L^{-1}), in one
+ * thread-block-cluster launch on the ctx's high-priority factor stream,
+ * ordered after all work already enqueued on the ctx stream.  d <= 128 (else
+ * IHS_ERR_UNSUPPORTED), m >= 1.  Not positive definite: IHS_ERR_NOT_SPD
+ * (device status) and Hinv = 0.  SA must stay unmodified, and Hinv unread,
+ * until the factor is joined into the ctx stream: by an ihs_ols_apply on the
+ * same Hinv, or ihs_ctx_synchronize / ihs_ctx_destroy on this ctx.  Several
+ * factors (distinct Hinv) may be in flight.
+ * ihs_ols_apply: x_next = x + Hinv g (one CTA; d <= 1024), after the pending
+ * factor that writes this Hinv, if any.  x_next may alias x. */
+ihs_status ihs_ols_factor(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, double scale,
+                          double *Hinv);
+ihs_status ihs_ols_apply(ihs_ctx ctx, const double *Hinv, const double *g, int64_t d,
+                         const double *x, double *x_next);
+
+/* One look-ahead OLS step on one rank (nothing to all-reduce): the pass over A
+ * (dense) at x forms g = A^T (b - A x) (written to g, d) and, if SA_next is
+ * not NULL, S^{iter_next} A into SA_next (m x d, as ihs_sketch); if Hinv_next
+ * is also not NULL, ihs_ols_factor(SA_next -> Hinv_next) is enqueued as soon
+ * as SA_next is complete; then x_next = x + Hinv g, where Hinv is the factor
+ * of the current iteration's sketch (its pending factor is joined first).  The
+ * gradient reduction and the update are one launch.  Iterating
+ *   x^{t+1} = step(iter_next = t + 1, x^t, Hinv = H_t^{-1}, -> H_{t+1}^{-1})
+ * after a prologue ihs_sketch(t0) + ihs_ols_factor gives the IHS iterates of
+ * ihs_solve_ols.  Statuses as for ihs_ols_factor / ihs_sketch_grad. */
+ihs_status ihs_ols_lookahead_step(ihs_ctx ctx, const ihs_matrix *A, const ihs_sketch_spec *spec,
+                                  uint64_t iter_next, const double *b, const double *x,
+                                  const double *Hinv, double *SA_next, double *Hinv_next,
+                                  double *g, double *x_next);
 
 /* a6, OLS: x_next = x + H^{-1} g (Eq. (2) with C = R^d).
  * d <= 160: blocked Cholesky in one CTA; d > 160: Jacobi-preconditioned

@@ -29,7 +29,7 @@ OK, ERR_INVALID_ARGUMENT, ERR_DIMENSION_MISMATCH, ERR_NOT_SPD, ERR_NOT_CONVERGED
     ERR_OUT_OF_MEMORY, ERR_UNSUPPORTED = range(9)
 COUNTSKETCH, SJLT = 0, 1
 K_SORT, K_SKETCH, K_SJLT, K_CSR, K_GRAD, K_REDUCE, K_GRAM, K_CHOL, K_PG = range(9)
-KERNEL_GROUPS = ("sort", "sketch", "sjlt", "csr", "grad", "reduce", "gram", "chol", "pg")
+KERNEL_GROUPS = ("sort", "sketch", "sjlt", "csr", "grad", "reduce", "gram", "chol", "pg", "factor", "apply")
 DENSE, CSR = 0, 1
 
 
@@ -84,6 +84,11 @@ _EXPORTS = {
     "ihs_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "ihs_gram_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ihs_ols_factor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p]),
+    "ihs_ols_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "ihs_ols_lookahead_step": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.POINTER(SketchSpec), C.c_uint64,
+                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                         C.c_void_p]),
     "ihs_l1ball_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_double,
                                     C.POINTER(InnerCfg), C.c_void_p, C.c_void_p]),
     "ihs_lasso_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_double,
@@ -341,6 +346,40 @@ def ihs_ols_update(H, g, x, out=None, ctx: Context | None = None):
     xn = out if out is not None else torch.empty_like(x)
     _check(lib().ihs_ols_update(ctx._bind(), _p(H), _p(g), x.numel(), _p(x), _p(xn)), "ihs_ols_update")
     return xn
+
+
+def ihs_ols_factor(SA: torch.Tensor, scale: float = 1.0, out=None, ctx: Context | None = None):
+    """Look-ahead OLS, part 1: Hinv = (scale^2 SA^T SA)^{-1} (d <= 128), computed on
+    the context's factor stream after the work already on its stream.  Joined by
+    the next ihs_ols_apply / ctx.synchronize(); read Hinv only after one of them."""
+    ctx = ctx or default_context(SA.device)
+    m, d = SA.shape
+    Hinv = out if out is not None else _f64((d, d), SA.device)
+    _check(lib().ihs_ols_factor(ctx._bind(), _p(SA), m, d, float(scale), _p(Hinv)), "ihs_ols_factor")
+    return Hinv
+
+
+def ihs_ols_apply(Hinv, g, x, out=None, ctx: Context | None = None):
+    """Look-ahead OLS, part 2: x_next = x + Hinv g (after the pending factor)."""
+    ctx = ctx or default_context(Hinv.device)
+    xn = out if out is not None else torch.empty_like(x)
+    _check(lib().ihs_ols_apply(ctx._bind(), _p(Hinv), _p(g), x.numel(), _p(x), _p(xn)), "ihs_ols_apply")
+    return xn
+
+
+def ihs_ols_lookahead_step(A, spec: Spec, it_next: int, b, x, Hinv, SA_next=None, Hinv_next=None, g=None,
+                           out=None, ctx: Context | None = None):
+    """One look-ahead OLS step on one rank (ihs.h): g at x, S^{it_next} A into
+    SA_next and its factor into Hinv_next (both optional), x_next = x + Hinv g.
+    Returns (x_next, g)."""
+    A = as_matrix(A)
+    ctx = ctx or default_context(A.device)
+    g = g if g is not None else _f64(A.d, A.device)
+    xn = out if out is not None else torch.empty_like(x)
+    mc, sp = A.c(), spec.c()
+    _check(lib().ihs_ols_lookahead_step(ctx._bind(), C.byref(mc), C.byref(sp), it_next, _p(b), _p(x), _p(Hinv),
+                                        _p(SA_next), _p(Hinv_next), _p(g), _p(xn)), "ihs_ols_lookahead_step")
+    return xn, g
 
 
 def inner_cfg(max_inner=20000, power_iters=50, inner_tol=1e-14, lip_safety=1.05) -> InnerCfg:

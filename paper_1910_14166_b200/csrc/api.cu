@@ -89,6 +89,17 @@ struct ihs_ctx_s {
     const void *A = nullptr;
   } pre;
   int pre_set = 0;
+  // Look-ahead OLS factor (ihs_ols_factor): its own high-priority stream so
+  // the Gram + Cholesky + inverse of the NEXT sketch run beside this pass's
+  // gather; joined into `stream` by ihs_ols_apply / synchronize / destroy.
+  cudaStream_t fstream = nullptr;
+  cudaEvent_t ev_fmain = nullptr;
+  struct Factor {  // one in-flight factor per output buffer
+    const double *Hinv = nullptr;
+    cudaEvent_t done = nullptr;
+    bool pending = false;
+  } fac[4];
+  bool f_pending = false;  // any fac[k].pending
   int64_t pg_warm_d = -1;  // S_PG holds a power-iteration vector for this d
   struct Rec { int group; cudaEvent_t a, b; };
   std::vector<Rec> recs;
@@ -132,12 +143,14 @@ ihs_status from_cuda(cudaError_t e) {
 #define IHS_CUDA(expr) IHS_TRY(from_cuda(expr))
 
 void join_side(ihs_ctx c);
+void join_factor(ihs_ctx c);
 
 template <typename T>
 ihs_status scratch(ihs_ctx c, Slot s, size_t bytes, T **out) {
   bytes = std::max<size_t>(bytes, 256);
   if (c->cap[s] < bytes) {
     join_side(c);  // the side stream may still use this slot
+    join_factor(c);  // so may the factor stream (S_PACK)
     if (c->slot[s]) {
       cudaError_t e = cudaFreeAsync(c->slot[s], c->stream);
       if (e != cudaSuccess) return from_cuda(e);
@@ -188,6 +201,17 @@ void join_side(ihs_ctx c) {
   }
 }
 
+void join_factor(ihs_ctx c) {
+  if (c->f_pending) {
+    for (auto &f : c->fac)
+      if (f.pending) {
+        cudaStreamWaitEvent(c->stream, f.done, 0);
+        f.pending = false;
+      }
+    c->f_pending = false;
+  }
+}
+
 ihs_status check_spec(const ihs_sketch_spec *spec) {
   if (!spec) return IHS_ERR_INVALID_ARGUMENT;
   if (spec->m < 1 || spec->s < 1) return IHS_ERR_INVALID_ARGUMENT;
@@ -222,8 +246,24 @@ ihs_status check_matrix(const ihs_matrix *A) {
 double spec_scale(const ihs_sketch_spec *spec) { return spec->s > 1 ? 1.0 / std::sqrt((double)spec->s) : 1.0; }
 
 // ---- a2 (and a5 when g != null), local partials ------------------------------
+unsigned *reduce_counter(ihs_ctx c) { return reinterpret_cast<unsigned *>(c->d_status + 1); }
+
+// One look-ahead OLS step riding on a pass (no all-reduce between the pass and
+// the update, i.e. one rank): after the gathers, the factor of this pass's SA
+// (S^{t+1} A) is enqueued into Hinv_next (if set); the gradient reduction then
+// also applies x_next = x + Hinv g in its last CTA (one launch).
+struct LookStep {
+  const double *Hinv;
+  const double *x;
+  double *x_next;
+  double *Hinv_next;
+};
+ihs_status ols_factor_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *Hinv);
+ihs_status wait_factor(ihs_ctx c, const double *Hinv);
+ihs_status ols_apply_impl(ihs_ctx c, const double *Hinv, const double *g, int64_t d, const double *x, double *xn);
+
 ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter,
-                            const double *b, const double *x, double *SA, double *g) {
+                            const double *b, const double *x, double *SA, double *g, const LookStep *ls = nullptr) {
   const uint64_t key = iter_key(spec->seed, iter);
   const int64_t n = A->n_rows, d = A->n_cols, m = spec->m;
   const int s = spec->s;
@@ -295,7 +335,8 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
         nseg = (int)std::max<int64_t>(1, std::min<int64_t>((7 * (int64_t)c->num_sms + M * nb - 1) / (M * nb),
                                                            n / (M * 512)));
       double *gpart = nullptr;
-      if (fuse) IHS_TRY(scratch(c, S_GPART, (size_t)M * d * 8 * nseg, &gpart));
+      if (fuse)
+        IHS_TRY(scratch(c, S_GPART, ((size_t)M * d * nseg + reduce_rows_tmp(M * nseg, d)) * 8, &gpart));
       double *sapart = nullptr;
       if (nseg > 1) IHS_TRY(scratch(c, S_SJLT, (size_t)nseg * nb * M * d * 8, &sapart));
       const double scale = spec_scale(spec);
@@ -358,8 +399,11 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
         }
       }
       if (fuse) {
-        Prof pr(c, IHS_K_REDUCE);
-        IHS_CUDA(launch_reduce_rows(gpart, M * nseg, d, g, st, lc_of(c)));
+        if (ls && ls->Hinv_next) IHS_TRY(ols_factor_impl(c, SA, m, d, 1.0, ls->Hinv_next));
+        if (ls) IHS_TRY(wait_factor(c, ls->Hinv));
+        Prof pr(c, ls ? IHS_K_APPLY : IHS_K_REDUCE);
+        IHS_CUDA(launch_reduce_rows(gpart, M * nseg, d, g, gpart + M * nseg * d, reduce_counter(c), st, lc_of(c),
+                                    ls ? ls->Hinv : nullptr, ls ? ls->x : nullptr, ls ? ls->x_next : nullptr));
       }
     } else if (use_stream) {
       double *part;
@@ -379,16 +423,21 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
     if (d > 1024) return IHS_ERR_UNSUPPORTED;
     const int64_t nb = grad_dense_blocks(n, d, c->num_sms);
     double *gpart;
-    IHS_TRY(scratch(c, S_GPART, (size_t)nb * d * 8, &gpart));
+    IHS_TRY(scratch(c, S_GPART, ((size_t)nb * d + reduce_rows_tmp(nb, d)) * 8, &gpart));
     if (n == 0) {
       IHS_CUDA(cudaMemsetAsync(g, 0, (size_t)d * 8, st));
+      if (ls && ls->Hinv_next && SA) IHS_TRY(ols_factor_impl(c, SA, m, d, 1.0, ls->Hinv_next));
+      if (ls) IHS_TRY(ols_apply_impl(c, ls->Hinv, g, d, ls->x, ls->x_next));
     } else {
       {
         Prof pr(c, IHS_K_GRAD);
         IHS_CUDA(launch_grad_dense(A->values, n, d, b, x, gpart, nb, st, lc_of(c)));
       }
-      Prof pr(c, IHS_K_REDUCE);
-      IHS_CUDA(launch_reduce_rows(gpart, nb, d, g, st, lc_of(c)));
+      if (ls && ls->Hinv_next && SA) IHS_TRY(ols_factor_impl(c, SA, m, d, 1.0, ls->Hinv_next));
+      if (ls) IHS_TRY(wait_factor(c, ls->Hinv));
+      Prof pr(c, ls ? IHS_K_APPLY : IHS_K_REDUCE);
+      IHS_CUDA(launch_reduce_rows(gpart, nb, d, g, gpart + nb * d, reduce_counter(c), st, lc_of(c),
+                                  ls ? ls->Hinv : nullptr, ls ? ls->x : nullptr, ls ? ls->x_next : nullptr));
     }
   }
   return IHS_OK;
@@ -427,6 +476,66 @@ ihs_status gram_ols_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, doub
   }
   IHS_TRY(gram_impl(c, SA, m, d, scale, H));
   return ols_impl(c, H, g, d, x, xn);
+}
+
+// Look-ahead OLS, part 1: Hinv = (scale^2 SA^T SA)^{-1} on the factor stream,
+// ordered after everything already enqueued on the ctx stream.  Completion is
+// tracked per output buffer, so ihs_ols_apply on the previous buffer does not
+// wait for this factor (the look-ahead loop enqueues the factor of S^{t+1}
+// before the apply of H_t^{-1}, so that its cluster is placed before the next
+// pass's gather fills the SMs).
+ihs_status ols_factor_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *Hinv) {
+  if (!gram_ols_supported(d) || m < 1) return IHS_ERR_UNSUPPORTED;
+  if (!c->fstream) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    IHS_CUDA(cudaStreamCreateWithPriority(&c->fstream, cudaStreamNonBlocking, hi));
+    IHS_CUDA(cudaEventCreateWithFlags(&c->ev_fmain, cudaEventDisableTiming));
+    for (auto &f : c->fac) IHS_CUDA(cudaEventCreateWithFlags(&f.done, cudaEventDisableTiming));
+  }
+  ihs_ctx_s::Factor *slot = nullptr;
+  for (auto &f : c->fac)
+    if (f.pending && f.Hinv == Hinv) slot = &f;  // a rewrite of the same buffer: fstream order suffices
+  if (!slot)
+    for (auto &f : c->fac)
+      if (!f.pending) {
+        slot = &f;
+        break;
+      }
+  if (!slot) {
+    join_factor(c);
+    slot = &c->fac[0];
+  }
+  IHS_CUDA(cudaEventRecord(c->ev_fmain, c->stream));
+  IHS_CUDA(cudaStreamWaitEvent(c->fstream, c->ev_fmain, 0));
+  static const int max_cluster = getenv("IHS_LOOKAHEAD_CLUSTER") ? atoi(getenv("IHS_LOOKAHEAD_CLUSTER")) : 8;
+  {
+    Prof pr(c, IHS_K_FACTOR, c->fstream);
+    IHS_CUDA(launch_ols_factor(SA, m, d, scale, Hinv, c->d_status, max_cluster, c->fstream, lc_of(c)));
+  }
+  IHS_CUDA(cudaEventRecord(slot->done, c->fstream));
+  slot->Hinv = Hinv;
+  slot->pending = true;
+  c->f_pending = true;
+  return IHS_OK;
+}
+
+// Look-ahead OLS, part 2: x_next = x + Hinv g on the ctx stream, after the
+// pending factor that writes Hinv (if any).
+ihs_status wait_factor(ihs_ctx c, const double *Hinv) {
+  for (auto &f : c->fac)
+    if (f.pending && f.Hinv == Hinv) {
+      IHS_CUDA(cudaStreamWaitEvent(c->stream, f.done, 0));
+      f.pending = false;
+    }
+  return IHS_OK;
+}
+
+ihs_status ols_apply_impl(ihs_ctx c, const double *Hinv, const double *g, int64_t d, const double *x, double *xn) {
+  IHS_TRY(wait_factor(c, Hinv));
+  Prof pr(c, IHS_K_APPLY);
+  IHS_CUDA(launch_ols_apply(Hinv, g, d, x, xn, c->stream, lc_of(c)));
+  return IHS_OK;
 }
 
 ihs_inner_cfg default_inner() {
@@ -470,6 +579,7 @@ bool is_host_ptr(const void *p) {
 }
 
 ihs_status sync_status(ihs_ctx c) {
+  join_factor(c);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return from_cuda(e);
   int st = 0;
@@ -480,6 +590,61 @@ ihs_status sync_status(ihs_ctx c) {
     cudaMemcpy(c->d_status, &zero, sizeof(int), cudaMemcpyHostToDevice);
   }
   return (ihs_status)st;
+}
+
+// Look-ahead OLS loop (ihs_ols_factor / ihs_ols_apply):
+// a prologue pass forms S^{iter0} A and its H^{-1}; pass t then reads A once
+// for [S^{t+1} A | g^t] (one all-reduce), applies x^{t+1} = x^t + H_t^{-1} g^t,
+// and factorises H_{t+1} on the factor stream beside pass t + 1.  The last
+// pass forms g only.  T + 1 passes over A for T iterations, none of the d x d
+// work on the critical path but the apply.
+ihs_status ols_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, const double *b,
+                              uint64_t iter0, int32_t T, double *xh) {
+  const int64_t d = A->n_cols, m = spec->m, pk = m * d + d;
+  double *packs, *Hinv;
+  IHS_TRY(scratch(c, S_PACK, (size_t)2 * pk * 8, &packs));
+  IHS_TRY(scratch(c, S_H, (size_t)2 * d * d * 8, &Hinv));
+  auto allreduce = [&](double *buf, int64_t cnt) -> ihs_status {
+    if (c->world > 1) {
+      if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
+      if (g_nccl.AllReduce(buf, buf, (size_t)cnt, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
+        return IHS_ERR_COMM;
+    }
+    return IHS_OK;
+  };
+  IHS_TRY(sketch_grad_impl(c, A, spec, iter0, nullptr, nullptr, packs, nullptr));
+  IHS_TRY(allreduce(packs, m * d));
+  IHS_TRY(ols_factor_impl(c, packs, m, d, 1.0, Hinv));
+  for (int32_t t = 0; t < T; ++t) {
+    const int cur = t & 1, nxt = cur ^ 1;
+    const bool more = t + 1 < T;
+    double *SAn = packs + nxt * pk, *gn = SAn + m * d;
+    const double *x = xh + (int64_t)t * d;
+    double *xn = xh + (int64_t)(t + 1) * d;
+    if (c->world == 1) {  // factor, gradient reduction and update inside the pass
+      const LookStep ls{Hinv + cur * d * d, x, xn, more ? Hinv + nxt * d * d : nullptr};
+      IHS_TRY(sketch_grad_impl(c, A, spec, iter0 + (uint64_t)t + 1, b, x, more ? SAn : nullptr, gn, &ls));
+      continue;
+    }
+    IHS_TRY(sketch_grad_impl(c, A, spec, iter0 + (uint64_t)t + 1, b, x, more ? SAn : nullptr, gn));
+    IHS_TRY(more ? allreduce(SAn, pk) : allreduce(gn, d));
+    if (more) IHS_TRY(ols_factor_impl(c, SAn, m, d, 1.0, Hinv + nxt * d * d));
+    IHS_TRY(ols_apply_impl(c, Hinv + cur * d * d, gn, d, x, xn));
+  }
+  return IHS_OK;
+}
+
+// The look-ahead schedule pays when a pass over A is long next to the Gram +
+// Cholesky it hides: dense, d <= 128, n d >= 2^24 (per rank), T >= 3, and a
+// CountSketch (an SJLT pass is s gathers, next to which the d x d work is
+// < 0.3% on C5 and the measured difference was within run-to-run noise).
+// IHS_LOOKAHEAD=0 disables it, =1 uses it whenever supported.
+bool use_lookahead(const ihs_matrix *A, const ihs_sketch_spec *spec, int32_t T) {
+  static const char *env = getenv("IHS_LOOKAHEAD");
+  const int64_t d = A->n_cols;
+  const bool ok = A->layout == IHS_DENSE_ROW_MAJOR && gram_ols_supported(d) && spec->m >= 1 && T >= 1;
+  if (env) return ok && std::strcmp(env, "0") != 0;
+  return ok && spec->s == 1 && T >= 3 && A->n_rows * d >= (int64_t(1) << 24);
 }
 
 // Shared IHS loop (a1-a7).  constraint 0 = OLS, 1 = l1 ball.
@@ -552,7 +717,9 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
   if (trace)
     for (auto &e : ev) IHS_CUDA(cudaEventCreate(&e));
   ihs_status result = IHS_OK;
-  for (int32_t t = 0; t < T; ++t) {
+  const bool lookahead = constraint == 0 && !trace && use_lookahead(&A, spec, T);
+  if (lookahead) IHS_TRY(ols_lookahead_loop(c, &A, spec, b, iter0, T, xh));
+  for (int32_t t = 0; !lookahead && t < T; ++t) {
     const double *x = xh + (int64_t)t * d;
     double *xn = xh + (int64_t)(t + 1) * d;
     if (trace) cudaEventRecord(ev[0], st);
@@ -644,11 +811,11 @@ ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
   c->device = device;
   c->stream = (cudaStream_t)stream;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMalloc(&c->d_status, sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&c->d_status, 4 * sizeof(int)) != cudaSuccess) {  // [0] status, [1] reduce counter
     delete c;
     return IHS_ERR_OUT_OF_MEMORY;
   }
-  cudaMemset(c->d_status, 0, sizeof(int));
+  cudaMemset(c->d_status, 0, 4 * sizeof(int));
   if (const char *e = getenv("IHS_GATHER"))
     c->gather = !std::strcmp(e, "ldg") ? 0 : !std::strcmp(e, "async") ? 2 : 1;
   if (const char *e = getenv("IHS_PREFETCH")) c->prefetch = std::strcmp(e, "0") != 0;
@@ -659,7 +826,14 @@ ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
 ihs_status ihs_ctx_destroy(ihs_ctx c) {
   if (!c) return IHS_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
+  join_factor(c);
   cudaStreamSynchronize(c->stream);
+  if (c->fstream) {
+    cudaStreamSynchronize(c->fstream);
+    cudaStreamDestroy(c->fstream);
+    cudaEventDestroy(c->ev_fmain);
+    for (auto &f : c->fac) cudaEventDestroy(f.done);
+  }
   if (c->side) {
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);
@@ -677,6 +851,7 @@ ihs_status ihs_ctx_destroy(ihs_ctx c) {
 
 ihs_status ihs_ctx_set_stream(ihs_ctx c, void *stream) {
   if (!c) return IHS_ERR_INVALID_ARGUMENT;
+  if (c->f_pending && (cudaStream_t)stream != c->stream) join_factor(c);
   c->stream = (cudaStream_t)stream;
   return IHS_OK;
 }
@@ -792,6 +967,20 @@ ihs_status ihs_sketch_grad(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec
   return sketch_grad_impl(c, A, spec, iter, b, x, SA, gout);
 }
 
+ihs_status ihs_ols_lookahead_step(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter_next,
+                                  const double *b, const double *x, const double *Hinv, double *SA_next,
+                                  double *Hinv_next, double *gout, double *xn) {
+  if (!c || !x || !Hinv || !gout || !xn || (!b && A && A->n_rows > 0) || (Hinv_next && !SA_next))
+    return IHS_ERR_INVALID_ARGUMENT;
+  IHS_TRY(check_matrix(A));
+  IHS_TRY(check_spec(spec));
+  if (A->layout != IHS_DENSE_ROW_MAJOR || A->n_cols > 1024) return IHS_ERR_UNSUPPORTED;
+  if (Hinv_next && !gram_ols_supported(A->n_cols)) return IHS_ERR_UNSUPPORTED;
+  DevGuard g(c->device);
+  const LookStep ls{Hinv, x, xn, Hinv_next};
+  return sketch_grad_impl(c, A, spec, iter_next, b, x, SA_next, gout, &ls);
+}
+
 ihs_status ihs_gram(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {
   if (!c || !SA || !H || m < 1 || d < 1 || !std::isfinite(scale)) return IHS_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
@@ -803,6 +992,19 @@ ihs_status ihs_gram_ols_update(ihs_ctx c, const double *SA, int64_t m, int64_t d
   if (!c || !SA || !gv || !x || !xn || !H || d < 1 || m < 0) return IHS_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
   return gram_ols_impl(c, SA, m, d, scale, gv, x, xn, H);
+}
+
+ihs_status ihs_ols_factor(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *Hinv) {
+  if (!c || !SA || !Hinv || m < 1 || d < 1 || !std::isfinite(scale)) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return ols_factor_impl(c, SA, m, d, scale, Hinv);
+}
+
+ihs_status ihs_ols_apply(ihs_ctx c, const double *Hinv, const double *gv, int64_t d, const double *x, double *xn) {
+  if (!c || !Hinv || !gv || !x || !xn || d < 1) return IHS_ERR_INVALID_ARGUMENT;
+  if (d > 1024) return IHS_ERR_UNSUPPORTED;
+  DevGuard g(c->device);
+  return ols_apply_impl(c, Hinv, gv, d, x, xn);
 }
 
 ihs_status ihs_ols_update(ihs_ctx c, const double *H, const double *gv, int64_t d, const double *x, double *xn) {

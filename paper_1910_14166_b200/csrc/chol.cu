@@ -45,9 +45,10 @@ constexpr int kBThreads = 256;
 // The factorisation and solves on the loaded augmented Ls (shared memory), by
 // the whole CTA of kBThreads threads: shared by chol_blocked_kernel (H from
 // global) and gram_ols_kernel (H reduced from a cluster's Gram partials).
+// Factorisation only: Ls holds L (lower triangle) and rdiag[j] = 1 / L_jj on
+// return; true (for every thread) if a pivot was not positive.
 template <int NBLK>
-__device__ __forceinline__ void chol_blocked_body(double *Ls, double *rdiag, double *colbuf, int &s_bad, int d,
-                                                  const double *__restrict__ x, double *x_next, int *status) {
+__device__ __forceinline__ bool chol_factor_body(double *Ls, double *rdiag, double *colbuf, int &s_bad) {
   constexpr int D = 32 * NBLK;
   constexpr int lda = D + 4;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -98,7 +99,16 @@ __device__ __forceinline__ void chol_blocked_body(double *Ls, double *rdiag, dou
     }
     __syncthreads();
   }
-  if (s_bad) {
+  return s_bad != 0;
+}
+
+template <int NBLK>
+__device__ __forceinline__ void chol_blocked_body(double *Ls, double *rdiag, double *colbuf, int &s_bad, int d,
+                                                  const double *__restrict__ x, double *x_next, int *status) {
+  constexpr int D = 32 * NBLK;
+  constexpr int lda = D + 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (chol_factor_body<NBLK>(Ls, rdiag, colbuf, s_bad)) {
     for (int i = tid; i < d; i += kBThreads) x_next[i] = x[i];
     if (tid == 0) set_status(status, 3 /* IHS_ERR_NOT_SPD */);
     return;
@@ -127,6 +137,51 @@ __device__ __forceinline__ void chol_blocked_body(double *Ls, double *rdiag, dou
       const int i = lane + 32 * s;
       if (i < d) x_next[i] = x[i] + z[s];
     }
+  }
+}
+
+// H^{-1} = L^{-T} L^{-1} from the factor in Ls / rdiag (for the look-ahead
+// OLS step, api.cu): Y = L^{-1} by forward substitution on all D right-hand
+// sides at once (row i of Y from rows < i; thread c owns column c, the L row is
+// a shared-memory broadcast), Y packed by rows in Yp (Y[i][c] at i(i+1)/2 + c),
+// then Hinv = Y^T Y (thread per entry, i fastest so the Y loads are contiguous).
+// The identity padding rows (>= d) of L give Y[k][c] = 0 for k >= d > c.
+template <int NBLK>
+__device__ __forceinline__ void chol_inverse_body(const double *Ls, const double *rdiag, double *Yp, int d,
+                                                  double *__restrict__ Hinv) {
+  constexpr int D = 32 * NBLK;
+  constexpr int lda = D + 4;
+  const int tid = threadIdx.x;
+#pragma unroll 1
+  for (int i = 0; i < d; ++i) {
+    const double *Li = Ls + i * lda;
+    for (int c = tid; c <= i; c += kBThreads) {
+      double s0 = (c == i) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int k = c;
+      for (; k + 3 < i; k += 4) {
+        s0 -= Li[k] * Yp[k * (k + 1) / 2 + c];
+        s1 -= Li[k + 1] * Yp[(k + 1) * (k + 2) / 2 + c];
+        s2 -= Li[k + 2] * Yp[(k + 2) * (k + 3) / 2 + c];
+        s3 -= Li[k + 3] * Yp[(k + 3) * (k + 4) / 2 + c];
+      }
+      for (; k < i; ++k) s0 -= Li[k] * Yp[k * (k + 1) / 2 + c];
+      Yp[i * (i + 1) / 2 + c] = ((s0 + s1) + (s2 + s3)) * rdiag[i];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < d * d; e += kBThreads) {
+    const int i = e % d, j = e / d;
+    if (i < j) continue;
+    double s0 = 0.0, s1 = 0.0;
+    int k = i;
+    for (; k + 1 < d; k += 2) {
+      s0 += Yp[k * (k + 1) / 2 + i] * Yp[k * (k + 1) / 2 + j];
+      s1 += Yp[(k + 1) * (k + 2) / 2 + i] * Yp[(k + 1) * (k + 2) / 2 + j];
+    }
+    if (k < d) s0 += Yp[k * (k + 1) / 2 + i] * Yp[k * (k + 1) / 2 + j];
+    const double v = s0 + s1;
+    Hinv[(int64_t)j * d + i] = v;
+    Hinv[(int64_t)i * d + j] = v;
   }
 }
 
@@ -165,11 +220,13 @@ __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *_
 // Replaces the Gram launch pair + the Cholesky launch (one launch, H never
 // round-trips through L2 on the critical path; H_out, if given, gets a copy).
 constexpr int kGoRows = 64;  // SA rows per staging chunk
-template <int NBLK>
+// INV (the look-ahead factor, api.cu): no right-hand side; CTA 0 factorises
+// and writes H^{-1} to Hinv (zeros and IHS_ERR_NOT_SPD on a non-positive pivot).
+template <int NBLK, bool INV>
 __global__ void __launch_bounds__(kBThreads, 1) gram_ols_kernel(const double *__restrict__ SA, int64_t m, int d,
                                                                double scale2, const double *__restrict__ g,
                                                                const double *__restrict__ x, double *x_next,
-                                                               double *H_out, int *status) {
+                                                               double *H_out, int *status, double *Hinv) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   constexpr int D = 32 * NBLK;
@@ -189,7 +246,7 @@ __global__ void __launch_bounds__(kBThreads, 1) gram_ols_kernel(const double *__
         if (i >= d)  // identity padding; the lower triangle of H arrives from the reducers
           for (int c = lane; c <= i; c += 32) Ls[i * lda + c] = (c == i ? 1.0 : 0.0);
       } else {
-        for (int c = lane; c < D; c += 32) Ls[i * lda + c] = (i == D && c < d) ? g[c] : 0.0;
+        for (int c = lane; c < D; c += 32) Ls[i * lda + c] = (!INV && i == D && c < d) ? g[c] : 0.0;
       }
     }
   } else {
@@ -269,21 +326,32 @@ __global__ void __launch_bounds__(kBThreads, 1) gram_ols_kernel(const double *__
   }
   cluster.sync();
   if (rank != 0) return;
-  chol_blocked_body<NBLK>(sm, sm + DA * lda, colbuf, s_bad, d, x, x_next, status);
+  if constexpr (INV) {
+    if (chol_factor_body<NBLK>(sm, sm + DA * lda, colbuf, s_bad)) {
+      for (int e = tid; e < d * d; e += kBThreads) Hinv[e] = 0.0;
+      if (tid == 0) set_status(status, 3 /* IHS_ERR_NOT_SPD */);
+      return;
+    }
+    chol_inverse_body<NBLK>(sm, sm + DA * lda, sm + DA * lda + D, d, Hinv);
+  } else {
+    chol_blocked_body<NBLK>(sm, sm + DA * lda, colbuf, s_bad, d, x, x_next, status);
+  }
 }
 
-template <int NBLK>
+template <int NBLK, bool INV>
 cudaError_t launch_gram_ols_t(const double *SA, int64_t m, int d, double scale, const double *g, const double *x,
-                              double *x_next, double *H_out, int *status, cudaStream_t st) {
+                              double *x_next, double *H_out, int *status, double *Hinv, int max_cluster,
+                              cudaStream_t st) {
   constexpr int D = 32 * NBLK;
-  const size_t smem_chol = ((size_t)(D + 8) * (D + 4) + D) * 8;
+  const size_t smem_chol = ((size_t)(D + 8) * (D + 4) + D + (INV ? (size_t)D * (D + 1) / 2 : 0)) * 8;
   const size_t smem_gram = ((size_t)kGoRows * (D + 4) + (size_t)D * D) * 8;
   const size_t smem = std::max(smem_chol, smem_gram);
-  auto kern = gram_ols_kernel<NBLK>;
+  auto kern = gram_ols_kernel<NBLK, INV>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaError_t e = cudaErrorUnknown;
-  for (int cs : {16, 8}) {
+  for (int cs : {16, 8, 4}) {
+    if (cs > max_cluster) continue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
     cfg.blockDim = dim3(kBThreads);
@@ -296,7 +364,7 @@ cudaError_t launch_gram_ols_t(const double *SA, int64_t m, int d, double scale, 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, SA, m, d, scale * scale, g, x, x_next, H_out, status);
+    e = cudaLaunchKernelEx(&cfg, kern, SA, m, d, scale * scale, g, x, x_next, H_out, status, Hinv);
     if (e == cudaSuccess) return e;
     cudaGetLastError();
   }
@@ -326,14 +394,78 @@ bool gram_ols_supported(int64_t d) { return d >= 1 && d <= 128; }
 cudaError_t launch_gram_ols(const double *SA, int64_t m, int64_t d, double scale, const double *g, const double *x,
                             double *x_next, double *H_out, int *status, cudaStream_t st, LaunchCounter lc) {
   cudaError_t e;
+#define GO(NB) launch_gram_ols_t<NB, false>(SA, m, (int)d, scale, g, x, x_next, H_out, status, nullptr, 16, st)
   switch ((d + 31) / 32) {
-    case 1: e = launch_gram_ols_t<1>(SA, m, (int)d, scale, g, x, x_next, H_out, status, st); break;
-    case 2: e = launch_gram_ols_t<2>(SA, m, (int)d, scale, g, x, x_next, H_out, status, st); break;
-    case 3: e = launch_gram_ols_t<3>(SA, m, (int)d, scale, g, x, x_next, H_out, status, st); break;
-    default: e = launch_gram_ols_t<4>(SA, m, (int)d, scale, g, x, x_next, H_out, status, st); break;
+    case 1: e = GO(1); break;
+    case 2: e = GO(2); break;
+    case 3: e = GO(3); break;
+    default: e = GO(4); break;
   }
+#undef GO
   lc.add();
   return e;
+}
+
+// The look-ahead factor: Hinv = (scale^2 SA^T SA)^{-1} in one cluster launch of
+// at most max_cluster CTAs (it runs beside the sketch gather of the next pass,
+// so it should leave that kernel's wave of bucket CTAs room on the other SMs).
+cudaError_t launch_ols_factor(const double *SA, int64_t m, int64_t d, double scale, double *Hinv, int *status,
+                              int max_cluster, cudaStream_t st, LaunchCounter lc) {
+  cudaError_t e;
+#define GO(NB) launch_gram_ols_t<NB, true>(SA, m, (int)d, scale, nullptr, nullptr, nullptr, nullptr, status, Hinv, \
+                                           max_cluster, st)
+  switch ((d + 31) / 32) {
+    case 1: e = GO(1); break;
+    case 2: e = GO(2); break;
+    case 3: e = GO(3); break;
+    default: e = GO(4); break;
+  }
+#undef GO
+  lc.add();
+  return e;
+}
+
+// x_next = x + Hinv g: one CTA, warp w owns rows w, w + 32, ...; lanes stride
+// the row (coalesced) and a fixed shuffle tree sums them (deterministic).
+__global__ void __launch_bounds__(1024) ols_apply_kernel(const double *__restrict__ Hinv,
+                                                         const double *__restrict__ g, int d,
+                                                         const double *__restrict__ x, double *x_next) {
+  __shared__ double gs[1024];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c = threadIdx.x; c < d; c += 1024) gs[c] = g[c];
+  __syncthreads();
+  // warp w rows 4w.., 4 rows x 4 column chunks of loads in flight before the adds
+  const int nk = (d + 31) / 32;
+  for (int i0 = warp * 4; i0 < d; i0 += 128) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int kb = 0; kb < nk; kb += 4) {
+      double h[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = lane + 32 * (kb + k);
+          h[q][k] = (i0 + q < d && c < d) ? Hinv[(int64_t)(i0 + q) * d + c] * gs[c] : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += (h[q][0] + h[q][1]) + (h[q][2] + h[q][3]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double v = acc[q];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && i0 + q < d) x_next[i0 + q] = x[i0 + q] + v;
+    }
+  }
+}
+
+cudaError_t launch_ols_apply(const double *Hinv, const double *g, int64_t d, const double *x, double *x_next,
+                             cudaStream_t st, LaunchCounter lc) {
+  if (d > 1024) return cudaErrorInvalidValue;
+  ols_apply_kernel<<<1, 1024, 0, st>>>(Hinv, g, (int)d, x, x_next);
+  lc.add();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,

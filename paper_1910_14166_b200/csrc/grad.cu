@@ -139,33 +139,35 @@ __global__ void sqnorm_csr_kernel(int64_t n, const int64_t *__restrict__ row_ptr
   }
 }
 
-// out[c] = sum_r part[r*d + c]: warp w sums rows w, w+32, ... ascending; then
-// warp 0 adds the 32 warp sums in order.  Fixed order => deterministic.
+// out[y*d + c] = sum over rows r in [y*rpb, min(rows, (y+1)*rpb)) of part[r*d + c]:
+// blockIdx.y splits the rows, warp w sums rows r0+w, r0+w+W, ... ascending;
+// then warp 0 adds the W warp sums in order.  Fixed order => deterministic.
 __global__ void __launch_bounds__(1024) reduce_rows_kernel(const double *__restrict__ part, int64_t rows, int d,
-                                                           double *__restrict__ out) {
+                                                           int64_t rpb, double *__restrict__ out) {
   __shared__ double sm[32][33];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int c = blockIdx.x * 32 + lane;
+  const int64_t r0 = (int64_t)blockIdx.y * rpb, r1 = min(rows, r0 + rpb);
   // 4 interleaved partial sums per thread (independent L2 loads in flight),
   // combined in a fixed order: deterministic
   double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
   if (c < d) {
-    int64_t r = warp;
-    for (; r + 96 < rows; r += 128) {
+    int64_t r = r0 + warp;
+    for (; r + 3 * nw < r1; r += 4 * nw) {
       s0 += part[r * d + c];
-      s1 += part[(r + 32) * d + c];
-      s2 += part[(r + 64) * d + c];
-      s3 += part[(r + 96) * d + c];
+      s1 += part[(r + nw) * d + c];
+      s2 += part[(r + 2 * nw) * d + c];
+      s3 += part[(r + 3 * nw) * d + c];
     }
-    for (; r < rows; r += 32) s0 += part[r * d + c];
+    for (; r < r1; r += nw) s0 += part[r * d + c];
   }
   const double s = (s0 + s1) + (s2 + s3);
   sm[warp][lane] = s;
   __syncthreads();
   if (warp == 0 && c < d) {
     double t = 0.0;
-    for (int w = 0; w < 32; ++w) t += sm[w][lane];
-    out[c] = t;
+    for (int w = 0; w < nw; ++w) t += sm[w][lane];
+    out[(int64_t)blockIdx.y * d + c] = t;
   }
 }
 
@@ -234,9 +236,103 @@ cudaError_t launch_grad_dense(const double *A, int64_t n, int64_t d, const doubl
   return cudaGetLastError();
 }
 
-cudaError_t launch_reduce_rows(const double *part, int64_t rows, int64_t d, double *out, cudaStream_t st,
-                               LaunchCounter lc) {
-  reduce_rows_kernel<<<(unsigned)((d + 31) / 32), 1024, 0, st>>>(part, rows, (int)d, out);
+int64_t reduce_rows_tmp(int64_t rows, int64_t d) {
+  return ((rows + kReduceRowsPerCta - 1) / kReduceRowsPerCta) * d;
+}
+
+// One launch for out[c] = sum_r part[r*d + c]: CTA (x, y) sums rows
+// [y*64, (y+1)*64) of columns [32x, 32x + 32) into tmp[y*d + c] (16 warps, a
+// fixed order); the last CTA to finish (device-scope counter, left at 0) adds
+// the R = gridDim.y partials of every column in order into out (deterministic)
+// and, when Hinv is given, applies x_next = x + Hinv out (the look-ahead OLS
+// step when no all-reduce separates the two, api.cu).  Replaces a d/32-CTA
+// single level (9.9 us for 1024 x 128 on B200) and a second launch.
+constexpr int kRedThreads = 512;
+__global__ void __launch_bounds__(kRedThreads) reduce_rows_last_kernel(
+    const double *__restrict__ part, int64_t rows, int d, double *tmp, double *out, unsigned *counter,
+    const double *__restrict__ Hinv, const double *__restrict__ x, double *x_next) {
+  constexpr int NW = kRedThreads / 32;
+  __shared__ double sm[NW][33];
+  __shared__ double gs[1024];
+  __shared__ bool last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
+  const int64_t r0 = (int64_t)blockIdx.y * kReduceRowsPerCta, r1 = min(rows, r0 + kReduceRowsPerCta);
+  static_assert(kReduceRowsPerCta == 4 * NW, "four rows per warp");
+  // rows r0 + warp + NW k (k < 4 covers the 64 rows): loads first, then the adds
+  // in k order, so the four L2 round trips overlap (a runtime-bounded loop
+  // would issue each load only after the previous add)
+  double v[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int64_t r = r0 + warp + NW * k;
+    v[k] = (c < d && r < r1) ? part[r * d + c] : 0.0;
+  }
+  sm[warp][lane] = (v[0] + v[1]) + (v[2] + v[3]);
+  __syncthreads();
+  if (warp == 0 && c < d) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) t += sm[w][lane];
+    tmp[(int64_t)blockIdx.y * d + c] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int R = gridDim.y;
+  for (int cc = threadIdx.x; cc < d; cc += kRedThreads) {
+    double acc = 0.0;
+    for (int y0 = 0; y0 < R; y0 += 8) {  // 8 loads in flight, added in y order
+      double u[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) u[k] = (y0 + k < R) ? __ldcg(tmp + (int64_t)(y0 + k) * d + cc) : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += u[k];
+    }
+    out[cc] = acc;
+    gs[cc] = acc;
+  }
+  if (threadIdx.x == 0) *counter = 0;
+  if (!Hinv) return;
+  __syncthreads();
+  // x_next = x + Hinv g: warp w rows 4w.., 4 rows x 4 column chunks of loads in flight
+  const int nk = (d + 31) / 32;
+  for (int i0 = warp * 4; i0 < d; i0 += NW * 4) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int kb = 0; kb < nk; kb += 4) {
+      double h[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int cc = lane + 32 * (kb + k);
+          h[q][k] = (i0 + q < d && cc < d) ? __ldcg(Hinv + (int64_t)(i0 + q) * d + cc) * gs[cc] : 0.0;
+        }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q] += (h[q][0] + h[q][1]) + (h[q][2] + h[q][3]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double v = acc[q];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && i0 + q < d) x_next[i0 + q] = x[i0 + q] + v;
+    }
+  }
+}
+
+cudaError_t launch_reduce_rows(const double *part, int64_t rows, int64_t d, double *out, double *tmp,
+                               unsigned *counter, cudaStream_t st, LaunchCounter lc, const double *Hinv,
+                               const double *x, double *x_next) {
+  if (d > 1024) return cudaErrorInvalidValue;
+  const unsigned gx = (unsigned)((d + 31) / 32);
+  const int64_t R = std::max<int64_t>(1, (rows + kReduceRowsPerCta - 1) / kReduceRowsPerCta);
+  if (R > 65535) return cudaErrorInvalidValue;
+  reduce_rows_last_kernel<<<dim3(gx, (unsigned)R), kRedThreads, 0, st>>>(part, rows, (int)d, tmp, out, counter,
+                                                                          Hinv, x, x_next);
   lc.add();
   return cudaGetLastError();
 }
@@ -269,7 +365,7 @@ cudaError_t launch_pred_err2_impl(int layout, int64_t n, int64_t d, const double
     } else {
       sqnorm_csr_kernel<<<(unsigned)nblocks, 256, 0, st>>>(n, row_ptr, col, values, v, part);
     }
-    reduce_rows_kernel<<<1, 1024, 0, st>>>(part, nblocks, 1, err2 + k);
+    reduce_rows_kernel<<<1, 1024, 0, st>>>(part, nblocks, 1, nblocks, err2 + k);
     lc.add(3);
   }
   return cudaGetLastError();

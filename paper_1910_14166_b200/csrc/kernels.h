@@ -103,8 +103,15 @@ int64_t grad_dense_blocks(int64_t n, int64_t d, int num_sms);
 cudaError_t launch_grad_dense(const double *A, int64_t n, int64_t d, const double *bvec, const double *x,
                               double *gpart, int64_t nblocks, cudaStream_t st, LaunchCounter lc);
 // out[c] = sum_{r < rows} part[r*d + c] (fixed order), c < d.
-cudaError_t launch_reduce_rows(const double *part, int64_t rows, int64_t d, double *out, cudaStream_t st,
-                               LaunchCounter lc);
+constexpr int64_t kReduceRowsPerCta = 64;
+// scratch doubles launch_reduce_rows needs in tmp
+int64_t reduce_rows_tmp(int64_t rows, int64_t d);
+// out = column sums of part (rows x d), one launch, deterministic; counter: a
+// device unsigned that is 0 on entry (left 0).  Hinv != nullptr: also
+// x_next = x + Hinv out.  d <= 1024.
+cudaError_t launch_reduce_rows(const double *part, int64_t rows, int64_t d, double *out, double *tmp,
+                               unsigned *counter, cudaStream_t st, LaunchCounter lc, const double *Hinv = nullptr,
+                               const double *x = nullptr, double *x_next = nullptr);
 
 // ---- a4 Gram on DMMA ---------------------------------------------------------
 struct GramPlan {
@@ -130,6 +137,12 @@ cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const
 
 // a4 + a6 fused (d <= 128): H = scale^2 SA^T SA and x_next = x + H^{-1} g in one
 // cluster launch; H_out (optional) receives H.
+// look-ahead OLS (d <= 128): Hinv = (scale^2 SA^T SA)^{-1} in one cluster
+// launch (<= max_cluster CTAs), then x_next = x + Hinv g (one CTA)
+cudaError_t launch_ols_factor(const double *SA, int64_t m, int64_t d, double scale, double *Hinv, int *status,
+                              int max_cluster, cudaStream_t st, LaunchCounter lc);
+cudaError_t launch_ols_apply(const double *Hinv, const double *g, int64_t d, const double *x, double *x_next,
+                             cudaStream_t st, LaunchCounter lc);
 bool gram_ols_supported(int64_t d);
 cudaError_t launch_gram_ols(const double *SA, int64_t m, int64_t d, double scale, const double *g, const double *x,
                             double *x_next, double *H_out, int *status, cudaStream_t st, LaunchCounter lc);

@@ -51,6 +51,19 @@ class CudaOps:
     def gram_ols(self, SA, g, x, xn, H):
         P.ihs_gram_ols_update(SA, g, x, out=xn, H=H, ctx=self.ctx)
 
+    def sketch(self, A, spec, t, SA):
+        P.ihs_sketch(A, spec, t, out=SA, ctx=self.ctx)
+
+    def ols_factor(self, SA, Hinv):
+        P.ihs_ols_factor(SA, out=Hinv, ctx=self.ctx)
+
+    def ols_apply(self, Hinv, g, x, xn):
+        P.ihs_ols_apply(Hinv, g, x, out=xn, ctx=self.ctx)
+
+    def lookahead_step(self, A, spec, t_next, b, x, Hinv, SA_next, Hinv_next, g, xn):
+        P.ihs_ols_lookahead_step(A, spec, t_next, b, x, Hinv, SA_next=SA_next, Hinv_next=Hinv_next, g=g, out=xn,
+                                 ctx=self.ctx)
+
     def l1(self, H, g, x, tau, cfg, xn, inner):
         P.ihs_l1ball_update(H, g, x, tau, cfg=cfg, out=xn, inner=inner, ctx=self.ctx)
 
@@ -61,11 +74,32 @@ class CudaOps:
         return P.ihs_pred_err2(A, X, xref, ctx=self.ctx)
 
 
+def lookahead_default(A, d: int, spec: P.Spec) -> bool:
+    """The look-ahead OLS schedule pays when one pass over A is long next to
+    the Gram + Cholesky it hides (d <= 128, dense, CountSketch, n d >= 2^24 on
+    this rank); IHS_LOOKAHEAD=0/1 overrides (the rule of ihs_solve_ols, api.cu)."""
+    import os
+    env = os.environ.get("IHS_LOOKAHEAD")
+    ok = isinstance(A, P.Dense) and 1 <= d <= 128
+    if env is not None:
+        return ok and env != "0"
+    return ok and spec.s == 1 and A.n * d >= (1 << 24)
+
+
 class ShardedIHS:
-    """One rank's view of the row-sharded IHS problem."""
+    """One rank's view of the row-sharded IHS problem.
+
+    OLS look-ahead (``lookahead``; DESIGN.md section 9): the sketch S^{t+1}
+    does not depend on x, so the pass over A that forms g^t also forms
+    S^{t+1} A, the all-reduce carries [S^{t+1} A | g^t], and H_{t+1}^{-1}
+    (Gram + Cholesky + inverse, ``ols_factor``) is computed on a side stream
+    during the NEXT pass; the step itself only applies x^{t+1} = x^t +
+    H_t^{-1} g^t (``ols_apply``).  Same iterates as the plain schedule (each
+    iteration still uses its own S^t), to rounding.  A step whose t does not
+    follow the previous one first sketches S^t A (the prologue)."""
 
     def __init__(self, A, b: torch.Tensor, spec: P.Spec, *, constraint: str = "ols", radius: float = 0.0,
-                 cfg=None, ops=None, allreduce=None, group=None):
+                 cfg=None, ops=None, allreduce=None, group=None, lookahead: bool | None = None):
         self.A = A
         self.b = b
         self.spec = spec
@@ -75,6 +109,10 @@ class ShardedIHS:
         self.group = group
         self.ops = ops if ops is not None else CudaOps(P.default_context(b.device))
         self.allreduce = allreduce if allreduce is not None else (lambda t: torch_allreduce(t, group))
+        world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        # one rank and the default exchange: nothing to all-reduce, so the
+        # look-ahead step can be the single fused call (ihs_ols_lookahead_step)
+        self._solo = allreduce is None and world == 1
         d, m = A.d, spec.m
         dev = b.device
         self.d, self.m = d, m
@@ -83,9 +121,45 @@ class ShardedIHS:
         self.g = self.pack[m * d:]
         self.H = torch.empty((d, d), dtype=torch.float64, device=dev)
         self.inner = torch.zeros(1, dtype=torch.int32, device=dev)
+        if lookahead is None:
+            lookahead = lookahead_default(A, d, spec)
+        self.lookahead = bool(lookahead) and constraint == "ols" and hasattr(self.ops, "ols_factor")
+        self._la_t = None  # iteration whose H^{-1} is in self.Hinv[self._la_cur]
+        if self.lookahead:
+            self.packs = torch.empty((2, m * d + d), dtype=torch.float64, device=dev)
+            self.Hinv = torch.empty((2, d, d), dtype=torch.float64, device=dev)
+            self._la_cur = 0
+
+    def prime(self, t: int) -> None:
+        """Look-ahead prologue: S^t A (all-reduced) and its H^{-1}, so that step(t) is one pass."""
+        if not self.lookahead or self._la_t == t:
+            return
+        m, d = self.m, self.d
+        pk = self.packs[0]
+        self.ops.sketch(self.A, self.spec, t, pk[: m * d].view(m, d))
+        self.allreduce(pk[: m * d])
+        self.ops.ols_factor(pk[: m * d].view(m, d), self.Hinv[0])
+        self._la_t, self._la_cur = t, 0
 
     def step(self, t: int, x: torch.Tensor, xn: torch.Tensor) -> torch.Tensor:
         """x^{t+1} from x^t: a1-a2+a5 (local), a3 (all-reduce), a4, a6 (replicated)."""
+        if self.lookahead:
+            self.prime(t)
+            m, d = self.m, self.d
+            cur, nxt = self._la_cur, 1 - self._la_cur
+            pk = self.packs[nxt]
+            SAn, gn = pk[: m * d].view(m, d), pk[m * d:]
+            if self._solo and hasattr(self.ops, "lookahead_step"):
+                self.ops.lookahead_step(self.A, self.spec, t + 1, self.b, x, self.Hinv[cur], SAn, self.Hinv[nxt], gn,
+                                        xn)
+                self._la_t, self._la_cur = t + 1, nxt
+                return xn
+            self.ops.sketch_grad(self.A, self.spec, t + 1, self.b, x, SAn, gn)  # S^{t+1} A and g^t
+            self.allreduce(pk)
+            self.ops.ols_factor(SAn, self.Hinv[nxt])  # beside the next pass (placed before its gather)
+            self.ops.ols_apply(self.Hinv[cur], gn, x, xn)
+            self._la_t, self._la_cur = t + 1, nxt
+            return xn
         self.ops.sketch_grad(self.A, self.spec, t, self.b, x, self.SA, self.g)
         self.allreduce(self.pack)
         if self.constraint == "ols" and hasattr(self.ops, "gram_ols"):  # a4 + a6 fused (one launch)

@@ -89,6 +89,12 @@ def main():
     xo, _ = oracle.ihs_solve(A, b, m=cfg.m, s=1, T=6)
     worst = max(oracle.pred_rel_err(a, c, A) for a, c in zip(out["x_hist"].cpu().numpy()[1:], xo[1:]))
     check("ihs solve C2 scaled", worst <= 1e-9, f"{worst:.2e}")
+    # short solves (look-ahead: T = 1 is the prologue + one gradient-only pass)
+    for T in (1, 2):
+        out = P.ihs_solve_ols(prob["A"].to(DEV), prob["b"].to(DEV), P.Spec(m=cfg.m), T, iter0=5)
+        xo, _ = oracle.ihs_solve(A, b, m=cfg.m, s=1, T=T, iter0=5)
+        worst = max(oracle.pred_rel_err(a, c, A) for a, c in zip(out["x_hist"].cpu().numpy()[1:], xo[1:]))
+        check(f"ihs solve C2 scaled T={T}", worst <= 1e-9, f"{worst:.2e}")
     print("ALL OK")
 
 

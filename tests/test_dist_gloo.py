@@ -49,6 +49,20 @@ class OracleOps:
                                                                  dtype=torch.float64)
 
 
+class OracleLookaheadOps(OracleOps):
+    """+ the look-ahead OLS calls (sketch only, H^{-1}, apply), test backend only."""
+
+    def sketch(self, A, spec, t, SA):
+        SA.copy_(torch.from_numpy(self.o.sketch_dense(A.A.numpy(), spec.seed, t, spec.m, spec.s,
+                                                      row_offset=A.row_offset)))
+
+    def ols_factor(self, SA, Hinv):
+        Hinv.copy_(torch.from_numpy(np.linalg.inv(self.o.gram(SA.numpy()))))
+
+    def ols_apply(self, Hinv, g, x, xn):
+        xn.copy_(x + Hinv @ g)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -72,8 +86,10 @@ def _worker(rank, world, port, case, out):
         r0, r1 = shard_rows(cfg.n, rank, world)
         A = P.Dense(prob["A"][r0:r1].contiguous(), row_offset=r0)
         b = prob["b"][r0:r1].contiguous()
-        S = ShardedIHS(A, b, P.Spec(m=case["m"], s=case["s"]), ops=OracleOps(), constraint=case["constraint"],
-                       radius=prob["tau"])
+        la = case.get("lookahead", False)
+        S = ShardedIHS(A, b, P.Spec(m=case["m"], s=case["s"]), ops=OracleLookaheadOps() if la else OracleOps(),
+                       constraint=case["constraint"], radius=prob["tau"], lookahead=la)
+        assert S.lookahead == la
         xh = S.solve(case["T"], iter0=case["iter0"])
         xopt = S.exact_ols() if case["constraint"] == "ols" else None
         errs = S.pred_errors(xh, xopt) if xopt is not None else None
@@ -105,6 +121,7 @@ def test_shard_rows_partition():
     {"cfg": "C1", "n": 2000, "m": 200, "s": 1, "T": 6, "iter0": 0, "constraint": "ols"},
     {"cfg": "C5", "n": 3001, "m": 256, "s": 8, "T": 4, "iter0": 7, "constraint": "ols"},
     {"cfg": "C4", "n": 4000, "m": 512, "s": 1, "T": 4, "iter0": 0, "constraint": "l1ball"},
+    {"cfg": "C2", "n": 5001, "m": 256, "s": 1, "T": 5, "iter0": 2, "constraint": "ols", "lookahead": True},
 ])
 def test_sharded_ihs_matches_unsharded_oracle(oracle_mod, case):
     import synthetic

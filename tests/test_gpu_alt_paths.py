@@ -18,6 +18,7 @@ SETS = {
                               "IHS_PG_WARM": "0", "IHS_PREFETCH": "0"},
     "tile_async_pgcta": {"IHS_SJLT": "tile", "IHS_GATHER": "async", "IHS_PG_CTA": "1", "IHS_FUSE": "1"},
     "pg_single": {"IHS_PG_SINGLE": "1"},
+    "lookahead": {"IHS_LOOKAHEAD": "1", "IHS_LOOKAHEAD_CLUSTER": "4"},
 }
 
 

@@ -54,9 +54,13 @@ def check_hash(P, oracle_mod, cfg, t, windows):
         np.testing.assert_array_equal(sg.cpu().numpy(), so)
 
 
-@pytest.mark.parametrize("name", ["C2", "C4", "C5", "C4P"])
+@pytest.mark.parametrize("name", ["C2", "C2-plain", "C4", "C5", "C4P"])
 def test_dense_full_size(P, oracle_mod, name):
+    """One step in the bench's launch configuration (C2: the look-ahead OLS
+    schedule by default; C2-plain and C5 (SJLT): the plain one)."""
     from paper_1910_14166_b200.dist import CudaOps, ShardedIHS
+    plain = name.endswith("-plain")
+    name = name.split("-")[0]
     cfg, prob = dense_full(name)
     n, d = cfg.n, cfg.d
     t = 3
@@ -64,15 +68,30 @@ def test_dense_full_size(P, oracle_mod, name):
     ctx = P.Context(0)
     spec = P.Spec(m=cfg.m, s=cfg.s)
     S = ShardedIHS(P.Dense(prob["A"]), prob["b"], spec, ops=CudaOps(ctx), constraint=cfg.constraint,
-                   radius=prob["lam"] if cfg.constraint == "lasso" else prob["tau"])
+                   radius=prob["lam"] if cfg.constraint == "lasso" else prob["tau"], lookahead=False if plain else None)
+    assert S.lookahead == (cfg.constraint == "ols" and cfg.s == 1 and not plain)
     rng = np.random.default_rng(0)
     x = torch.from_numpy(rng.standard_normal(d) * 0.1).to(DEV)
     xn = torch.empty_like(x)
     S.step(t, x, xn)  # the bench's launch configuration
     torch.cuda.synchronize()
     assert ctx.status() == P.OK
-    SA, g, H = S.SA.cpu().numpy(), S.g.cpu().numpy(), S.H.cpu().numpy()
     A = prob["A"].cpu().numpy()
+    m = cfg.m
+    if S.lookahead:  # prologue: S^t A in packs[0]; the step: [S^{t+1} A | g^t] in packs[1]
+        SA, g = S.packs[0][: m * d].view(m, d).cpu().numpy(), S.packs[1][m * d:].cpu().numpy()
+        SA1 = S.packs[1][: m * d].view(m, d).cpu().numpy()
+        H = oracle_mod.gram(SA)
+        Hinv = S.Hinv[0].cpu().numpy()
+        assert rel_fro(Hinv @ H, np.eye(d)) <= 1e-11
+        rows1 = np.array([0, m - 1, m // 3])
+        ref1 = oracle_mod.sketch_dense_rows(A, 0, t + 1, m, cfg.s, rows1)
+        if cfg.s == 1:
+            np.testing.assert_array_equal(SA1[rows1], ref1)
+        else:
+            assert rel_fro(SA1[rows1], ref1) <= 1e-12
+    else:
+        SA, g, H = S.SA.cpu().numpy(), S.g.cpu().numpy(), S.H.cpu().numpy()
     b = prob["b"].cpu().numpy()
     xh = x.cpu().numpy()
     # sampled SA rows, including the first/last bucket of a block

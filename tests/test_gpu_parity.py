@@ -208,6 +208,67 @@ def test_gram_ols_fused(P, oracle_mod, m, d):
     assert np.linalg.norm(u - uo) <= 1e-11 * np.linalg.norm(uo)
 
 
+@pytest.mark.parametrize("m,d", [(200, 10), (1024, 128), (4096, 96), (40, 5), (777, 100), (64, 1), (2048, 33),
+                                 (3000, 128)])
+def test_ols_factor_apply(P, oracle_mod, m, d):
+    """Look-ahead OLS: Hinv = (scale^2 SA^T SA)^{-1} on the factor stream, then
+    x + Hinv g, against the oracle's Gram and Cholesky step."""
+    rng = np.random.default_rng(3 * m + d)
+    SA = rng.standard_normal((m, d))
+    g = rng.standard_normal(d)
+    x = rng.standard_normal(d)
+    ctx = P.Context(0)
+    Hinv = P.ihs_ols_factor(torch.from_numpy(SA).to(DEV), scale=0.5, ctx=ctx)
+    xn = P.ihs_ols_apply(Hinv, torch.from_numpy(g).to(DEV), torch.from_numpy(x).to(DEV), ctx=ctx)
+    assert ctx.status() == P.OK
+    Ho = 0.25 * oracle_mod.gram(SA)
+    Hi = Hinv.cpu().numpy()
+    np.testing.assert_array_equal(Hi, Hi.T)
+    kappa = np.linalg.cond(Ho)
+    assert rel_fro(Hi @ Ho, np.eye(d)) <= 1e-14 * kappa * d
+    xo = oracle_mod.ols_step(Ho, g, x)
+    u, uo = xn.cpu().numpy() - x, xo - x
+    assert np.linalg.norm(u - uo) <= 1e-14 * kappa * d * np.linalg.norm(uo)
+
+
+def test_ols_factor_not_spd_and_unsupported(P):
+    ctx = P.Context(0)
+    SA = torch.zeros((4, 6), dtype=torch.float64, device=DEV)
+    SA[:4, :4] = torch.eye(4, dtype=torch.float64, device=DEV)  # rank 4 < d = 6
+    Hinv = P.ihs_ols_factor(SA, ctx=ctx)
+    x = torch.ones(6, dtype=torch.float64, device=DEV)
+    xn = P.ihs_ols_apply(Hinv, x, x, ctx=ctx)
+    assert ctx.status() == P.ERR_NOT_SPD
+    assert torch.equal(Hinv, torch.zeros_like(Hinv)) and torch.equal(xn, x)
+    with pytest.raises(P.IhsError):
+        P.ihs_ols_factor(torch.ones((300, 129), dtype=torch.float64, device=DEV), ctx=ctx)
+
+
+@pytest.mark.parametrize("solo", [True, False])
+@pytest.mark.parametrize("cfg_name,n,T,iter0", [("C2", 40_000, 6, 0), ("C1", 2000, 5, 3), ("C5", 30_001, 4, 2)])
+def test_sharded_lookahead_matches_oracle(P, oracle_mod, cfg_name, n, T, iter0, solo):
+    """The look-ahead schedule (S^{t+1} A formed in pass t, H^{-1} beside the
+    next pass) reproduces the oracle's iterates; a step whose t does not follow
+    the previous one re-runs the prologue.  solo: one fused call per step
+    (ihs_ols_lookahead_step); else sketch_grad / all-reduce hook / factor / apply."""
+    from paper_1910_14166_b200.dist import CudaOps, ShardedIHS
+    cfg, A, b, prob = dense_case(cfg_name, n)
+    ctx = P.Context(0)
+    S = ShardedIHS(P.Dense(prob["A"].to(DEV)), prob["b"].to(DEV), P.Spec(m=cfg.m, s=cfg.s), ops=CudaOps(ctx),
+                   lookahead=True, allreduce=None if solo else (lambda t: None))
+    assert S.lookahead and S._solo == solo
+    xh = S.solve(T, iter0=iter0).cpu().numpy()
+    xo, _ = oracle_mod.ihs_solve(A, b, m=cfg.m, s=cfg.s, T=T, iter0=iter0)
+    for t in range(1, T + 1):
+        assert oracle_mod.pred_rel_err(xh[t], xo[t], A) <= 1e-9, t
+    # out-of-order step: iteration iter0 + 2 from x^2 again
+    x2 = torch.from_numpy(xo[2]).to(DEV)
+    xn = torch.empty_like(x2)
+    S.step(iter0 + 2, x2, xn)
+    assert oracle_mod.pred_rel_err(xn.cpu().numpy(), xo[3], A) <= 1e-9
+    assert ctx.status() == P.OK
+
+
 def test_ols_update_not_spd(P):
     ctx = P.Context(0)
     H = torch.diag(torch.tensor([1.0, -1.0, 2.0], dtype=torch.float64, device=DEV))
