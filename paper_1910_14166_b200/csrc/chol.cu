@@ -140,48 +140,111 @@ __device__ __forceinline__ void chol_blocked_body(double *Ls, double *rdiag, dou
   }
 }
 
-// H^{-1} = L^{-T} L^{-1} from the factor in Ls / rdiag (for the look-ahead
-// OLS step, api.cu): Y = L^{-1} by forward substitution on all D right-hand
-// sides at once (row i of Y from rows < i; thread c owns column c, the L row is
-// a shared-memory broadcast), Y packed by rows in Yp (Y[i][c] at i(i+1)/2 + c),
-// then Hinv = Y^T Y (thread per entry, i fastest so the Y loads are contiguous).
-// The identity padding rows (>= d) of L give Y[k][c] = 0 for k >= d > c.
+// H^{-1} = L^{-T} L^{-1} from the factor in Ls / rdiag (the look-ahead OLS
+// factor, api.cu), with Y = L^{-1} kept TRANSPOSED in the unused upper
+// triangle of Ls (Ls[a][b] = Y[b][a] for a < b; Y's diagonal is rdiag), so no
+// extra shared memory beyond one 32 x 36 buffer per column block:
+//   A. warp I inverts the diagonal block L_II (lane c owns column c of Y_II in
+//      registers; the L row is a broadcast; 32 x 32 fully unrolled);
+//   B. row blocks I = 1.. in order: T_IJ = sum_{K=J}^{I-1} L_IK Y_KJ, then
+//      Y_IJ = -Y_II T_IJ (DMMA m8n8k4 f64, 8x8 tiles over the 8 warps);
+//   C. Hinv = Y^T Y, lower 8x8 tiles on DMMA, both halves written to global.
+// Both operands of every DMMA are rows of Ls at leading dimension D + 4, the
+// conflict-free fragment pattern of the factorisation.  (A thread-per-column
+// forward substitution on packed rows took ~200 us at d = 128; this ~10 us.)
 template <int NBLK>
-__device__ __forceinline__ void chol_inverse_body(const double *Ls, const double *rdiag, double *Yp, int d,
+__device__ __forceinline__ double yT(const double *Ls, const double *rdiag, int a, int b) {
+  constexpr int lda = 32 * NBLK + 4;  // Y[b][a]: upper storage, diagonal in rdiag, zero above
+  return b > a ? Ls[a * lda + b] : (b == a ? rdiag[a] : 0.0);
+}
+
+template <int NBLK>
+__device__ __forceinline__ void chol_inverse_body(double *Ls, const double *rdiag, double *Tt, int d,
                                                   double *__restrict__ Hinv) {
   constexpr int D = 32 * NBLK;
   constexpr int lda = D + 4;
-  const int tid = threadIdx.x;
+  constexpr int ldt = 36;  // Tt: per J, 32 x ldt (T transposed)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // A. diagonal blocks
+  if (warp < NBLK) {
+    const int I0 = 32 * warp, c = lane;
+    double y[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) s = fma(-Ls[(I0 + i) * lda + I0 + k], y[k], s);
+      y[i] = s * rdiag[I0 + i];
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i > c) Ls[(I0 + c) * lda + I0 + i] = y[i];
+  }
+  __syncthreads();
+  const int r4 = lane >> 2, k4 = lane & 3;
+  // B. off-diagonal blocks, row block by row block
 #pragma unroll 1
-  for (int i = 0; i < d; ++i) {
-    const double *Li = Ls + i * lda;
-    for (int c = tid; c <= i; c += kBThreads) {
-      double s0 = (c == i) ? 1.0 : 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int k = c;
-      for (; k + 3 < i; k += 4) {
-        s0 -= Li[k] * Yp[k * (k + 1) / 2 + c];
-        s1 -= Li[k + 1] * Yp[(k + 1) * (k + 2) / 2 + c];
-        s2 -= Li[k + 2] * Yp[(k + 2) * (k + 3) / 2 + c];
-        s3 -= Li[k + 3] * Yp[(k + 3) * (k + 4) / 2 + c];
+  for (int I = 1; I < NBLK; ++I) {
+    // T_IJ (J < I): 16 tiles each
+    for (int t = warp; t < 16 * I; t += kBThreads / 32) {
+      const int J = t >> 4, ti = (t >> 2) & 3, tn = t & 3;
+      const int R = 32 * I + 8 * ti, N = 32 * J + 8 * tn;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k0 = 32 * J; k0 < 32 * I; k0 += 4) {
+        const double a = Ls[(R + r4) * lda + k0 + k4];            // L[R + r][k]
+        const double b = yT<NBLK>(Ls, rdiag, N + r4, k0 + k4);     // Y[k][N + n]
+        dmma884(c0, c1, a, b);
       }
-      for (; k < i; ++k) s0 -= Li[k] * Yp[k * (k + 1) / 2 + c];
-      Yp[i * (i + 1) / 2 + c] = ((s0 + s1) + (s2 + s3)) * rdiag[i];
+      double *T = Tt + J * 32 * ldt;  // T[r][n] stored at Tt[n][r]
+      const int r = 8 * ti + r4, n = 8 * tn + 2 * k4;
+      T[n * ldt + r] = c0;
+      T[(n + 1) * ldt + r] = c1;
+    }
+    __syncthreads();
+    // Y_IJ = -Y_II T_IJ, stored transposed into Ls[32J + n][32I + r]
+    for (int t = warp; t < 16 * I; t += kBThreads / 32) {
+      const int J = t >> 4, ti = (t >> 2) & 3, tn = t & 3;
+      const double *T = Tt + J * 32 * ldt;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < 32; k0 += 4) {
+        const double a = yT<NBLK>(Ls, rdiag, 32 * I + k0 + k4, 32 * I + 8 * ti + r4);  // Y_II[r][k]
+        const double b = T[(8 * tn + r4) * ldt + k0 + k4];                           // T[k][n]
+        dmma884(c0, c1, a, b);
+      }
+      const int r = 32 * I + 8 * ti + r4, n = 32 * J + 8 * tn + 2 * k4;
+      Ls[n * lda + r] = -c0;
+      Ls[(n + 1) * lda + r] = -c1;
     }
     __syncthreads();
   }
-  for (int e = tid; e < d * d; e += kBThreads) {
-    const int i = e % d, j = e / d;
-    if (i < j) continue;
-    double s0 = 0.0, s1 = 0.0;
-    int k = i;
-    for (; k + 1 < d; k += 2) {
-      s0 += Yp[k * (k + 1) / 2 + i] * Yp[k * (k + 1) / 2 + j];
-      s1 += Yp[(k + 1) * (k + 2) / 2 + i] * Yp[(k + 1) * (k + 2) / 2 + j];
+  // C. Hinv[p][q] = sum_{k >= p} Y[k][p] Y[k][q], lower 8x8 tiles (tp >= tq)
+  constexpr int NT8 = D / 8;
+  for (int t = warp; t < NT8 * (NT8 + 1) / 2; t += kBThreads / 32) {
+    int tp = 0, rem = t;
+    while (rem > tp) {
+      rem -= tp + 1;
+      ++tp;
     }
-    if (k < d) s0 += Yp[k * (k + 1) / 2 + i] * Yp[k * (k + 1) / 2 + j];
-    const double v = s0 + s1;
-    Hinv[(int64_t)j * d + i] = v;
-    Hinv[(int64_t)i * d + j] = v;
+    const int tq = rem, P0 = 8 * tp, Q0 = 8 * tq;
+    if (P0 >= d) continue;
+    double c0 = 0.0, c1 = 0.0;
+    for (int k0 = P0; k0 < D; k0 += 4) {
+      const double a = yT<NBLK>(Ls, rdiag, P0 + r4, k0 + k4);  // Y[k][p]
+      const double b = yT<NBLK>(Ls, rdiag, Q0 + r4, k0 + k4);  // Y[k][q]
+      dmma884(c0, c1, a, b);
+    }
+    const int p = P0 + r4, q = Q0 + 2 * k4;
+    if (p < d) {
+      if (q < d) {
+        Hinv[(int64_t)p * d + q] = c0;
+        Hinv[(int64_t)q * d + p] = c0;
+      }
+      if (q + 1 < d) {
+        Hinv[(int64_t)p * d + q + 1] = c1;
+        Hinv[(int64_t)(q + 1) * d + p] = c1;
+      }
+    }
   }
 }
 
@@ -200,13 +263,24 @@ __global__ void __launch_bounds__(kBThreads) chol_blocked_kernel(const double *_
   __shared__ int s_bad;
   __shared__ double colbuf[64];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = warp; i < DA; i += kBThreads / 32) {
-    if (i < D) {
-      for (int c = lane; c <= i; c += 32) Ls[i * lda + c] = (i < d) ? H[(int64_t)i * d + c] : (c == i ? 1.0 : 0.0);
-    } else {
-      for (int c = lane; c < D; c += 32) Ls[i * lda + c] = (i == D && c < d) ? g[c] : 0.0;
+  // lower triangle of H (identity padding), 16 loads in flight per thread
+  constexpr int PER = D * D / kBThreads;
+#pragma unroll 1
+  for (int k0 = 0; k0 < PER; k0 += 16) {
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int e = tid + (k0 + k) * kBThreads, i = e / D, c = e % D;
+      v[k] = (k0 + k < PER && c <= i) ? ((i < d) ? H[(int64_t)i * d + c] : (c == i ? 1.0 : 0.0)) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int e = tid + (k0 + k) * kBThreads, i = e / D, c = e % D;
+      if (k0 + k < PER && c <= i) Ls[i * lda + c] = v[k];
     }
   }
+  for (int i = D + warp; i < DA; i += kBThreads / 32)
+    for (int c = lane; c < D; c += 32) Ls[i * lda + c] = (i == D && c < d) ? g[c] : 0.0;
   chol_blocked_body<NBLK>(Ls, rdiag, colbuf, s_bad, d, x, x_next, status);
 }
 
@@ -264,9 +338,20 @@ __global__ void __launch_bounds__(kBThreads, 1) gram_ols_kernel(const double *__
     for (int64_t rb = r0; rb < r1; rb += kGoRows) {
       const int rows = (int)min((int64_t)kGoRows, r1 - rb);
       __syncthreads();  // the previous chunk's fragments are consumed
-      for (int e = tid; e < kGoRows * D; e += kBThreads) {
-        const int r = e / D, c = e % D;
-        S[r * lds + c] = (r < rows && c < d) ? SA[(rb + r) * d + c] : 0.0;
+      // all loads of the chunk in flight before the stores (a runtime-bounded
+      // loop issued one L2 round trip at a time: the factor took 0.35 ms
+      // beside a gather)
+      constexpr int PER = kGoRows * D / kBThreads;
+      double v[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * kBThreads, r = e / D, c = e % D;
+        v[k] = (r < rows && c < d) ? SA[(rb + r) * d + c] : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int e = tid + k * kBThreads;
+        S[(e / D) * lds + e % D] = v[k];
       }
       __syncthreads();
 #pragma unroll
@@ -311,11 +396,19 @@ __global__ void __launch_bounds__(kBThreads, 1) gram_ols_kernel(const double *__
     // reduce a slice of the lower triangle over the partials (CTA order) into CTA 0
     double *Ls0 = cluster.map_shared_rank(sm, 0);
     const int nw = cs - 1;
+    const double *parts[15];
+#pragma unroll
+    for (int r = 1; r < 16; ++r) parts[r - 1] = cluster.map_shared_rank(sm + kGoRows * lds, r < cs ? r : 1);
     for (int e = (rank - 1) * kBThreads + tid; e < D * D; e += nw * kBThreads) {
       const int i = e / D, j = e % D;
       if (j > i || i >= d) continue;
+      double u[15];  // the cs - 1 DSMEM loads in flight, then added in CTA order
+#pragma unroll
+      for (int r = 1; r < 16; ++r) u[r - 1] = (r < cs) ? parts[r - 1][e] : 0.0;
       double v = 0.0;
-      for (int r = 1; r < cs; ++r) v += cluster.map_shared_rank(sm + kGoRows * lds, r)[e];
+#pragma unroll
+      for (int r = 1; r < 16; ++r)
+        if (r < cs) v += u[r - 1];
       v *= scale2;
       Ls0[i * lda + j] = v;
       if (H_out) {
@@ -343,7 +436,7 @@ cudaError_t launch_gram_ols_t(const double *SA, int64_t m, int d, double scale, 
                               double *x_next, double *H_out, int *status, double *Hinv, int max_cluster,
                               cudaStream_t st) {
   constexpr int D = 32 * NBLK;
-  const size_t smem_chol = ((size_t)(D + 8) * (D + 4) + D + (INV ? (size_t)D * (D + 1) / 2 : 0)) * 8;
+  const size_t smem_chol = ((size_t)(D + 8) * (D + 4) + D + (INV ? (size_t)NBLK * 32 * 36 : 0)) * 8;
   const size_t smem_gram = ((size_t)kGoRows * (D + 4) + (size_t)D * D) * 8;
   const size_t smem = std::max(smem_chol, smem_gram);
   auto kern = gram_ols_kernel<NBLK, INV>;

@@ -131,4 +131,23 @@ constexpr size_t kExclusiveSmem = 200 * 1024;
     }                                                                                                \
   } while (0)
 
+// Copy cnt contiguous doubles global -> shared with 16 loads in flight per
+// thread (a runtime-bounded copy loop issues one L2 round trip at a time).
+__device__ __forceinline__ void load_rows(double *dst, const double *__restrict__ src, int64_t cnt, int tid,
+                                          int nthreads) {
+  for (int64_t e0 = tid; e0 < cnt; e0 += 16 * (int64_t)nthreads) {
+    double v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int64_t e = e0 + (int64_t)k * nthreads;
+      v[k] = e < cnt ? src[e] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int64_t e = e0 + (int64_t)k * nthreads;
+      if (e < cnt) dst[e] = v[k];
+    }
+  }
+}
+
 }  // namespace ihs

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kCgThreads) ols_cg_kernel(const double *__rest
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = blockIdx.x * rows_per, i1 = min(d, i0 + rows_per);
   if (smem_rows)
-    for (int e = tid; e < (i1 - i0) * d; e += kCgThreads) Hs[e] = H[(int64_t)i0 * d + e];
+    load_rows(Hs, H + (int64_t)i0 * d, (int64_t)(i1 - i0) * d, tid, kCgThreads);
   // full-length vectors, element c = tid + kCgThreads * k, in registers
   double u[kCgMaxPer], r[kCgMaxPer], z[kCgMaxPer], p[kCgMaxPer], dinv[kCgMaxPer];
   double rz = 0.0, gg = 0.0;

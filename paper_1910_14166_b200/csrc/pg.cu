@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(kCT) pg_cluster_kernel(const double *__restric
   double *zb = w + d;                // 2 x d : z (or H v), double-buffered by step parity
   __shared__ double red[2 * kCW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t e = tid; e < (int64_t)(r1 - r0) * d; e += kCT) Hs[e] = H[(int64_t)r0 * d + e];
+  load_rows(Hs, H + (int64_t)r0 * d, (int64_t)(r1 - r0) * d, tid, kCT);
   for (int i = tid; i < d; i += kCT) {
     xs[i] = x[i];
     gs[i] = g[i];
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
   double *gs = Hs + (size_t)R * d;   // R (my rows of g)
   double *zb = gs + R;               // 2 x d : z (or H v), double-buffered by step parity
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int64_t e = tid; e < (int64_t)(r1 - r0) * d; e += kCT) Hs[e] = H[(int64_t)r0 * d + e];
+  load_rows(Hs, H + (int64_t)r0 * d, (int64_t)(r1 - r0) * d, tid, kCT);
   for (int i = tid; i < r1 - r0; i += kCT) gs[i] = g[r0 + i];
   double xv[K], yv[K], vv[K], wv[K];
 #pragma unroll
