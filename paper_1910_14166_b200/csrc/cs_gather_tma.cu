@@ -13,13 +13,17 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+#include <type_traits>
+
 namespace ihs {
 
 namespace {
 constexpr int kScanTile = 4096;
 constexpr int kMaxStages = 8;
 constexpr int kRingBytes = 24 * 1024;  // bytes in flight per CTA (~168 KiB per SM at 7 CTAs)
-constexpr int kRows = 4;  // rows per stage
+constexpr int kDefaultRows = 4;  // rows per stage
+constexpr int kDefaultCW = 2;    // consumer warps
 
 __device__ __forceinline__ int32_t scanned_at(const int32_t *hist, const int32_t *tile_sums, int64_t e) {
   return hist[e] + tile_sums[e / kScanTile];
@@ -61,14 +65,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 // thread forms the same residual r_i = b_i - (p0 + p1).  Warp 2 produces: it
 // holds the perm entries and b values a window ahead, waits until the slot
 // is released (one arrival per consumer warp) and issues one bulk copy per row.
-constexpr int kConsumers = 64;
-constexpr int kCW = kConsumers / 32;
-template <bool FUSE, int NC, bool SOLO>
-__global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tma_kernel(
+template <bool FUSE, int NC, bool SOLO, int CW, int KR>
+__global__ void __launch_bounds__(32 * CW + 32, NC * KR * CW >= 32 ? 6 : 7) cs_gather_tma_kernel(
     const double *__restrict__ A, int64_t n, int d, int m, const int32_t *__restrict__ hist,
     const int32_t *__restrict__ tile_sums, int64_t nchunks, const uint32_t *__restrict__ perm,
     const double *__restrict__ bvec, const double *__restrict__ x, double *__restrict__ SA,
     double *__restrict__ gpart, double scale, int kStages, GatherBatchStrides bst) {
+  constexpr int KC = 32 * CW;  // consumer threads
   extern __shared__ __align__(128) unsigned char smem_raw[];
   // blockIdx.y selects one SJLT block of a batch (its own sort and SA rows);
   // the gradient rides on batch entry 0 only
@@ -77,12 +80,12 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
   perm += blockIdx.y * bst.perm;
   SA += blockIdx.y * bst.sa;
   const bool fz = FUSE && (SOLO || blockIdx.y == 0);  // SOLO: a one-entry batch (compile-time)
-  double *ring = reinterpret_cast<double *>(smem_raw);                                // [kStages][kRows][d]
-  double *bs = ring + (size_t)kStages * kRows * d;                                    // [kStages][kRows]
-  double *pd = bs + kStages * kRows;                                                  // [kStages][kCW][kRows]
-  uint64_t *full = reinterpret_cast<uint64_t *>(pd + kStages * kCW * kRows);          // [kStages]
+  double *ring = reinterpret_cast<double *>(smem_raw);                                // [kStages][KR][d]
+  double *bs = ring + (size_t)kStages * KR * d;                                    // [kStages][KR]
+  double *pd = bs + kStages * KR;                                                  // [kStages][CW][KR]
+  uint64_t *full = reinterpret_cast<uint64_t *>(pd + kStages * CW * KR);          // [kStages]
   uint64_t *empty = full + kMaxStages;                                                // [kStages]
-  uint32_t *rid = reinterpret_cast<uint32_t *>(empty + kMaxStages);                   // [kStages][kRows]
+  double *sgn = reinterpret_cast<double *>(empty + kMaxStages);                       // [kStages][KR] +-1
   const int b = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int64_t beg = scanned_at(hist, tile_sums, (int64_t)b * nchunks);
@@ -97,26 +100,26 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
     if (gpart) gpart += z * (int64_t)m * d;
   }
   const int64_t len = end - beg;
-  const int64_t nb = (len + kRows - 1) / kRows;
+  const int64_t nb = (len + KR - 1) / KR;
   const uint32_t row_bytes = (uint32_t)d * 8u;
 
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kCW);
+      mbar_init(&empty[s], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (warp == kCW) {
+  if (warp == CW) {
     // ---------------- producer warp
     // The bucket's perm entries (and, fused, the b values they index) are
     // loaded a 32-row window at a time, one entry per lane, two windows ahead
     // for perm and one ahead for b (whose address depends on perm): neither
-    // dependent load sits on the per-stage path.  Each stage takes its kRows
+    // dependent load sits on the per-stage path.  Each stage takes its KR
     // entries from the current window by shuffle.
-    constexpr int kWinStages = 32 / kRows;
+    constexpr int kWinStages = 32 / KR;
     const int64_t nwin = (len + 31) / 32;
     auto perm_win = [&](int64_t w) -> uint32_t {
       const int64_t i = w * 32 + lane;
@@ -136,14 +139,14 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
       for (int ks = 0; ks < kWinStages; ++ks) {
         const int64_t k = w * kWinStages + ks;
         if (k >= nb) break;
-        const int cnt = (int)min((int64_t)kRows, len - k * kRows);
-        const int src = ks * kRows + (lane & (kRows - 1));
+        const int cnt = (int)min((int64_t)KR, len - k * KR);
+        const int src = ks * KR + (lane & (KR - 1));
         const uint32_t e = __shfl_sync(0xffffffffu, p_cur, src);
         const double bv = fz ? __shfl_sync(0xffffffffu, b_cur, src) : 0.0;
         if (k >= kStages) mbar_wait(&empty[s], ph ^ 1u);
         if (lane < cnt) {
-          rid[s * kRows + lane] = e;
-          if (fz) bs[s * kRows + lane] = bv;
+          sgn[s * KR + lane] = (e >> 31) ? -1.0 : 1.0;
+          if (fz) bs[s * KR + lane] = bv;
         }
         __syncwarp();
         if (lane == 0) {
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
         }
         __syncwarp();
         if (lane < cnt)
-          bulk_g2s(ring + ((size_t)s * kRows + lane) * d, A + (int64_t)(e & 0x7fffffffu) * d, row_bytes, &full[s]);
+          bulk_g2s(ring + ((size_t)s * KR + lane) * d, A + (int64_t)(e & 0x7fffffffu) * d, row_bytes, &full[s]);
         if (++s == kStages) {
           s = 0;
           ph ^= 1u;
@@ -170,86 +173,108 @@ __global__ void __launch_bounds__(kConsumers + 32, NC >= 4 ? 6 : 7) cs_gather_tm
   double acc[NC], gac[NC], xv[NC];
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    const int c = tid + kConsumers * q;
+    const int c = tid + KC * q;
     cv[q] = c < d;
     cc[q] = cv[q] ? c : d - 1;
     acc[q] = 0.0;
     gac[q] = 0.0;
     xv[q] = (fz && cv[q]) ? x[c] : 0.0;
   }
-  const int myu = reduced_row_of_lane<kRows>(lane);
-  const bool owner = owner_lane_of_row<kRows>(myu) == lane;
+  const int myu = reduced_row_of_lane<KR>(lane);
+  const bool owner = owner_lane_of_row<KR>(myu) == lane;
+  // loop-invariant shared-memory offsets of this thread's columns in a stage
+  int off[KR][NC];
+#pragma unroll
+  for (int r = 0; r < KR; ++r)
+#pragma unroll
+    for (int q = 0; q < NC; ++q) off[r][q] = r * d + cc[q];
   int s = 0;
   uint32_t ph = 0;
-  for (int64_t k = 0; k < nb; ++k, s = (s + 1 == kStages) ? 0 : s + 1, ph ^= (s == 0) ? 1u : 0u) {
-    const int cnt = (int)min((int64_t)kRows, len - k * kRows);
-    mbar_wait(&full[s], ph);
-    const double *st = ring + (size_t)s * kRows * d;
-    double a[kRows][NC];
+  // One stage.  FULL (every stage but a bucket's last): no row predicates, so
+  // the stage is straight-line code.  The sign is applied as fma(+-1, a, acc),
+  // which rounds exactly like acc + (+-a): the ascending-row sum is unchanged.
+  auto stage = [&](auto full_tag, int cnt) {
+    constexpr bool FULL = decltype(full_tag)::value;
+    const double *st = ring + (size_t)s * KR * d;
+    double a[KR][NC];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      const int rr = r < cnt ? r : 0;  // rows past the end were not copied: read row 0
+    for (int r = 0; r < KR; ++r)
 #pragma unroll
-      for (int q = 0; q < NC; ++q) a[r][q] = st[(size_t)rr * d + cc[q]];
-    }
-    double res[kRows];
+      for (int q = 0; q < NC; ++q) a[r][q] = (FULL || r < cnt) ? st[off[r][q]] : 0.0;
+    double res[KR];
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) res[r] = 0.0;
+    for (int r = 0; r < KR; ++r) res[r] = 0.0;
     if (fz) {
-      double p[kRows];
+      double p[KR];
 #pragma unroll
-      for (int r = 0; r < kRows; ++r) {
+      for (int r = 0; r < KR; ++r) {
         p[r] = a[r][0] * xv[0];
 #pragma unroll
         for (int q = 1; q < NC; ++q) p[r] = fma(a[r][q], xv[q], p[r]);
       }
-      transpose_reduce<kRows>(p, lane);
-      if (owner) pd[(s * kCW + warp) * kRows + myu] = p[0];
-      asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory");
+      transpose_reduce<KR>(p, lane);
+      if (owner) pd[(s * CW + warp) * KR + myu] = p[0];
+      if constexpr (CW > 1) {
+        asm volatile("bar.sync 1, %0;" ::"n"(KC) : "memory");
+      } else {
+        __syncwarp();
+      }
 #pragma unroll
-      for (int r = 0; r < kRows; ++r) {
-        double dot = pd[(s * kCW + 0) * kRows + r];
+      for (int r = 0; r < KR; ++r) {
+        double dot = pd[(s * CW + 0) * KR + r];
 #pragma unroll
-        for (int w = 1; w < kCW; ++w) dot += pd[(s * kCW + w) * kRows + r];
-        res[r] = (r < cnt) ? bs[s * kRows + r] - dot : 0.0;
+        for (int w = 1; w < CW; ++w) dot += pd[(s * CW + w) * KR + r];
+        res[r] = (FULL || r < cnt) ? bs[s * KR + r] - dot : 0.0;
       }
     }
 #pragma unroll
-    for (int r = 0; r < kRows; ++r) {
-      if (r < cnt) {
-        const bool neg = (rid[s * kRows + r] >> 31) != 0;
+    for (int r = 0; r < KR; ++r) {
+      if (FULL || r < cnt) {
+        const double sg = sgn[s * KR + r];
 #pragma unroll
         for (int q = 0; q < NC; ++q) {
-          acc[q] += neg ? -a[r][q] : a[r][q];
+          acc[q] = fma(sg, a[r][q], acc[q]);
           if (fz) gac[q] = fma(res[r], a[r][q], gac[q]);
         }
       }
     }
+  };
+  const int64_t nfull = len / KR;
+  for (int64_t k = 0; k < nb; ++k) {
+    mbar_wait(&full[s], ph);
+    if (k < nfull)
+      stage(std::true_type{}, KR);
+    else
+      stage(std::false_type{}, (int)(len - k * KR));
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == kStages) {
+      s = 0;
+      ph ^= 1u;
+    }
   }
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     if (cv[q]) {
-      SA[(int64_t)b * d + tid + kConsumers * q] = scale == 1.0 ? acc[q] : acc[q] * scale;
-      if (fz) gpart[(int64_t)b * d + tid + kConsumers * q] = gac[q];
+      SA[(int64_t)b * d + tid + KC * q] = scale == 1.0 ? acc[q] : acc[q] * scale;
+      if (fz) gpart[(int64_t)b * d + tid + KC * q] = gac[q];
     }
   }
 }
 
-template <bool FUSE, int NC>
+template <bool FUSE, int NC, int CW, int KR>
 void launch_tma_t(size_t smem, int nst, int nb, GatherBatchStrides bst, const double *A, int64_t n, int d, int m,
                   const int32_t *hist, const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm,
                   const double *bvec, const double *x, double *SA, double *gpart, double scale, cudaStream_t st) {
   if (nb == 1) {
-    IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC, true>), smem);
-    cs_gather_tma_kernel<FUSE, NC, true><<<dim3((unsigned)m, 1, (unsigned)bst.nseg), kConsumers + 32, smem, st>>>(
+    IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC, true, CW, KR>), smem);
+    cs_gather_tma_kernel<FUSE, NC, true, CW, KR><<<dim3((unsigned)m, 1, (unsigned)bst.nseg), 32 * CW + 32, smem, st>>>(
         A, n, d, m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, nst, bst);
   } else {
-    IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC, false>), smem);
-    cs_gather_tma_kernel<FUSE, NC, false><<<dim3((unsigned)m, (unsigned)nb, (unsigned)bst.nseg), kConsumers + 32, smem,
-                                            st>>>(
-        A, n, d, m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, nst, bst);
+    IHS_SMEM_ATTR((cs_gather_tma_kernel<FUSE, NC, false, CW, KR>), smem);
+    cs_gather_tma_kernel<FUSE, NC, false, CW, KR>
+        <<<dim3((unsigned)m, (unsigned)nb, (unsigned)bst.nseg), 32 * CW + 32, smem, st>>>(
+            A, n, d, m, hist, tile_sums, nchunks, perm, bvec, x, SA, gpart, scale, nst, bst);
   }
 }
 }  // namespace
@@ -262,20 +287,42 @@ cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t 
                                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
                                  const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
                                  LaunchCounter lc, int nbatch, GatherBatchStrides bst) {
-  // ring depth: ~kRingBytes of rows in flight per CTA, 2..kMaxStages stages
-  const int nst = (int)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, kRingBytes / (kRows * d * 8)));
-  const size_t smem = (size_t)nst * kRows * d * 8 + (size_t)nst * kRows * 8 * (1 + kCW) + 2 * kMaxStages * 8 +
-                      kMaxStages * kRows * 4 + 64;
-  const int nc = (int)((d + kConsumers - 1) / kConsumers);
+  // consumer warps (CW) and rows per stage (KR): IHS_GATHER_CW=1|2,
+  // IHS_GATHER_ROWS=4|8 (defaults measured on B200)
+  static const int cw_env = getenv("IHS_GATHER_CW") ? atoi(getenv("IHS_GATHER_CW")) : 0;
+  static const int kr_env = getenv("IHS_GATHER_ROWS") ? atoi(getenv("IHS_GATHER_ROWS")) : 0;
   const bool f = gpart != nullptr;
-#define IHS_TMA(NC)                                                                                               \
-  (f ? launch_tma_t<true, NC>(smem, nst, nbatch, bst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, bvec, \
-                              x, SA, gpart, scale, st)                                                           \
-     : launch_tma_t<false, NC>(smem, nst, nbatch, bst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm,      \
-                               nullptr, nullptr, SA, nullptr, scale, st))
-  if (nc <= 1) IHS_TMA(1);
-  else if (nc == 2) IHS_TMA(2);
-  else IHS_TMA(4);
+  const int CWv = cw_env == 1 || cw_env == 2 ? cw_env : kDefaultCW;
+  const int KRv = kr_env == 4 || kr_env == 8 ? kr_env : kDefaultRows;
+  // ring depth: ~kRingBytes of rows in flight per CTA, 2..kMaxStages stages
+  const int nst = (int)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, kRingBytes / (KRv * d * 8)));
+  const size_t smem = (size_t)nst * KRv * d * 8 + (size_t)nst * KRv * 8 * (1 + CWv) + 2 * kMaxStages * 8 +
+                      kMaxStages * KRv * 8 + 64;
+  const int nc = (int)((d + 32 * CWv - 1) / (32 * CWv));
+#define IHS_TMA(NC, CW, KR)                                                                                        \
+  (f ? launch_tma_t<true, NC, CW, KR>(smem, nst, nbatch, bst, A, n, (int)d, (int)m, hist, tile_sums, nchunks, perm, \
+                                      bvec, x, SA, gpart, scale, st)                                               \
+     : launch_tma_t<false, NC, CW, KR>(smem, nst, nbatch, bst, A, n, (int)d, (int)m, hist, tile_sums, nchunks,     \
+                                       perm, nullptr, nullptr, SA, nullptr, scale, st))
+#define IHS_TMA_NC(CW, KR)   \
+  if (nc <= 1)               \
+    IHS_TMA(1, CW, KR);      \
+  else if (nc == 2)          \
+    IHS_TMA(2, CW, KR);      \
+  else if (nc <= 4)          \
+    IHS_TMA(4, CW, KR);      \
+  else                       \
+    IHS_TMA(8, CW, KR);
+  if (CWv == 2 && KRv == 4) {
+    IHS_TMA_NC(2, 4)
+  } else if (CWv == 2) {
+    IHS_TMA_NC(2, 8)
+  } else if (KRv == 4) {
+    IHS_TMA_NC(1, 4)
+  } else {
+    IHS_TMA_NC(1, 8)
+  }
+#undef IHS_TMA_NC
 #undef IHS_TMA
   lc.add();
   return cudaGetLastError();

@@ -45,6 +45,8 @@ if has ncu; then
   $B --config C2 > $OUT/plain1_C2.log 2>&1 &&
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cs_gather_tma -s 3 -c 1 \
     -o $OUT/full_C2 -f $B --config C2 > $OUT/ncu_full_C2.log 2>&1
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"gram_ols|reduce_rows_last" -s 6 -c 2 \
+    -o $OUT/full_C2_factor -f $B --config C2 > $OUT/ncu_full_C2_factor.log 2>&1
   $B --config C3 > $OUT/plain1_C3.log 2>&1 &&
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"gram_streamk|csr_sketch|ols_cg" -s 9 -c 3 \
     -o $OUT/full_C3 -f $B --config C3 > $OUT/ncu_full_C3.log 2>&1
