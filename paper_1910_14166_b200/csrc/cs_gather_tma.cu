@@ -53,6 +53,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// The same copy with an L2 eviction-priority hint (evict_first for A: the
+// stream does not push the sort arrays and b out of L2).
+__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -128,6 +139,8 @@ __global__ void __launch_bounds__(32 * CW + 32, NC * KR * CW >= 32 ? 6 : 7) cs_g
     auto b_win = [&](int64_t w, uint32_t e) -> double {
       return (fz && w < nwin && w * 32 + lane < len) ? bvec[e & 0x7fffffffu] : 0.0;
     };
+    uint64_t pol = 0;
+    if (bst.hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     uint32_t p_cur = perm_win(0), p_next = perm_win(1);
     int s = 0;
     uint32_t ph = 0;
@@ -154,8 +167,13 @@ __global__ void __launch_bounds__(32 * CW + 32, NC * KR * CW >= 32 ? 6 : 7) cs_g
           mbar_expect_tx(&full[s], (uint32_t)cnt * row_bytes);
         }
         __syncwarp();
-        if (lane < cnt)
-          bulk_g2s(ring + ((size_t)s * KR + lane) * d, A + (int64_t)(e & 0x7fffffffu) * d, row_bytes, &full[s]);
+        if (lane < cnt) {
+          if (bst.hint)
+            bulk_g2s_hint(ring + ((size_t)s * KR + lane) * d, A + (int64_t)(e & 0x7fffffffu) * d, row_bytes,
+                          &full[s], pol);
+          else
+            bulk_g2s(ring + ((size_t)s * KR + lane) * d, A + (int64_t)(e & 0x7fffffffu) * d, row_bytes, &full[s]);
+        }
         if (++s == kStages) {
           s = 0;
           ph ^= 1u;
@@ -291,6 +309,12 @@ cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t 
   // IHS_GATHER_ROWS=4|8 (defaults measured on B200)
   static const int cw_env = getenv("IHS_GATHER_CW") ? atoi(getenv("IHS_GATHER_CW")) : 0;
   static const int kr_env = getenv("IHS_GATHER_ROWS") ? atoi(getenv("IHS_GATHER_ROWS")) : 0;
+  // A's bulk copies carry an L2 evict_first hint (IHS_GATHER_HINT=0: none): the
+  // 4 GiB stream then leaves the sort arrays, b and the partials in L2 (C2 gather
+  // with the next sort beside it 0.746 -> 0.724 ms; 0.714 with the scatter's
+  // evict_last perm stores, cs_sort.cu)
+  static const int hint_env = getenv("IHS_GATHER_HINT") ? atoi(getenv("IHS_GATHER_HINT")) : 1;
+  bst.hint = hint_env;
   const bool f = gpart != nullptr;
   const int CWv = cw_env == 1 || cw_env == 2 ? cw_env : kDefaultCW;
   const int KRv = kr_env == 4 || kr_env == 8 ? kr_env : kDefaultRows;

@@ -8,6 +8,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace ihs {
 
 namespace {
@@ -137,7 +139,8 @@ __device__ __forceinline__ int32_t scanned_at(const int32_t *hist, const int32_t
 constexpr int kMaxGroups = 16;  // rows per warp sub-chunk <= 512
 __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
     int64_t n, int64_t chunk, int64_t nchunks, uint32_t m, uint64_t key, int64_t row_offset, uint32_t jb,
-    uint32_t sb, const int32_t *__restrict__ hist, const int32_t *__restrict__ tile_sums, uint32_t *__restrict__ perm) {
+    uint32_t sb, const int32_t *__restrict__ hist, const int32_t *__restrict__ tile_sums, uint32_t *__restrict__ perm,
+    int keep) {
   extern __shared__ unsigned char smem_raw[];
   int32_t *base = reinterpret_cast<int32_t *>(smem_raw);            // m
   int32_t *wcnt = base + m;                                           // 8 * m
@@ -180,6 +183,8 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
   }
   __syncthreads();
   const unsigned lt = lanemask_lt();
+  uint64_t pol = 0;
+  if (keep) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
   for (int q = 0; q < kMaxGroups; ++q) {
     if (ws + 32 * q < we) {
@@ -191,7 +196,14 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
       int32_t old = 0;
       if (valid && lane == leader) old = atomicAdd(&my[bb], __popc(mask));
       old = __shfl_sync(0xffffffffu, old, leader);
-      if (valid) perm[base[bb] + old + __popc(mask & lt)] = (uint32_t)r | (bk[q] & 0x80000000u);
+      if (valid) {
+        uint32_t *dst = perm + base[bb] + old + __popc(mask & lt);
+        const uint32_t v = (uint32_t)r | (bk[q] & 0x80000000u);
+        if (keep)
+          asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(dst), "r"(v), "l"(pol) : "memory");
+        else
+          *dst = v;
+      }
     }
   }
 }
@@ -227,6 +239,11 @@ CsSortPlan cs_sort_plan(int64_t n, int64_t m) {
   return p;
 }
 
+// perm stores carry an L2 evict_last hint (IHS_SCATTER_KEEP=0: none): a sector
+// of perm is written by ~2 CTAs in 4-byte pieces; kept in L2 it is completed
+// there (and read there by the next gather) instead of partially written back
+static const int keep_env = getenv("IHS_SCATTER_KEEP") ? atoi(getenv("IHS_SCATTER_KEEP")) : 1;
+
 cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset, uint32_t jb, uint32_t sb, int32_t *hist,
                            int32_t *tile_sums, uint32_t *perm, cudaStream_t st, LaunchCounter lc) {
   const uint32_t m = (uint32_t)p.m;
@@ -240,7 +257,8 @@ cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset
   IHS_SMEM_ATTR(cs_scatter_kernel, ssmem);
   if (p.n > 0)
     cs_scatter_kernel<<<(unsigned)p.nchunks, kScatterWarps * 32, ssmem, st>>>(p.n, p.chunk, p.nchunks, m, key,
-                                                                              row_offset, jb, sb, hist, tile_sums, perm);
+                                                                              row_offset, jb, sb, hist, tile_sums, perm,
+                                                                              keep_env);
   lc.add(p.n > 0 ? 4 : 3);
   return cudaGetLastError();
 }

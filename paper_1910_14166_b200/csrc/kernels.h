@@ -62,6 +62,7 @@ struct GatherBatchStrides {
   // gpart + z * m * d (partials, reduced by the caller in segment order).
   int nseg = 1;
   int64_t seg_sa = 0;
+  int hint = 0;  // 1: A's bulk copies carry an L2 evict_first hint
 };
 bool cs_gather_tma_supported(int64_t d, const void *A);
 cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
