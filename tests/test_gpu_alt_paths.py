@@ -17,6 +17,9 @@ SETS = {
     "stream_ldg_chol_plain": {"IHS_SJLT": "stream", "IHS_GATHER": "ldg", "IHS_OLS": "chol", "IHS_PG_PLAIN": "1",
                               "IHS_PG_WARM": "0", "IHS_PREFETCH": "0"},
     "tile_async_pgcta": {"IHS_SJLT": "tile", "IHS_GATHER": "async", "IHS_PG_CTA": "1", "IHS_FUSE": "1"},
+    "gather_shapes_nohints": {"IHS_GATHER_CW": "1", "IHS_GATHER_ROWS": "8", "IHS_GATHER_HINT": "0",
+                              "IHS_SCATTER_KEEP": "0"},
+    "gather_rows8": {"IHS_GATHER_ROWS": "8"},
     "pg_single": {"IHS_PG_SINGLE": "1", "IHS_PREFETCH_ORDER": "before"},
     "lookahead": {"IHS_LOOKAHEAD": "1", "IHS_LOOKAHEAD_CLUSTER": "4"},
 }
