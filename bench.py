@@ -427,8 +427,11 @@ def main():
             e2e = {"value": cfg.n * T_e2e / sec, "unit": UNIT, "h2d_bytes_per_step": 8 * n_loc * d + 8 * n_loc,
                    "d2h_bytes_per_step": 8 * d, "ms_per_step": sec * 1e3,
                    "step": f"one ihs_solve_ols call ({T_e2e} IHS iterations) on host-pinned A, b; x read back",
-                   "x_matches_device_run": bool(torch.equal(xo_h.to(dev), xh2[T_e2e])) if ttt and ttt.get("iterations")
-                   and T_e2e == ttt["iterations"] else None}
+                   # the solve call's last pass forms g alone (no sketch to look ahead to), so x^T
+                   # agrees with the step-by-step device run to rounding, not bit for bit
+                   "x_rel_diff_vs_device_run": float(torch.linalg.norm(xo_h.to(dev) - xh2[T_e2e])
+                                                     / torch.linalg.norm(xh2[T_e2e]))
+                   if ttt and ttt.get("iterations") and T_e2e == ttt["iterations"] else None}
             ctx2.close()
             del A_h, b_h
         except Exception as ex:  # report, do not hide
