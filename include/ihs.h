@@ -196,6 +196,14 @@ ihs_status ihs_ols_factor(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, d
 ihs_status ihs_ols_apply(ihs_ctx ctx, const double *Hinv, const double *g, int64_t d,
                          const double *x, double *x_next);
 
+/* Look-ahead Gram for the l1-ball / LASSO updates: H = scale^2 SA^T SA (d x d)
+ * on the factor stream (as ihs_ols_factor, with a Gram plan for a few SMs so it
+ * runs beside other work).  Joined by the next ihs_l1ball_update /
+ * ihs_lasso_update / ihs_ols_update / ihs_ols_apply that reads this H, or by
+ * ihs_ctx_synchronize / ihs_ctx_destroy. */
+ihs_status ihs_gram_lookahead(ihs_ctx ctx, const double *SA, int64_t m, int64_t d, double scale,
+                              double *H);
+
 /* One look-ahead OLS step on one rank (nothing to all-reduce): the pass over A
  * (dense) at x forms g = A^T (b - A x) (written to g, d) and, if SA_next is
  * not NULL, S^{iter_next} A into SA_next (m x d, as ihs_sketch); if Hinv_next

@@ -85,6 +85,7 @@ _EXPORTS = {
     "ihs_gram_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p]),
     "ihs_ols_factor": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p]),
+    "ihs_gram_lookahead": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p]),
     "ihs_ols_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "ihs_ols_lookahead_step": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.POINTER(SketchSpec), C.c_uint64,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -357,6 +358,16 @@ def ihs_ols_factor(SA: torch.Tensor, scale: float = 1.0, out=None, ctx: Context 
     Hinv = out if out is not None else _f64((d, d), SA.device)
     _check(lib().ihs_ols_factor(ctx._bind(), _p(SA), m, d, float(scale), _p(Hinv)), "ihs_ols_factor")
     return Hinv
+
+
+def ihs_gram_lookahead(SA: torch.Tensor, scale: float = 1.0, out=None, ctx: Context | None = None):
+    """H = scale^2 SA^T SA on the context's factor stream (look-ahead Gram for the
+    l1 / LASSO updates); joined by the next update that reads H / ctx.synchronize()."""
+    ctx = ctx or default_context(SA.device)
+    m, d = SA.shape
+    H = out if out is not None else _f64((d, d), SA.device)
+    _check(lib().ihs_gram_lookahead(ctx._bind(), _p(SA), m, d, float(scale), _p(H)), "ihs_gram_lookahead")
+    return H
 
 
 def ihs_ols_apply(Hinv, g, x, out=None, ctx: Context | None = None):

@@ -55,7 +55,7 @@ constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 
 enum Slot {
   S_PERM, S_HIST, S_TILES, S_GPART, S_GRAM, S_SJLT, S_CHOL, S_PACK, S_H, S_X, S_MISC, S_ERR,
-  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_PG, S_NSLOTS
+  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_PG, S_GRAMF, S_NSLOTS
 };
 }  // namespace
 
@@ -474,6 +474,7 @@ ihs_status gram_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double s
 }
 
 ihs_status ols_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const double *x, double *xn) {
+  IHS_TRY(wait_factor(c, H));
   double *sc;
   IHS_TRY(scratch(c, S_CHOL, chol_scratch_bytes(d), &sc));
   Prof pr(c, IHS_K_CHOL);
@@ -505,8 +506,9 @@ ihs_status gram_ols_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, doub
 // wait for this factor (the look-ahead loop enqueues the factor of S^{t+1}
 // before the apply of H_t^{-1}, so that its cluster is placed before the next
 // pass's gather fills the SMs).
-ihs_status ols_factor_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *Hinv) {
-  if (!gram_ols_supported(d) || m < 1) return IHS_ERR_UNSUPPORTED;
+// The factor stream, ordered after everything already on the ctx stream; the
+// returned record gets the completion event of the work enqueued next.
+ihs_status factor_begin(ihs_ctx c, const double *out, ihs_ctx_s::Factor **rec) {
   if (!c->fstream) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
@@ -516,7 +518,7 @@ ihs_status ols_factor_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, do
   }
   ihs_ctx_s::Factor *slot = nullptr;
   for (auto &f : c->fac)
-    if (f.pending && f.Hinv == Hinv) slot = &f;  // a rewrite of the same buffer: fstream order suffices
+    if (f.pending && f.Hinv == out) slot = &f;  // a rewrite of the same buffer: fstream order suffices
   if (!slot)
     for (auto &f : c->fac)
       if (!f.pending) {
@@ -529,16 +531,46 @@ ihs_status ols_factor_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, do
   }
   IHS_CUDA(cudaEventRecord(c->ev_fmain, c->stream));
   IHS_CUDA(cudaStreamWaitEvent(c->fstream, c->ev_fmain, 0));
+  *rec = slot;
+  return IHS_OK;
+}
+
+ihs_status factor_end(ihs_ctx c, const double *out, ihs_ctx_s::Factor *slot) {
+  IHS_CUDA(cudaEventRecord(slot->done, c->fstream));
+  slot->Hinv = out;
+  slot->pending = true;
+  c->f_pending = true;
+  return IHS_OK;
+}
+
+// Look-ahead Gram for the l1 / LASSO updates: H = scale^2 SA^T SA on the factor
+// stream with a Gram plan for a few SMs (it runs beside the previous update's
+// PG cluster; the update that reads H joins it).
+ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {
+  if (m < 1 || d < 1) return IHS_ERR_INVALID_ARGUMENT;
+  static const int side_sms = getenv("IHS_LOOKAHEAD_SMS") ? std::max(1, atoi(getenv("IHS_LOOKAHEAD_SMS"))) : 16;
+  GramPlan p = gram_plan(m, d, std::min(side_sms, c->num_sms));
+  double *part;
+  IHS_TRY(scratch(c, S_GRAMF, p.partial_bytes(), &part));  // (before factor_begin: a regrowth joins)
+  ihs_ctx_s::Factor *slot;
+  IHS_TRY(factor_begin(c, H, &slot));
+  {
+    Prof pr(c, IHS_K_FACTOR, c->fstream);
+    IHS_CUDA(launch_gram(p, SA, scale, part, H, c->fstream, lc_of(c)));
+  }
+  return factor_end(c, H, slot);
+}
+
+ihs_status ols_factor_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *Hinv) {
+  if (!gram_ols_supported(d) || m < 1) return IHS_ERR_UNSUPPORTED;
+  ihs_ctx_s::Factor *slot;
+  IHS_TRY(factor_begin(c, Hinv, &slot));
   static const int max_cluster = getenv("IHS_LOOKAHEAD_CLUSTER") ? atoi(getenv("IHS_LOOKAHEAD_CLUSTER")) : 8;
   {
     Prof pr(c, IHS_K_FACTOR, c->fstream);
     IHS_CUDA(launch_ols_factor(SA, m, d, scale, Hinv, c->d_status, max_cluster, c->fstream, lc_of(c)));
   }
-  IHS_CUDA(cudaEventRecord(slot->done, c->fstream));
-  slot->Hinv = Hinv;
-  slot->pending = true;
-  c->f_pending = true;
-  return IHS_OK;
+  return factor_end(c, Hinv, slot);
 }
 
 // Look-ahead OLS, part 2: x_next = x + Hinv g on the ctx stream, after the
@@ -575,6 +607,7 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
   if (k.max_inner < 1 || k.power_iters < 1 || !(k.inner_tol >= 0.0) || !(k.lip_safety > 0.0))
     return IHS_ERR_INVALID_ARGUMENT;
   if (!pg_supported(d) || (prox && !lasso_supported(d))) return IHS_ERR_UNSUPPORTED;
+  IHS_TRY(wait_factor(c, H));  // a look-ahead Gram that writes H
   // warm-started power iteration across calls with the same d (IHS_PG_WARM=0 off)
   static const bool warm_env = !getenv("IHS_PG_WARM") || std::strcmp(getenv("IHS_PG_WARM"), "0") != 0;
   double *ev = nullptr;
@@ -655,6 +688,40 @@ ihs_status ols_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_s
   return IHS_OK;
 }
 
+// Look-ahead for the l1 ball / LASSO (constraint 1 / 2): the Gram of S^{t+1} A
+// (formed by pass t with g^t) runs on the factor stream beside the PG update of
+// iteration t; the update of t + 1 then finds H_{t+1} ready.  T + 1 passes.
+ihs_status pg_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, const double *b,
+                             uint64_t iter0, int32_t T, double *xh, double radius, const ihs_inner_cfg *cfg,
+                             int32_t *inner_dev, int prox) {
+  const int64_t d = A->n_cols, m = spec->m, pk = m * d + d;
+  double *packs, *H;
+  IHS_TRY(scratch(c, S_PACK, (size_t)2 * pk * 8, &packs));
+  IHS_TRY(scratch(c, S_H, (size_t)2 * d * d * 8, &H));
+  auto allreduce = [&](double *buf, int64_t cnt) -> ihs_status {
+    if (c->world > 1) {
+      if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
+      if (g_nccl.AllReduce(buf, buf, (size_t)cnt, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
+        return IHS_ERR_COMM;
+    }
+    return IHS_OK;
+  };
+  IHS_TRY(sketch_grad_impl(c, A, spec, iter0, nullptr, nullptr, packs, nullptr));
+  IHS_TRY(allreduce(packs, m * d));
+  IHS_TRY(gram_side_impl(c, packs, m, d, 1.0, H));
+  for (int32_t t = 0; t < T; ++t) {
+    const int cur = t & 1, nxt = cur ^ 1;
+    const bool more = t + 1 < T;
+    double *SAn = packs + nxt * pk, *gn = SAn + m * d;
+    const double *x = xh + (int64_t)t * d;
+    IHS_TRY(sketch_grad_impl(c, A, spec, iter0 + (uint64_t)t + 1, b, x, more ? SAn : nullptr, gn));
+    IHS_TRY(more ? allreduce(SAn, pk) : allreduce(gn, d));
+    if (more) IHS_TRY(gram_side_impl(c, SAn, m, d, 1.0, H + nxt * d * d));
+    IHS_TRY(l1_impl(c, H + cur * d * d, gn, d, x, radius, cfg, xh + (int64_t)(t + 1) * d, inner_dev + t, prox));
+  }
+  return IHS_OK;
+}
+
 // The look-ahead schedule pays when a pass over A is long next to the Gram +
 // Cholesky it hides: dense, d <= 128, n d >= 2^24 (per rank), T >= 3, and a
 // CountSketch (an SJLT pass is s gathers, next to which the d x d work is
@@ -666,6 +733,15 @@ bool use_lookahead(const ihs_matrix *A, const ihs_sketch_spec *spec, int32_t T) 
   const bool ok = A->layout == IHS_DENSE_ROW_MAJOR && gram_ols_supported(d) && spec->m >= 1 && T >= 1;
   if (env) return ok && std::strcmp(env, "0") != 0;
   return ok && spec->s == 1 && T >= 3 && A->n_rows * d >= (int64_t(1) << 24);
+}
+
+// l1 / LASSO look-ahead (the Gram only): dense CountSketch, n d >= 2^24, T >= 3;
+// IHS_LOOKAHEAD=0 / 1 as for OLS.
+bool use_lookahead_pg(const ihs_matrix *A, const ihs_sketch_spec *spec, int32_t T) {
+  static const char *env = getenv("IHS_LOOKAHEAD");
+  const bool ok = A->layout == IHS_DENSE_ROW_MAJOR && spec->m >= 1 && T >= 1 && pg_supported(A->n_cols);
+  if (env) return ok && std::strcmp(env, "0") != 0;
+  return ok && spec->s == 1 && T >= 3 && A->n_rows * A->n_cols >= (int64_t(1) << 24);
 }
 
 // Shared IHS loop (a1-a7).  constraint 0 = OLS, 1 = l1 ball.
@@ -738,8 +814,10 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
   if (trace)
     for (auto &e : ev) IHS_CUDA(cudaEventCreate(&e));
   ihs_status result = IHS_OK;
-  const bool lookahead = constraint == 0 && !trace && use_lookahead(&A, spec, T);
-  if (lookahead) IHS_TRY(ols_lookahead_loop(c, &A, spec, b, iter0, T, xh));
+  const bool lookahead = !trace && (constraint == 0 ? use_lookahead(&A, spec, T) : use_lookahead_pg(&A, spec, T));
+  if (lookahead && constraint == 0) IHS_TRY(ols_lookahead_loop(c, &A, spec, b, iter0, T, xh));
+  if (lookahead && constraint >= 1)
+    IHS_TRY(pg_lookahead_loop(c, &A, spec, b, iter0, T, xh, radius, cfg, inner_dev, constraint == 2 ? 1 : 0));
   for (int32_t t = 0; !lookahead && t < T; ++t) {
     const double *x = xh + (int64_t)t * d;
     double *xn = xh + (int64_t)(t + 1) * d;
@@ -1019,6 +1097,12 @@ ihs_status ihs_ols_factor(ihs_ctx c, const double *SA, int64_t m, int64_t d, dou
   if (!c || !SA || !Hinv || m < 1 || d < 1 || !std::isfinite(scale)) return IHS_ERR_INVALID_ARGUMENT;
   DevGuard g(c->device);
   return ols_factor_impl(c, SA, m, d, scale, Hinv);
+}
+
+ihs_status ihs_gram_lookahead(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {
+  if (!c || !SA || !H || m < 1 || d < 1 || !std::isfinite(scale)) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  return gram_side_impl(c, SA, m, d, scale, H);
 }
 
 ihs_status ihs_ols_apply(ihs_ctx c, const double *Hinv, const double *gv, int64_t d, const double *x, double *xn) {

@@ -60,6 +60,9 @@ class CudaOps:
     def ols_apply(self, Hinv, g, x, xn):
         P.ihs_ols_apply(Hinv, g, x, out=xn, ctx=self.ctx)
 
+    def gram_lookahead(self, SA, H):
+        P.ihs_gram_lookahead(SA, out=H, ctx=self.ctx)
+
     def lookahead_step(self, A, spec, t_next, b, x, Hinv, SA_next, Hinv_next, g, xn):
         P.ihs_ols_lookahead_step(A, spec, t_next, b, x, Hinv, SA_next=SA_next, Hinv_next=Hinv_next, g=g, out=xn,
                                  ctx=self.ctx)
@@ -74,13 +77,13 @@ class CudaOps:
         return P.ihs_pred_err2(A, X, xref, ctx=self.ctx)
 
 
-def lookahead_default(A, d: int, spec: P.Spec) -> bool:
-    """The look-ahead OLS schedule pays when one pass over A is long next to
-    the Gram + Cholesky it hides (d <= 128, dense, CountSketch, n d >= 2^24 on
-    this rank); IHS_LOOKAHEAD=0/1 overrides (the rule of ihs_solve_ols, api.cu)."""
+def lookahead_default(A, d: int, spec: P.Spec, constraint: str = "ols") -> bool:
+    """The look-ahead schedule pays when one pass over A is long next to the
+    d x d work it hides (dense, CountSketch, n d >= 2^24 on this rank; OLS:
+    d <= 128); IHS_LOOKAHEAD=0/1 overrides (the rule of ihs_solve_*, api.cu)."""
     import os
     env = os.environ.get("IHS_LOOKAHEAD")
-    ok = isinstance(A, P.Dense) and 1 <= d <= 128
+    ok = isinstance(A, P.Dense) and d >= 1 and (d <= 128 or constraint != "ols")
     if env is not None:
         return ok and env != "0"
     return ok and spec.s == 1 and A.n * d >= (1 << 24)
@@ -95,8 +98,10 @@ class ShardedIHS:
     (Gram + Cholesky + inverse, ``ols_factor``) is computed on a side stream
     during the NEXT pass; the step itself only applies x^{t+1} = x^t +
     H_t^{-1} g^t (``ols_apply``).  Same iterates as the plain schedule (each
-    iteration still uses its own S^t), to rounding.  A step whose t does not
-    follow the previous one first sketches S^t A (the prologue)."""
+    iteration still uses its own S^t), to rounding.  For the l1 ball / LASSO
+    only the Gram looks ahead (``gram_lookahead``: H_{t+1} beside the PG
+    update of t).  A step whose t does not follow the previous one first
+    sketches S^t A (the prologue)."""
 
     def __init__(self, A, b: torch.Tensor, spec: P.Spec, *, constraint: str = "ols", radius: float = 0.0,
                  cfg=None, ops=None, allreduce=None, group=None, lookahead: bool | None = None):
@@ -122,12 +127,13 @@ class ShardedIHS:
         self.H = torch.empty((d, d), dtype=torch.float64, device=dev)
         self.inner = torch.zeros(1, dtype=torch.int32, device=dev)
         if lookahead is None:
-            lookahead = lookahead_default(A, d, spec)
-        self.lookahead = bool(lookahead) and constraint == "ols" and hasattr(self.ops, "ols_factor")
+            lookahead = lookahead_default(A, d, spec, constraint)
+        need = "ols_factor" if constraint == "ols" else "gram_lookahead"
+        self.lookahead = bool(lookahead) and hasattr(self.ops, need)
         self._la_t = None  # iteration whose H^{-1} is in self.Hinv[self._la_cur]
         if self.lookahead:
             self.packs = torch.empty((2, m * d + d), dtype=torch.float64, device=dev)
-            self.Hinv = torch.empty((2, d, d), dtype=torch.float64, device=dev)
+            self.Hinv = torch.empty((2, d, d), dtype=torch.float64, device=dev)  # H^{-1} (OLS) or H
             self._la_cur = 0
 
     def prime(self, t: int) -> None:
@@ -138,7 +144,10 @@ class ShardedIHS:
         pk = self.packs[0]
         self.ops.sketch(self.A, self.spec, t, pk[: m * d].view(m, d))
         self.allreduce(pk[: m * d])
-        self.ops.ols_factor(pk[: m * d].view(m, d), self.Hinv[0])
+        if self.constraint == "ols":
+            self.ops.ols_factor(pk[: m * d].view(m, d), self.Hinv[0])
+        else:
+            self.ops.gram_lookahead(pk[: m * d].view(m, d), self.Hinv[0])
         self._la_t, self._la_cur = t, 0
 
     def step(self, t: int, x: torch.Tensor, xn: torch.Tensor) -> torch.Tensor:
@@ -149,6 +158,17 @@ class ShardedIHS:
             cur, nxt = self._la_cur, 1 - self._la_cur
             pk = self.packs[nxt]
             SAn, gn = pk[: m * d].view(m, d), pk[m * d:]
+            if self.constraint != "ols":  # l1 / LASSO: only the Gram looks ahead
+                self.ops.sketch_grad(self.A, self.spec, t + 1, self.b, x, SAn, gn)
+                self.allreduce(pk)
+                self.ops.gram_lookahead(SAn, self.Hinv[nxt])  # beside this update's PG
+                H = self.Hinv[cur]
+                if self.constraint == "lasso":
+                    self.ops.lasso(H, gn, x, self.radius, self.cfg, xn, self.inner)
+                else:
+                    self.ops.l1(H, gn, x, self.radius, self.cfg, xn, self.inner)
+                self._la_t, self._la_cur = t + 1, nxt
+                return xn
             if self._solo and hasattr(self.ops, "lookahead_step"):
                 self.ops.lookahead_step(self.A, self.spec, t + 1, self.b, x, self.Hinv[cur], SAn, self.Hinv[nxt], gn,
                                         xn)

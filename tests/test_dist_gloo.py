@@ -62,6 +62,9 @@ class OracleLookaheadOps(OracleOps):
     def ols_apply(self, Hinv, g, x, xn):
         xn.copy_(x + Hinv @ g)
 
+    def gram_lookahead(self, SA, H):
+        H.copy_(torch.from_numpy(self.o.gram(SA.numpy())))
+
 
 def _free_port():
     s = socket.socket()
@@ -122,6 +125,7 @@ def test_shard_rows_partition():
     {"cfg": "C5", "n": 3001, "m": 256, "s": 8, "T": 4, "iter0": 7, "constraint": "ols"},
     {"cfg": "C4", "n": 4000, "m": 512, "s": 1, "T": 4, "iter0": 0, "constraint": "l1ball"},
     {"cfg": "C2", "n": 5001, "m": 256, "s": 1, "T": 5, "iter0": 2, "constraint": "ols", "lookahead": True},
+    {"cfg": "C4", "n": 4000, "m": 512, "s": 1, "T": 4, "iter0": 1, "constraint": "l1ball", "lookahead": True},
 ])
 def test_sharded_ihs_matches_unsharded_oracle(oracle_mod, case):
     import synthetic

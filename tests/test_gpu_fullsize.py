@@ -56,7 +56,7 @@ def check_hash(P, oracle_mod, cfg, t, windows):
 
 @pytest.mark.parametrize("name", ["C2", "C2-plain", "C4", "C5", "C4P"])
 def test_dense_full_size(P, oracle_mod, name):
-    """One step in the bench's launch configuration (C2: the look-ahead OLS
+    """One step in the bench's launch configuration (C2, C4, C4P: the look-ahead
     schedule by default; C2-plain and C5 (SJLT): the plain one)."""
     from paper_1910_14166_b200.dist import CudaOps, ShardedIHS
     plain = name.endswith("-plain")
@@ -69,7 +69,7 @@ def test_dense_full_size(P, oracle_mod, name):
     spec = P.Spec(m=cfg.m, s=cfg.s)
     S = ShardedIHS(P.Dense(prob["A"]), prob["b"], spec, ops=CudaOps(ctx), constraint=cfg.constraint,
                    radius=prob["lam"] if cfg.constraint == "lasso" else prob["tau"], lookahead=False if plain else None)
-    assert S.lookahead == (cfg.constraint == "ols" and cfg.s == 1 and not plain)
+    assert S.lookahead == (cfg.s == 1 and not plain)
     rng = np.random.default_rng(0)
     x = torch.from_numpy(rng.standard_normal(d) * 0.1).to(DEV)
     xn = torch.empty_like(x)
@@ -82,8 +82,11 @@ def test_dense_full_size(P, oracle_mod, name):
         SA, g = S.packs[0][: m * d].view(m, d).cpu().numpy(), S.packs[1][m * d:].cpu().numpy()
         SA1 = S.packs[1][: m * d].view(m, d).cpu().numpy()
         H = oracle_mod.gram(SA)
-        Hinv = S.Hinv[0].cpu().numpy()
-        assert rel_fro(Hinv @ H, np.eye(d)) <= 1e-11
+        if cfg.constraint == "ols":  # H^{-1} of S^t A
+            assert rel_fro(S.Hinv[0].cpu().numpy() @ H, np.eye(d)) <= 1e-11
+        else:  # the look-ahead Gram of S^t A (what the update used)
+            H = S.Hinv[0].cpu().numpy()
+            assert rel_fro(H, oracle_mod.gram(SA)) <= 1e-12
         rows1 = np.array([0, m - 1, m // 3])
         ref1 = oracle_mod.sketch_dense_rows(A, 0, t + 1, m, cfg.s, rows1)
         if cfg.s == 1:

@@ -269,6 +269,34 @@ def test_sharded_lookahead_matches_oracle(P, oracle_mod, cfg_name, n, T, iter0, 
     assert ctx.status() == P.OK
 
 
+@pytest.mark.parametrize("constraint", ["l1ball", "lasso"])
+def test_sharded_lookahead_pg_matches_oracle(P, oracle_mod, constraint):
+    """l1 ball / LASSO look-ahead: H_{t+1} (ihs_gram_lookahead) beside the update of t."""
+    from paper_1910_14166_b200.dist import CudaOps, ShardedIHS
+    name = "C4" if constraint == "l1ball" else "C4P"
+    cfg, A, b, prob = dense_case(name, 20_000)
+    radius = prob["tau"] if constraint == "l1ball" else prob["lam"]
+    ctx = P.Context(0)
+    S = ShardedIHS(P.Dense(prob["A"].to(DEV)), prob["b"].to(DEV), P.Spec(m=cfg.m), ops=CudaOps(ctx),
+                   constraint=constraint, radius=radius, lookahead=True)
+    assert S.lookahead
+    T = 4
+    xh = S.solve(T, iter0=1).cpu().numpy()
+    xo, _ = oracle_mod.ihs_solve(A, b, m=cfg.m, s=1, T=T, iter0=1, constraint=constraint, tau=radius)
+    for t in range(1, T + 1):
+        assert oracle_mod.pred_rel_err(xh[t], xo[t], A) <= 1e-9, t
+    assert ctx.status() == P.OK
+
+
+def test_gram_lookahead(P, oracle_mod):
+    rng = np.random.default_rng(5)
+    SA = rng.standard_normal((2048, 256))
+    ctx = P.Context(0)
+    H = P.ihs_gram_lookahead(torch.from_numpy(SA).to(DEV), scale=0.5, ctx=ctx)
+    ctx.synchronize()
+    assert rel_fro(H.cpu().numpy(), 0.25 * oracle_mod.gram(SA)) <= 1e-12
+
+
 def test_ols_update_not_spd(P):
     ctx = P.Context(0)
     H = torch.diag(torch.tensor([1.0, -1.0, 2.0], dtype=torch.float64, device=DEV))
