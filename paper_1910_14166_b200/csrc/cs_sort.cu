@@ -8,6 +8,7 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <algorithm>
 #include <cstdlib>
 
 namespace ihs {
@@ -32,21 +33,26 @@ __global__ void hash_export_kernel(uint64_t key, uint32_t s, uint32_t M, int64_t
 }
 
 // Per-chunk bucket histogram, written bucket-major: hist[b * nchunks + chunk].
+// CTA k handles chunks k, k + gridDim.x, ... (gridDim.x = nchunks by default;
+// fewer, persistent CTAs with IHS_SORT_CTAS).
 __global__ void __launch_bounds__(kHistThreads) cs_hist_kernel(int64_t n, int64_t chunk, int64_t nchunks,
                                                                uint32_t m, uint64_t key, int64_t row_offset,
                                                                uint32_t jb, uint32_t sb, int32_t *__restrict__ hist) {
   extern __shared__ int32_t cnt[];
-  for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) cnt[b] = 0;
-  __syncthreads();
-  const int64_t r0 = blockIdx.x * chunk;
-  const int64_t r1 = min(n, r0 + chunk);
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
-    bool neg;
-    uint32_t b = hash_bucket(key, (uint64_t)(row_offset + r), jb, sb, m, neg) - jb * m;
-    atomicAdd(&cnt[b], 1);
+  for (int64_t cb = blockIdx.x; cb < nchunks; cb += gridDim.x) {
+    for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    const int64_t r0 = cb * chunk;
+    const int64_t r1 = min(n, r0 + chunk);
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+      bool neg;
+      uint32_t b = hash_bucket(key, (uint64_t)(row_offset + r), jb, sb, m, neg) - jb * m;
+      atomicAdd(&cnt[b], 1);
+    }
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) hist[(int64_t)b * nchunks + cb] = cnt[b];
+    __syncthreads();
   }
-  __syncthreads();
-  for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) hist[(int64_t)b * nchunks + blockIdx.x] = cnt[b];
 }
 
 // Exclusive scan, phase 1: each 4096-entry tile scanned locally in place; the
@@ -137,8 +143,8 @@ __device__ __forceinline__ int32_t scanned_at(const int32_t *hist, const int32_t
 // complete in issue order, so positions follow ascending row order within
 // every bucket (stable).
 constexpr int kMaxGroups = 16;  // rows per warp sub-chunk <= 512
-__global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
-    int64_t n, int64_t chunk, int64_t nchunks, uint32_t m, uint64_t key, int64_t row_offset, uint32_t jb,
+__device__ __forceinline__ void cs_scatter_chunk(
+    int64_t cb, int64_t n, int64_t chunk, int64_t nchunks, uint32_t m, uint64_t key, int64_t row_offset, uint32_t jb,
     uint32_t sb, const int32_t *__restrict__ hist, const int32_t *__restrict__ tile_sums, uint32_t *__restrict__ perm,
     int keep) {
   extern __shared__ unsigned char smem_raw[];
@@ -147,7 +153,7 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (uint32_t e = threadIdx.x; e < kScatterWarps * m; e += blockDim.x) wcnt[e] = 0;
   __syncthreads();
-  const int64_t r0 = blockIdx.x * chunk;
+  const int64_t r0 = cb * chunk;
   const int64_t r1 = min(n, r0 + chunk);
   const int64_t sub = chunk / kScatterWarps;
   const int64_t ws = r0 + warp * sub;
@@ -172,7 +178,7 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
   }
   __syncthreads();
   for (uint32_t b = threadIdx.x; b < m; b += blockDim.x) {
-    base[b] = scanned_at(hist, tile_sums, (int64_t)b * nchunks + blockIdx.x);
+    base[b] = scanned_at(hist, tile_sums, (int64_t)b * nchunks + cb);
     int32_t acc = 0;
 #pragma unroll
     for (int w = 0; w < kScatterWarps; ++w) {
@@ -205,6 +211,16 @@ __global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
           *dst = v;
       }
     }
+  }
+}
+
+__global__ void __launch_bounds__(kScatterWarps * 32) cs_scatter_kernel(
+    int64_t n, int64_t chunk, int64_t nchunks, uint32_t m, uint64_t key, int64_t row_offset, uint32_t jb,
+    uint32_t sb, const int32_t *__restrict__ hist, const int32_t *__restrict__ tile_sums, uint32_t *__restrict__ perm,
+    int keep) {
+  for (int64_t cb = blockIdx.x; cb < nchunks; cb += gridDim.x) {
+    cs_scatter_chunk(cb, n, chunk, nchunks, m, key, row_offset, jb, sb, hist, tile_sums, perm, keep);
+    __syncthreads();
   }
 }
 }  // namespace
@@ -249,14 +265,16 @@ cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset
   const uint32_t m = (uint32_t)p.m;
   size_t hsmem = 4 * (size_t)m;
   IHS_SMEM_ATTR(cs_hist_kernel, hsmem);
-  cs_hist_kernel<<<(unsigned)p.nchunks, kHistThreads, hsmem, st>>>(p.n, p.chunk, p.nchunks, m, key, row_offset, jb, sb,
+  static const int sort_ctas = getenv("IHS_SORT_CTAS") ? atoi(getenv("IHS_SORT_CTAS")) : 0;
+  const unsigned grid = (unsigned)(sort_ctas > 0 ? std::min<int64_t>(sort_ctas, p.nchunks) : p.nchunks);
+  cs_hist_kernel<<<grid, kHistThreads, hsmem, st>>>(p.n, p.chunk, p.nchunks, m, key, row_offset, jb, sb,
                                                                     hist);
   scan_tiles_kernel<<<(unsigned)p.ntiles, 1024, 0, st>>>(hist, p.entries, tile_sums);
   scan_sums_kernel<<<1, 1024, 0, st>>>(tile_sums, p.ntiles);
   size_t ssmem = (4 + 4 * kScatterWarps) * (size_t)m;
   IHS_SMEM_ATTR(cs_scatter_kernel, ssmem);
   if (p.n > 0)
-    cs_scatter_kernel<<<(unsigned)p.nchunks, kScatterWarps * 32, ssmem, st>>>(p.n, p.chunk, p.nchunks, m, key,
+    cs_scatter_kernel<<<grid, kScatterWarps * 32, ssmem, st>>>(p.n, p.chunk, p.nchunks, m, key,
                                                                               row_offset, jb, sb, hist, tile_sums, perm,
                                                                               keep_env);
   lc.add(p.n > 0 ? 4 : 3);
