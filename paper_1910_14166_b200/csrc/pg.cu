@@ -414,6 +414,7 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
   int kk = 0;
   bool converged = false;
   double tk = 1.0;  // FISTA momentum parameter (accel) -- plain PG keeps vv = yv
+  double theta_prev = 0.0;  // the last projection threshold (warm start; IHS_PG_THETA_WARM=0: off)
   while (kk < max_inner) {
 #pragma unroll
     for (int k = 0; k < K; ++k) wv[k] = vv[k] - xv[k];
@@ -432,9 +433,15 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
     double theta = prox ? radius / L : 0.0;
     const bool proj = prox || n1 > radius;
     if (!prox && proj) {  // Michelot's fixed point (reading R19), warp-local
-      theta = (n1 - radius) / (double)d;
-      double cprev = (double)d;
-      for (int guard = 0; guard <= d; ++guard) {
+      // Warm start from the previous inner step's threshold: from any theta
+      // above theta* one update lands at or below it (the update's active set
+      // is a subset of the true one), and from below the iteration rises
+      // monotonically to theta*, stopping when the active set repeats -- the
+      // same final set, hence the same theta, as the cold start (n1 - tau) / d.
+      bool warm_th = (accel & 2) && theta_prev > 0.0;
+      theta = warm_th ? theta_prev : (n1 - radius) / (double)d;
+      double cprev = warm_th ? -1.0 : (double)d;
+      for (int guard = 0; guard <= d + 1; ++guard) {
         double Sv = 0.0, cv = 0.0;
 #pragma unroll
         for (int k = 0; k < K; ++k) {
@@ -445,10 +452,17 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
         }
         Sv = warp_sum(Sv);
         cv = warp_sum(cv);
+        if (cv == 0.0 && warm_th) {  // started above every |z|: cold start instead
+          warm_th = false;
+          theta = (n1 - radius) / (double)d;
+          cprev = (double)d;
+          continue;
+        }
         if (cv == cprev || cv == 0.0) break;
         theta = (Sv - radius) / cv;
         cprev = cv;
       }
+      theta_prev = theta;
     }
     double dn[K], yy[K], rs[K], ynv[K];
 #pragma unroll
@@ -465,7 +479,7 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
       ynv[k] = yn;
     }
     const double dnn = wsum_k(dn), yyy = wsum_k(yy);
-    if (accel) {
+    if (accel & 1) {
       const double rsum = wsum_k(rs);
       double coef = 0.0;
       if (rsum > 0.0) {
@@ -555,7 +569,10 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
       return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
                                 x_next, inner_iters, status);
     }
-    static const int accel = (getenv("IHS_PG_PLAIN") && std::strcmp(getenv("IHS_PG_PLAIN"), "0") != 0) ? 0 : 1;
+    // accel bit 0: FISTA (IHS_PG_PLAIN=1: off); bit 1: warm-started projection
+    // threshold (IHS_PG_THETA_WARM=0: off)
+    static const int accel = ((getenv("IHS_PG_PLAIN") && std::strcmp(getenv("IHS_PG_PLAIN"), "0") != 0) ? 0 : 1) |
+                             ((getenv("IHS_PG_THETA_WARM") && !std::strcmp(getenv("IHS_PG_THETA_WARM"), "0")) ? 0 : 2);
     // warm start (scratch = d doubles holding the last eigenvector estimate):
     // a dozen power steps from it instead of power_iters from 1/sqrt(d)
     const bool warm_ok = warm_start && scratch;

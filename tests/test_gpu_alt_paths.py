@@ -20,7 +20,7 @@ SETS = {
     "gather_shapes_nohints": {"IHS_GATHER_CW": "1", "IHS_GATHER_ROWS": "8", "IHS_GATHER_HINT": "0",
                               "IHS_SCATTER_KEEP": "0"},
     "gather_rows8": {"IHS_GATHER_ROWS": "8"},
-    "pg_single": {"IHS_PG_SINGLE": "1", "IHS_PREFETCH_ORDER": "before"},
+    "pg_single": {"IHS_PG_SINGLE": "1", "IHS_PREFETCH_ORDER": "before", "IHS_PG_THETA_WARM": "0"},
     "lookahead": {"IHS_LOOKAHEAD": "1", "IHS_LOOKAHEAD_CLUSTER": "4"},
 }
 
