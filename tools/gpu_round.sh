@@ -50,6 +50,8 @@ if has ncu; then
   $B --config C3 > $OUT/plain1_C3.log 2>&1 &&
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"gram_streamk|csr_sketch|ols_cg" -s 9 -c 3 \
     -o $OUT/full_C3 -f $B --config C3 > $OUT/ncu_full_C3.log 2>&1
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:csr_sketch -s 3 -c 1 \
+    -o $OUT/full_C3_csr -f $B --config C3 > $OUT/ncu_full_C3_csr.log 2>&1
   $B --config C4 > $OUT/plain1_C4.log 2>&1 &&
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"pg_warp|cs_gather_tma" -s 6 -c 2 \
     -o $OUT/full_C4 -f $B --config C4 > $OUT/ncu_full_C4.log 2>&1
