@@ -330,7 +330,7 @@ def test_ols_update_indefinite_positive_diagonal(P, d):
     assert torch.equal(xn, x)
 
 
-@pytest.mark.parametrize("d,tau", [(16, 1.0), (256, 10.0), (64, 1e9), (5, 0.0)])
+@pytest.mark.parametrize("d,tau", [(16, 1.0), (256, 10.0), (64, 1e9), (5, 0.0), (100, 3.0), (200, 5.0)])
 def test_l1ball_update(P, oracle_mod, d, tau):
     rng = np.random.default_rng(d)
     H = spd(rng, d)
