@@ -723,7 +723,8 @@ ihs_status pg_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_sp
 }
 
 // The look-ahead schedule pays when a pass over A is long next to the Gram +
-// Cholesky it hides: dense, d <= 128, n d >= 2^24 (per rank), T >= 3, and a
+// Cholesky it hides: dense, d <= 128, n d >= 2^27 (per rank: a pass of >= ~0.17 ms
+// next to a ~0.11 ms factor, so also at C2 on 4 GPUs, not on 8), T >= 3, and a
 // CountSketch (an SJLT pass is s gathers, next to which the d x d work is
 // < 0.3% on C5 and the measured difference was within run-to-run noise).
 // IHS_LOOKAHEAD=0 disables it, =1 uses it whenever supported.
@@ -732,16 +733,16 @@ bool use_lookahead(const ihs_matrix *A, const ihs_sketch_spec *spec, int32_t T) 
   const int64_t d = A->n_cols;
   const bool ok = A->layout == IHS_DENSE_ROW_MAJOR && gram_ols_supported(d) && spec->m >= 1 && T >= 1;
   if (env) return ok && std::strcmp(env, "0") != 0;
-  return ok && spec->s == 1 && T >= 3 && A->n_rows * d >= (int64_t(1) << 24);
+  return ok && spec->s == 1 && T >= 3 && A->n_rows * d >= (int64_t(1) << 27);
 }
 
-// l1 / LASSO look-ahead (the Gram only): dense CountSketch, n d >= 2^24, T >= 3;
+// l1 / LASSO look-ahead (the Gram only): dense CountSketch, n d >= 2^27, T >= 3;
 // IHS_LOOKAHEAD=0 / 1 as for OLS.
 bool use_lookahead_pg(const ihs_matrix *A, const ihs_sketch_spec *spec, int32_t T) {
   static const char *env = getenv("IHS_LOOKAHEAD");
   const bool ok = A->layout == IHS_DENSE_ROW_MAJOR && spec->m >= 1 && T >= 1 && pg_supported(A->n_cols);
   if (env) return ok && std::strcmp(env, "0") != 0;
-  return ok && spec->s == 1 && T >= 3 && A->n_rows * A->n_cols >= (int64_t(1) << 24);
+  return ok && spec->s == 1 && T >= 3 && A->n_rows * A->n_cols >= (int64_t(1) << 27);
 }
 
 // Shared IHS loop (a1-a7).  constraint 0 = OLS, 1 = l1 ball.

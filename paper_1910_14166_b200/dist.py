@@ -79,14 +79,14 @@ class CudaOps:
 
 def lookahead_default(A, d: int, spec: P.Spec, constraint: str = "ols") -> bool:
     """The look-ahead schedule pays when one pass over A is long next to the
-    d x d work it hides (dense, CountSketch, n d >= 2^24 on this rank; OLS:
+    d x d work it hides (dense, CountSketch, n d >= 2^27 on this rank; OLS:
     d <= 128); IHS_LOOKAHEAD=0/1 overrides (the rule of ihs_solve_*, api.cu)."""
     import os
     env = os.environ.get("IHS_LOOKAHEAD")
     ok = isinstance(A, P.Dense) and d >= 1 and (d <= 128 or constraint != "ols")
     if env is not None:
         return ok and env != "0"
-    return ok and spec.s == 1 and A.n * d >= (1 << 24)
+    return ok and spec.s == 1 and A.n * d >= (1 << 27)
 
 
 class ShardedIHS:
