@@ -297,12 +297,16 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
     if (use_sort) {
       CsSortPlan p = cs_sort_plan(n, M);
       // SJLT blocks are gathered nb at a time (one launch, grid.y = block) so
-      // that a launch has about one wave of bucket CTAs (7 per SM) even when
-      // M = m / s is small.  The sort buffers hold all s blocks; two sets, so
+      // that a launch has about two waves of bucket CTAs (7 per SM resident)
+      // even when M = m / s is small: the gradient-carrying block's slower CTAs
+      // then share a launch with three others (C5: 35.4 -> 34.4 ms/step against
+      // one wave; IHS_SJLT_NB=k overrides).  The sort buffers hold all s blocks; two sets, so
       // the next iteration's sort can be prefetched into the other set.
       const bool tma = c->gather == 1 && cs_gather_tma_supported(d, A->values);
-      const int nb = tma ? (int)std::max<int64_t>(1, std::min<int64_t>(s, (7 * (int64_t)c->num_sms) / std::max<int64_t>(M, 1)))
-                         : 1;
+      static const int nb_env = getenv("IHS_SJLT_NB") ? atoi(getenv("IHS_SJLT_NB")) : 0;
+      const int nb = !tma ? 1
+                     : nb_env > 0 ? (int)std::min<int64_t>(s, nb_env)
+                                  : (int)std::max<int64_t>(1, std::min<int64_t>(s, (14 * (int64_t)c->num_sms) / std::max<int64_t>(M, 1)));
       const int64_t hs = (int64_t)(p.hist_bytes() / 4 + 63) / 64 * 64, ts = (int64_t)(p.tiles_bytes() / 4 + 63) / 64 * 64;
       const int64_t ps = (p.n + 63) / 64 * 64;
       const bool hit = c->pre.valid && c->pre.key == key && c->pre.row_offset == A->row_offset && c->pre.n == n &&
