@@ -368,7 +368,12 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       };
       if (c->prefetch && n > 0) {
         if (!c->side) {
-          IHS_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+          // IHS_SIDE_PRIO=1: the sort stream at the highest priority (its CTAs
+          // take freed slots before pending gather CTAs)
+          static const bool side_hi = getenv("IHS_SIDE_PRIO") && atoi(getenv("IHS_SIDE_PRIO")) == 1;
+          int lo = 0, hi = 0;
+          cudaDeviceGetStreamPriorityRange(&lo, &hi);
+          IHS_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, side_hi ? hi : lo));
           IHS_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
           IHS_CUDA(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
         }
