@@ -330,7 +330,12 @@ cudaError_t launch_reduce_rows(const double *part, int64_t rows, int64_t d, doub
   if (d > 1024) return cudaErrorInvalidValue;
   const unsigned gx = (unsigned)((d + 31) / 32);
   const int64_t R = std::max<int64_t>(1, (rows + kReduceRowsPerCta - 1) / kReduceRowsPerCta);
-  if (R > 65535) return cudaErrorInvalidValue;
+  if (R > 65535) {  // (> 4M partial rows) one level over d/32 CTAs, then the update apart
+    reduce_rows_kernel<<<gx, 1024, 0, st>>>(part, rows, (int)d, rows, out);
+    lc.add();
+    if (Hinv) return launch_ols_apply(Hinv, out, d, x, x_next, st, lc);
+    return cudaGetLastError();
+  }
   reduce_rows_last_kernel<<<dim3(gx, (unsigned)R), kRedThreads, 0, st>>>(part, rows, (int)d, tmp, out, counter,
                                                                           Hinv, x, x_next);
   lc.add();
