@@ -319,7 +319,17 @@ cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t 
   const int CWv = cw_env == 1 || cw_env == 2 ? cw_env : kDefaultCW;
   const int KRv = kr_env == 4 || kr_env == 8 ? kr_env : kDefaultRows;
   // ring depth: ~kRingBytes of rows in flight per CTA, 2..kMaxStages stages
-  const int nst = (int)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, kRingBytes / (KRv * d * 8)));
+  // Bytes of rows in flight per CTA, measured per shape on B200 (step time):
+  // the fused single-block gather (C2, d = 128) 16 KiB 0.688 / 24 KiB 0.738 /
+  // 12 KiB 0.705 / 20 KiB 0.703 ms; d = 256 (C4) 40 KiB 0.771 / 32 KiB 0.775 /
+  // 24 KiB 0.784; SJLT batches (C5, d = 96) 24 KiB 34.6 / 12 KiB 35.6 ms.
+  // IHS_GATHER_RING=<KiB> overrides.
+  static const int ring_env = getenv("IHS_GATHER_RING") ? atoi(getenv("IHS_GATHER_RING")) : 0;  // KiB
+  const int64_t ring = ring_env > 0                        ? (int64_t)ring_env * 1024
+                       : d >= 192                          ? 40 * 1024
+                       : (f && nbatch == 1 && d <= 128)    ? 16 * 1024
+                                                           : kRingBytes;
+  const int nst = (int)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, ring / (KRv * d * 8)));
   const size_t smem = (size_t)nst * KRv * d * 8 + (size_t)nst * KRv * 8 * (1 + CWv) + 2 * kMaxStages * 8 +
                       kMaxStages * KRv * 8 + 64;
   const int nc = (int)((d + 32 * CWv - 1) / (32 * CWv));
