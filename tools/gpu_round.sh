@@ -56,7 +56,7 @@ if has ncu; then
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"pg_warp|cs_gather_tma" -s 6 -c 2 \
     -o $OUT/full_C4 -f $B --config C4 > $OUT/ncu_full_C4.log 2>&1
   $B --config C5 > $OUT/plain1_C5.log 2>&1 &&
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cs_gather_tma -s 12 -c 1 \
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cs_gather_tma -s 6 -c 1 \
     -o $OUT/full_C5 -f $B --config C5 > $OUT/ncu_full_C5.log 2>&1
 fi
 ls -la $OUT
