@@ -62,7 +62,9 @@ def config_obj(cfg, world, extra=None):
                      f"({cfg.dist}), {cfg.family} m={cfg.m} s={cfg.s}",
          "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "sketch": cfg.family,
          "parallelism": f"row-shard x{world} + allreduce[SA|g]" if world > 1 else "single GPU",
-         "l2": "inputs larger than L2 (A = %.2f GiB per step)" % (cfg.a_bytes / 2**30)}
+         "l2": ("inputs larger than L2 (A = %.2f GiB per step)" % (cfg.a_bytes / 2**30)) if cfg.a_bytes > (126 << 20)
+         else ("inputs fit in L2 (A = %.2f MiB), not flushed between steps: a latency-bound small config, "
+               "not the headline workload" % (cfg.a_bytes / 2**20))}
     if extra:
         o.update(extra)
     return o
