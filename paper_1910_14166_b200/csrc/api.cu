@@ -55,7 +55,7 @@ constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 
 enum Slot {
   S_PERM, S_HIST, S_TILES, S_GPART, S_GRAM, S_SJLT, S_CHOL, S_PACK, S_H, S_X, S_MISC, S_ERR,
-  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_PG, S_GRAMF, S_NSLOTS
+  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_PG, S_GRAMF, S_PGF, S_NSLOTS
 };
 }  // namespace
 
@@ -98,7 +98,11 @@ struct ihs_ctx_s {
     const double *Hinv = nullptr;
     cudaEvent_t done = nullptr;
     bool pending = false;
+    bool L_ready = false;  // look-ahead Gram: the PG step bound of this H is in d_L[slot]
+    int64_t L_d = 0;
   } fac[4];
+  double *d_L = nullptr;     // [4] step bounds formed beside the pass
+  int64_t pgf_warm_d = -1;   // S_PGF holds the side power iteration's vector for this d
   bool f_pending = false;  // any fac[k].pending
   int64_t pg_warm_d = -1;  // S_PG holds a power-iteration vector for this d
   struct Rec { int group; cudaEvent_t a, b; };
@@ -540,6 +544,7 @@ ihs_status factor_begin(ihs_ctx c, const double *out, ihs_ctx_s::Factor **rec) {
   }
   IHS_CUDA(cudaEventRecord(c->ev_fmain, c->stream));
   IHS_CUDA(cudaStreamWaitEvent(c->fstream, c->ev_fmain, 0));
+  slot->L_ready = false;  // (set again by a look-ahead Gram that also forms the step bound)
   *rec = slot;
   return IHS_OK;
 }
@@ -555,17 +560,45 @@ ihs_status factor_end(ihs_ctx c, const double *out, ihs_ctx_s::Factor *slot) {
 // Look-ahead Gram for the l1 / LASSO updates: H = scale^2 SA^T SA on the factor
 // stream with a Gram plan for a few SMs (it runs beside the previous update's
 // PG cluster; the update that reads H joins it).
+ihs_inner_cfg default_inner();
+
 ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {
   if (m < 1 || d < 1) return IHS_ERR_INVALID_ARGUMENT;
   static const int side_sms = getenv("IHS_LOOKAHEAD_SMS") ? std::max(1, atoi(getenv("IHS_LOOKAHEAD_SMS"))) : 16;
   GramPlan p = gram_plan(m, d, std::min(side_sms, c->num_sms));
   double *part;
   IHS_TRY(scratch(c, S_GRAMF, p.partial_bytes(), &part));  // (before factor_begin: a regrowth joins)
+  static const bool side_power = !getenv("IHS_LOOKAHEAD_POWER") || atoi(getenv("IHS_LOOKAHEAD_POWER")) != 0;
+  const bool power = side_power && pg_supported(d);
+  double *ev = nullptr;
+  if (power) {  // allocated on the ctx stream before the factor stream's dependency is recorded
+    if (!c->d_L) IHS_CUDA(cudaMalloc(&c->d_L, 4 * sizeof(double)));
+    if (c->cap[S_PGF] < std::max<size_t>(pg_scratch_bytes(d), 256)) c->pgf_warm_d = -1;
+    IHS_TRY(scratch(c, S_PGF, pg_scratch_bytes(d), &ev));
+  }
   ihs_ctx_s::Factor *slot;
   IHS_TRY(factor_begin(c, H, &slot));
   {
     Prof pr(c, IHS_K_FACTOR, c->fstream);
     IHS_CUDA(launch_gram(p, SA, scale, part, H, c->fstream, lc_of(c)));
+  }
+  // ... and the PG step bound L = 1.05 lambda_max(H) (R10's power iteration,
+  // warm-started along the chain of look-ahead Grams exactly as the update
+  // would have), so the update of this H skips its power steps
+  slot->L_ready = false;
+  if (power) {
+    const ihs_inner_cfg k = default_inner();
+    Prof pr(c, IHS_K_FACTOR, c->fstream);
+    const cudaError_t e = launch_l1ball_update(H, nullptr, d, nullptr, 0.0, 0, k.power_iters, k.inner_tol,
+                                               k.lip_safety, nullptr, nullptr, ev, c->d_status, c->fstream, lc_of(c),
+                                               c->pgf_warm_d == d, 0, nullptr, c->d_L + (slot - c->fac));
+    if (e == cudaSuccess) {
+      c->pgf_warm_d = d;
+      slot->L_ready = true;
+      slot->L_d = d;
+    } else {
+      cudaGetLastError();
+    }
   }
   return factor_end(c, H, slot);
 }
@@ -617,6 +650,13 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
     return IHS_ERR_INVALID_ARGUMENT;
   if (!pg_supported(d) || (prox && !lasso_supported(d))) return IHS_ERR_UNSUPPORTED;
   IHS_TRY(wait_factor(c, H));  // a look-ahead Gram that writes H
+  const double *L_in = nullptr;  // ... and its step bound, formed beside the pass
+  for (auto &f : c->fac)
+    if (f.L_ready && f.Hinv == H) {
+      const ihs_inner_cfg k0 = default_inner();
+      if (f.L_d == d && k.power_iters == k0.power_iters && k.lip_safety == k0.lip_safety) L_in = c->d_L + (&f - c->fac);
+      f.L_ready = false;
+    }
   // warm-started power iteration across calls with the same d (IHS_PG_WARM=0 off)
   static const bool warm_env = !getenv("IHS_PG_WARM") || std::strcmp(getenv("IHS_PG_WARM"), "0") != 0;
   double *ev = nullptr;
@@ -625,8 +665,8 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
   const bool warm = warm_env && c->pg_warm_d == d;
   Prof pr(c, IHS_K_PG);
   IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.inner_tol, k.lip_safety, xn, inner,
-                                ev, c->d_status, c->stream, lc_of(c), warm, prox));
-  if (warm_env) c->pg_warm_d = d;
+                                ev, c->d_status, c->stream, lc_of(c), warm, prox, L_in, nullptr));
+  if (warm_env && !L_in) c->pg_warm_d = d;
   return IHS_OK;
 }
 
@@ -952,6 +992,7 @@ ihs_status ihs_ctx_destroy(ihs_ctx c) {
   for (int s = 0; s < S_NSLOTS; ++s)
     if (c->slot[s]) cudaFree(c->slot[s]);
   if (c->d_status) cudaFree(c->d_status);
+  if (c->d_L) cudaFree(c->d_L);
   if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   delete c;

@@ -165,7 +165,10 @@ int pg_cluster_size(int64_t d);
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
                                  int max_inner, int power_iters, double tol, double safety, double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
-                                 LaunchCounter lc, bool warm_start = false, int prox = 0);
+                                 LaunchCounter lc, bool warm_start = false, int prox = 0,
+                                 const double *L_in = nullptr, double *L_out = nullptr);
+// (L_in: use this step bound, no power iteration; L_out: power iteration only,
+// the bound written there -- the look-ahead, api.cu; warp kernel only)
 
 // ---- a7 error norms ----------------------------------------------------------
 cudaError_t launch_pred_err2(int layout, int64_t n, int64_t d, const double *values, const int64_t *row_ptr,

@@ -320,7 +320,8 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
                                                       int d, const double *__restrict__ x, double radius,
                                                       int max_inner, int power_iters, double tol, double safety,
                                                       double *x_next, int32_t *inner_iters, int *status, int accel,
-                                                      double *evec, int warm, int prox) {
+                                                      double *evec, int warm, int prox, const double *L_in,
+                                                      double *L_out) {
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   const int cs = (int)cluster.num_blocks();
@@ -333,12 +334,12 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
   double *zb = gs + R;               // 2 x d : z (or H v), double-buffered by step parity
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   load_rows(Hs, H + (int64_t)r0 * d, (int64_t)(r1 - r0) * d, tid, kCT);
-  for (int i = tid; i < r1 - r0; i += kCT) gs[i] = g[r0 + i];
+  for (int i = tid; i < r1 - r0; i += kCT) gs[i] = g ? g[r0 + i] : 0.0;
   double xv[K], yv[K], vv[K], wv[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int q = lane + 32 * k;
-    xv[k] = q < d ? x[q] : 0.0;
+    xv[k] = (q < d && x) ? x[q] : 0.0;
     yv[k] = xv[k];
     vv[k] = yv[k];
     // power iteration start: 1/sqrt(d) (reading R10), or, warm, the previous
@@ -384,8 +385,10 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
     }
     cluster.sync();
   };
+  // L_in: the step bound was formed beside the previous pass (look-ahead,
+  // api.cu) -- no power iteration here
   double lam = 0.0;
-  for (int it = 0; it < power_iters; ++it) {
+  for (int it = 0; !L_in && it < power_iters; ++it) {
     gemv_bcast(false, 1.0);
     const double *hv = zb + par * d;
     double hvv[K];
@@ -403,13 +406,18 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
     for (int k = 0; k < K; ++k) wv[k] = hvv[k] / lam;
     par ^= 1;
   }
-  const double L = (lam > 0.0) ? safety * lam : 1.0;
-  if (evec && rank == 0 && warp == 0 && lam > 0.0) {
+  const double L = L_in ? *L_in : (lam > 0.0) ? safety * lam : 1.0;
+  if (!L_in && evec && rank == 0 && warp == 0 && lam > 0.0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int q = lane + 32 * k;
       if (q < d) evec[q] = wv[k];
     }
+  }
+  if (L_out) {  // power-only launch (the look-ahead's step bound for the next update)
+    if (rank == 0 && tid == 0) *L_out = L;
+    cluster.sync();
+    return;
   }
   int kk = 0;
   bool converged = false;
@@ -537,7 +545,7 @@ size_t pg_scratch_bytes(int64_t d) { return (size_t)d * 8; }
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
                                  int max_inner, int power_iters, double tol, double safety, double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
-                                 LaunchCounter lc, bool warm_start, int prox) {
+                                 LaunchCounter lc, bool warm_start, int prox, const double *L_in, double *L_out) {
   static const bool use_cluster = !getenv("IHS_PG_SINGLE");
   static const bool warp_version = !getenv("IHS_PG_CTA");
   const int cs = use_cluster ? pg_cluster_size(d) : 0;
@@ -565,7 +573,7 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     cfg.numAttrs = 1;
     lc.add();
     if (!wv) {
-      if (prox) return cudaErrorNotSupported;
+      if (prox || L_out) return cudaErrorNotSupported;
       return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
                                 x_next, inner_iters, status);
     }
@@ -578,8 +586,9 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     const bool warm_ok = warm_start && scratch;
     const int piters = warm_ok ? std::min(power_iters, 12) : power_iters;
     return cudaLaunchKernelEx(&cfg, wkern, H, g, (int)d, x, radius, max_inner, piters, tol, safety, x_next,
-                              inner_iters, status, accel, scratch, warm_ok ? 1 : 0, prox);
+                              inner_iters, status, accel, scratch, warm_ok ? 1 : 0, prox, L_in, L_out);
   }
+  if (L_out) return cudaErrorNotSupported;  // power-only launches: the warp kernel only
   if (prox) return cudaErrorNotSupported;
   const size_t smem = (size_t)5 * d * 8;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
