@@ -83,9 +83,9 @@ def lookahead_default(A, d: int, spec: P.Spec, constraint: str = "ols") -> bool:
     d <= 128); IHS_LOOKAHEAD=0/1 overrides (the rule of ihs_solve_*, api.cu)."""
     import os
     env = os.environ.get("IHS_LOOKAHEAD")
+    if env is not None:  # forced: any matrix (OLS with d > 128 or CSR: the Gram-only form)
+        return d >= 1 and env != "0"
     ok = isinstance(A, P.Dense) and d >= 1 and (d <= 128 or constraint != "ols")
-    if env is not None:
-        return ok and env != "0"
     return ok and spec.s == 1 and A.n * d >= (1 << 27)
 
 
@@ -128,7 +128,11 @@ class ShardedIHS:
         self.inner = torch.zeros(1, dtype=torch.int32, device=dev)
         if lookahead is None:
             lookahead = lookahead_default(A, d, spec, constraint)
-        need = "ols_factor" if constraint == "ols" else "gram_lookahead"
+        # Gram-only look-ahead (H_{t+1} formed ahead, the update then solves with
+        # H_t): the l1 / LASSO updates, and OLS where the fused H^{-1} factor does
+        # not apply (d > 128 or a CSR matrix: the conjugate-gradient update)
+        self.la_gram_only = constraint != "ols" or d > 128 or not isinstance(A, P.Dense)
+        need = "gram_lookahead" if self.la_gram_only else "ols_factor"
         self.lookahead = bool(lookahead) and hasattr(self.ops, need)
         self._la_t = None  # iteration whose H^{-1} is in self.Hinv[self._la_cur]
         if self.lookahead:
@@ -144,10 +148,10 @@ class ShardedIHS:
         pk = self.packs[0]
         self.ops.sketch(self.A, self.spec, t, pk[: m * d].view(m, d))
         self.allreduce(pk[: m * d])
-        if self.constraint == "ols":
-            self.ops.ols_factor(pk[: m * d].view(m, d), self.Hinv[0])
-        else:
+        if self.la_gram_only:
             self.ops.gram_lookahead(pk[: m * d].view(m, d), self.Hinv[0])
+        else:
+            self.ops.ols_factor(pk[: m * d].view(m, d), self.Hinv[0])
         self._la_t, self._la_cur = t, 0
 
     def step(self, t: int, x: torch.Tensor, xn: torch.Tensor) -> torch.Tensor:
@@ -158,12 +162,14 @@ class ShardedIHS:
             cur, nxt = self._la_cur, 1 - self._la_cur
             pk = self.packs[nxt]
             SAn, gn = pk[: m * d].view(m, d), pk[m * d:]
-            if self.constraint != "ols":  # l1 / LASSO: only the Gram looks ahead
+            if self.la_gram_only:  # only the Gram looks ahead
                 self.ops.sketch_grad(self.A, self.spec, t + 1, self.b, x, SAn, gn)
                 self.allreduce(pk)
-                self.ops.gram_lookahead(SAn, self.Hinv[nxt])  # beside this update's PG
+                self.ops.gram_lookahead(SAn, self.Hinv[nxt])  # beside this update
                 H = self.Hinv[cur]
-                if self.constraint == "lasso":
+                if self.constraint == "ols":
+                    self.ops.ols(H, gn, x, xn)
+                elif self.constraint == "lasso":
                     self.ops.lasso(H, gn, x, self.radius, self.cfg, xn, self.inner)
                 else:
                     self.ops.l1(H, gn, x, self.radius, self.cfg, xn, self.inner)
