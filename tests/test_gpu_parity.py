@@ -288,6 +288,38 @@ def test_sharded_lookahead_pg_matches_oracle(P, oracle_mod, constraint):
     assert ctx.status() == P.OK
 
 
+@pytest.mark.parametrize("kind", ["csr", "dense_d200"])
+def test_sharded_lookahead_gram_only_ols(P, oracle_mod, kind):
+    """The Gram-only look-ahead for OLS (CSR, or d > 128: H_{t+1} ahead, the
+    conjugate-gradient / Cholesky update with H_t) reproduces the oracle."""
+    from paper_1910_14166_b200.dist import CudaOps, ShardedIHS
+    rng = np.random.default_rng(9)
+    T, m = 4, 2048
+    if kind == "csr":
+        n, d = 40_000, 200
+        rp, cl, vl = csr_case(n, d, 0.05, 4)
+        A_dev = P.Csr(torch.from_numpy(rp).to(DEV), torch.from_numpy(cl).to(DEV), torch.from_numpy(vl).to(DEV), d)
+        import scipy.sparse as sp
+        Ad = sp.csr_matrix((vl, cl, rp), shape=(n, d)).toarray()
+        okw = dict(csr=(rp, cl, vl), d=d)
+        s = 4
+    else:
+        n, d = 20_000, 200
+        Ad = rng.standard_normal((n, d))
+        A_dev = P.Dense(torch.from_numpy(Ad).to(DEV))
+        okw = dict(A=Ad)
+        s = 1
+    b = Ad @ rng.standard_normal(d) + rng.standard_normal(n)
+    ctx = P.Context(0)
+    S = ShardedIHS(A_dev, torch.from_numpy(b).to(DEV), P.Spec(m=m, s=s), ops=CudaOps(ctx), lookahead=True)
+    assert S.lookahead and S.la_gram_only
+    xh = S.solve(T, iter0=2).cpu().numpy()
+    xo, _ = oracle_mod.ihs_solve(b=b, m=m, s=s, T=T, iter0=2, **okw)
+    for t in range(1, T + 1):
+        assert oracle_mod.pred_rel_err(xh[t], xo[t], Ad) <= 1e-9, t
+    assert ctx.status() == P.OK
+
+
 def test_gram_lookahead(P, oracle_mod):
     rng = np.random.default_rng(5)
     SA = rng.standard_normal((2048, 256))
