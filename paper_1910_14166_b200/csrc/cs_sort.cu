@@ -161,6 +161,7 @@ __device__ __forceinline__ void cs_scatter_chunk(
   int32_t *my = wcnt + (size_t)warp * m;
   const int nbits = 32 - __clz((int)max(m - 1, 1u));  // bucket < 2^nbits
   uint32_t bk[kMaxGroups];
+  unsigned pm[kMaxGroups];  // peer masks of phase 1, reused by phase 2
 #pragma unroll
   for (int q = 0; q < kMaxGroups; ++q) {
     const int64_t r = ws + 32 * q + lane;
@@ -173,7 +174,10 @@ __device__ __forceinline__ void cs_scatter_chunk(
       const bool valid = r < we;
       const uint32_t bb = bk[q] & 0x7fffffffu;
       const unsigned mask = peers_by_ballot(bb, nbits, valid);
+      pm[q] = mask;
       if (valid && lane == __ffs(mask) - 1) atomicAdd(&my[bb], __popc(mask));
+    } else {
+      pm[q] = 0u;
     }
   }
   __syncthreads();
@@ -197,7 +201,7 @@ __device__ __forceinline__ void cs_scatter_chunk(
       const int64_t r = ws + 32 * q + lane;
       const bool valid = r < we;
       const uint32_t bb = bk[q] & 0x7fffffffu;
-      const unsigned mask = peers_by_ballot(bb, nbits, valid);
+      const unsigned mask = pm[q];
       const int leader = __ffs(mask) - 1;
       int32_t old = 0;
       if (valid && lane == leader) old = atomicAdd(&my[bb], __popc(mask));
