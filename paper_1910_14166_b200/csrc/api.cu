@@ -1001,7 +1001,8 @@ ihs_status ihs_ctx_destroy(ihs_ctx c) {
 
 ihs_status ihs_ctx_set_stream(ihs_ctx c, void *stream) {
   if (!c) return IHS_ERR_INVALID_ARGUMENT;
-  if (c->f_pending && (cudaStream_t)stream != c->stream) join_factor(c);
+  // pending factor / side work stays pending: it is joined into whichever stream
+  // the ctx is bound to when a call needs it (wait_factor / join_side)
   c->stream = (cudaStream_t)stream;
   return IHS_OK;
 }
