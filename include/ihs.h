@@ -101,6 +101,9 @@ const char *ihs_status_string(ihs_status st);
  * legacy default stream).  One context per (device, stream); no global state. */
 ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream);
 ihs_status ihs_ctx_destroy(ihs_ctx ctx);
+/* Rebind the ctx to another stream.  Work the ctx runs on its own streams (the
+ * sort prefetch, look-ahead factors) stays pending and is joined into the stream
+ * bound when a later call needs its result. */
 ihs_status ihs_ctx_set_stream(ihs_ctx ctx, void *stream);
 /* Wait for the ctx stream; return the first asynchronous error or device-side
  * status (IHS_ERR_NOT_SPD, IHS_ERR_NOT_CONVERGED) raised since the last call,
