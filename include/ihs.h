@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define IHS_ABI_VERSION 1
+#define IHS_ABI_VERSION 2
 
 typedef enum {
     IHS_OK = 0,
@@ -73,12 +73,18 @@ typedef struct {
     int64_t nnz;
 } ihs_matrix;
 
-/* Inner projected-gradient configuration (reading R10). */
+/* Inner projected-gradient configuration (reading R10; SPEC.md:266 gives
+ * 50 power iterations and a 5000-step cap for its own CPU solver). */
 typedef struct {
-    int32_t max_inner;    /* cap on PG steps per outer iteration (default 20000) */
-    int32_t power_iters;  /* power iterations for lambda_max(H) (default 50) */
-    double inner_tol;     /* stop when ||y+ - y|| <= tol * max(1, ||y||) (default 1e-14) */
-    double lip_safety;    /* step 1/(safety * lambda_max) (default 1.05) */
+    int32_t max_inner;        /* cap on PG steps per outer iteration (default 20000) */
+    int32_t power_iters;      /* power iterations for lambda_max(H) from 1/sqrt(d): the first
+                                 update of a context for this d (default 50) */
+    double inner_tol;         /* stop when ||y+ - y|| <= tol * max(1, ||y||) (default 1e-14) */
+    double lip_safety;        /* step 1/(safety * lambda_max) (default 1.05) */
+    int32_t warm_power_iters; /* power iterations on later updates with the same d, started from
+                                 the previous update's vector (default 12; >= 1; set it to
+                                 power_iters to give every update the cold count) */
+    int32_t reserved;         /* must be 0 */
 } ihs_inner_cfg;
 
 /* Per-iteration record written by the solve calls (host memory). Times in ms
@@ -111,6 +117,23 @@ ihs_status ihs_ctx_set_stream(ihs_ctx ctx, void *stream);
 ihs_status ihs_ctx_synchronize(ihs_ctx ctx);
 /* Number of kernels this ctx has launched so far (bench evidence). */
 int64_t ihs_ctx_kernel_launches(ihs_ctx ctx);
+
+/* Per-context options (initial values from the IHS_* environment variables
+ * named in brackets, read at ihs_ctx_create).  Unknown name or out-of-range
+ * value: IHS_ERR_INVALID_ARGUMENT.
+ *   "lookahead"    -1 (default) look-ahead schedules of the solve calls by size,
+ *                  0 off, 1 whenever supported                    [IHS_LOOKAHEAD]
+ *   "sjlt_onepass" 1 (default) dense SJLT in one read of A, 0 as s sorted
+ *                  CountSketch passes (bit-identical to the oracle) [IHS_SJLT=passes]
+ *   "ols_large"    d > 160 OLS step: 1 (default) conjugate gradients, then the
+ *                  blocked Cholesky in the same launch when CG does not finish;
+ *                  0 CG only (IHS_ERR_NOT_CONVERGED at its cap); 2 the Cholesky
+ *                  only (positive definiteness certified exactly, reading R22) [IHS_OLS]
+ *   "fuse_max_d"   a4 + a6 in one cluster launch up to this d (0..128, default 64) [IHS_FUSE]
+ *   "pg_warm"      1 (default) warm-started power iteration across l1 / LASSO updates [IHS_PG_WARM]
+ *   "prefetch"     1 (default) the next iteration's sort on the side stream   [IHS_PREFETCH] */
+ihs_status ihs_ctx_set_option(ihs_ctx ctx, const char *name, int64_t value);
+ihs_status ihs_ctx_get_option(ihs_ctx ctx, const char *name, int64_t *value);
 
 /* Per-kernel timing (bench evidence): when enabled, CUDA events are recorded on
  * the ctx stream around every launch of the kernel groups below.
@@ -149,21 +172,30 @@ ihs_status ihs_allreduce_sum(ihs_ctx ctx, double *buf, int64_t count);
 ihs_status ihs_hash(ihs_ctx ctx, const ihs_sketch_spec *spec, uint64_t iter,
                     int64_t row_begin, int64_t count, int32_t *bucket, int8_t *sign);
 
-/* a2: SA = S^(iter) A_local (m x d), the local partial sketch
- * (SJLT scaled by 1/sqrt(s)). */
+/* a2: SA = S^(iter) A_local (m x d) (section 2;
+ * SJLT scaled by 1/sqrt(s)).  reduce = 0: the local partial
+ * sketch; reduce != 0: summed in place over the ctx communicator afterwards
+ * (the full S A on every rank, by linearity -- BASELINE.json north_star; the
+ * same as ihs_allreduce_sum(SA, m*d); a no-op at world size 1).
+ * Dense SJLT is deterministic but, with "sjlt_onepass", not bit-identical to
+ * the oracle's single ascending sum (within 1e-12, reading R3). */
 ihs_status ihs_sketch(ihs_ctx ctx, const ihs_matrix *A, const ihs_sketch_spec *spec,
-                      uint64_t iter, double *SA);
+                      uint64_t iter, double *SA, int reduce);
 
-/* a5: g = A_local^T (b_local - A_local x) (d), local partial. */
+/* a5: g = A_local^T (b_local - A_local x) (d) (the linear term of Eq. (2),
+ * PAPER.md:83-86); reduce as for ihs_sketch. */
 ihs_status ihs_grad(ihs_ctx ctx, const ihs_matrix *A, const double *b, const double *x,
-                    double *g);
+                    double *g, int reduce);
 
-/* a2 + a5 in one pass over A where the layout allows (dense CountSketch with
- * d <= 256, CSR); otherwise two passes.  Writes SA (m x d) and g (d); g may
- * equal SA + m*d so that [SA | g] is one packed buffer for the allreduce. */
+/* a2 + a5 (NEXT-1): one pass over A where the layout allows (dense CountSketch
+ * with even d <= 256, CSR); dense SJLT: the one-read sketch pass and the
+ * gradient stream side by side; otherwise two passes.  Writes SA (m x d) and
+ * g (d); g may equal SA + m*d so that [SA | g] is one packed buffer: with
+ * reduce != 0 and g == SA + m*d it is summed over the communicator in ONE
+ * all-reduce of m*d + d doubles (a3), otherwise SA and g separately. */
 ihs_status ihs_sketch_grad(ihs_ctx ctx, const ihs_matrix *A, const ihs_sketch_spec *spec,
                            uint64_t iter, const double *b, const double *x,
-                           double *SA, double *g);
+                           double *SA, double *g, int reduce);
 
 /* a4: H = (SA)^T SA (d x d, full symmetric), fp64 on the DMMA tensor pipe
  * (PAPER.md:95, 104-106).  `scale` multiplies every SA entry on load (1.0, or
@@ -222,12 +254,14 @@ ihs_status ihs_ols_lookahead_step(ihs_ctx ctx, const ihs_matrix *A, const ihs_sk
                                   const double *Hinv, double *SA_next, double *Hinv_next,
                                   double *g, double *x_next);
 
-/* a6, OLS: x_next = x + H^{-1} g (Eq. (2) with C = R^d).
- * d <= 160: blocked Cholesky in one CTA; d > 160: Jacobi-preconditioned
- * conjugate gradients to a relative residual of 1e-15 in one cooperative
- * launch (reading R22; IHS_OLS=chol selects the multi-CTA Cholesky).  H not
- * positive definite sets IHS_ERR_NOT_SPD (device status) and writes
- * x_next = x.  H is not modified.  x_next may alias x. */
+/* a6, OLS: x_next = x + H^{-1} g (Eq. (2) with C = R^d; the
+ * QP "solved exactly").  d <= 160: blocked Cholesky in one
+ * CTA; d > 160: one cooperative launch per the "ols_large" option (default:
+ * Jacobi-preconditioned CG to a relative residual of 1e-15, falling back to
+ * the blocked Cholesky in the same launch when CG hits its cap min(2000, 4d)
+ * or meets p.Hp <= 0; reading R22).  H not positive definite (a Cholesky pivot
+ * <= 0) sets IHS_ERR_NOT_SPD (device status) and writes x_next = x (reading
+ * R13).  H is not modified.  x_next may alias x. */
 ihs_status ihs_ols_update(ihs_ctx ctx, const double *H, const double *g, int64_t d,
                           const double *x, double *x_next);
 
@@ -250,25 +284,38 @@ ihs_status ihs_lasso_update(ihs_ctx ctx, const double *H, const double *g, int64
                             const double *x, double lambda, const ihs_inner_cfg *cfg,
                             double *x_next, int32_t *inner_iters);
 
-/* a1-a7: n_iters IHS steps from x0 (NULL = 0), hash iterations iter0.. .
+/* a1-a7, Iterative Hessian Sketch (Eq. (2), section 1; a fresh
+ * sketch S^{t+1} per iteration, the exact gradient A^T(b - A x^t)):
+ * x^{t+1} = argmin_{x in C} 1/2 ||S^{t+1} A (x - x^t)||^2 - <A^T(b - A x^t), x - x^t>,
+ * n_iters steps from x0 (NULL = 0, reading R11), hash iterations iter0.. .
+ * ihs_solve_ols: C = R^d (the ihs_ols_update step).
  * A/b/x0/x/x_hist may be HOST or DEVICE pointers (detected per pointer); host
  * inputs are copied in and results copied out inside the call.  x_hist
  * (optional, (n_iters+1) x d) receives x^0..x^T.  trace (host, optional)
- * receives n_iters records and makes the call synchronous.  With a
- * communicator set, [SA | g] is summed across ranks every iteration and every
- * rank computes the same x.  Returns after the last step is enqueued (or
- * completed when any host pointer or trace is involved). */
+ * receives n_iters records and makes the call synchronous (plain schedule).
+ * With a communicator set, [SA | g] is summed across ranks every iteration and
+ * every rank computes the same x; the schedule (plain or look-ahead, option
+ * "lookahead") is decided from ceil(n_global / world) rows so that all ranks
+ * take the same one.  Returns after the last step is enqueued (or completed
+ * when any host pointer or trace is involved).  Errors: argument errors
+ * synchronously; IHS_ERR_NOT_SPD / IHS_ERR_NOT_CONVERGED of the inner steps at
+ * the next ihs_ctx_synchronize (or returned, when the call is synchronous). */
 ihs_status ihs_solve_ols(ihs_ctx ctx, const ihs_matrix *A, const double *b,
                          const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0,
                          const double *x0, double *x, double *x_hist,
                          ihs_iter_record *trace);
 
+/* The same loop with C = {||x||_1 <= radius} (the LASSO constraint of the
+ * paper's Eq. (1) setting; BASELINE.json configs[3]), each QP
+ * solved by ihs_l1ball_update with cfg (NULL = defaults). */
 ihs_status ihs_solve_l1ball(ihs_ctx ctx, const ihs_matrix *A, const double *b, double radius,
                             const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0,
                             const ihs_inner_cfg *cfg, const double *x0, double *x,
                             double *x_hist, ihs_iter_record *trace);
 
-/* NEXT-2: the same loop for the penalised LASSO (ihs_lasso_update inner step). */
+/* NEXT-2: the same loop for the penalised LASSO 1/2||Ax - b||^2 + lambda ||x||_1
+ * (section 3; the penalty kept in every step, reading R23),
+ * each QP solved by ihs_lasso_update. */
 ihs_status ihs_solve_lasso(ihs_ctx ctx, const ihs_matrix *A, const double *b, double lambda,
                            const ihs_sketch_spec *spec, int32_t n_iters, uint64_t iter0,
                            const ihs_inner_cfg *cfg, const double *x0, double *x,

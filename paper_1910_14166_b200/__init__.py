@@ -23,7 +23,7 @@ import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libihs.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 OK, ERR_INVALID_ARGUMENT, ERR_DIMENSION_MISMATCH, ERR_NOT_SPD, ERR_NOT_CONVERGED, ERR_CUDA, ERR_COMM, \
     ERR_OUT_OF_MEMORY, ERR_UNSUPPORTED = range(9)
@@ -52,7 +52,7 @@ class Matrix(C.Structure):
 
 class InnerCfg(C.Structure):
     _fields_ = [("max_inner", C.c_int32), ("power_iters", C.c_int32), ("inner_tol", C.c_double),
-                ("lip_safety", C.c_double)]
+                ("lip_safety", C.c_double), ("warm_power_iters", C.c_int32), ("reserved", C.c_int32)]
 
 
 class IterRecord(C.Structure):
@@ -68,6 +68,8 @@ _EXPORTS = {
     "ihs_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "ihs_ctx_synchronize": (C.c_int, [C.c_void_p]),
     "ihs_ctx_kernel_launches": (C.c_int64, [C.c_void_p]),
+    "ihs_ctx_set_option": (C.c_int, [C.c_void_p, C.c_char_p, C.c_int64]),
+    "ihs_ctx_get_option": (C.c_int, [C.c_void_p, C.c_char_p, C.POINTER(C.c_int64)]),
     "ihs_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int]),
     "ihs_ctx_profile": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "ihs_ctx_profile_reset": (C.c_int, [C.c_void_p]),
@@ -76,10 +78,11 @@ _EXPORTS = {
     "ihs_allreduce_sum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
     "ihs_hash": (C.c_int, [C.c_void_p, C.POINTER(SketchSpec), C.c_uint64, C.c_int64, C.c_int64, C.c_void_p,
                            C.c_void_p]),
-    "ihs_sketch": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.POINTER(SketchSpec), C.c_uint64, C.c_void_p]),
-    "ihs_grad": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ihs_sketch": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.POINTER(SketchSpec), C.c_uint64, C.c_void_p,
+                             C.c_int]),
+    "ihs_grad": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "ihs_sketch_grad": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.POINTER(SketchSpec), C.c_uint64, C.c_void_p,
-                                  C.c_void_p, C.c_void_p, C.c_void_p]),
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "ihs_gram": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p]),
     "ihs_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "ihs_gram_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
@@ -210,6 +213,18 @@ class Context:
             stream = torch.cuda.current_stream().cuda_stream
         _check(lib().ihs_ctx_create(C.byref(h), self.device, C.c_void_p(stream)), "ihs_ctx_create")
         self.h = h
+        # Tensors read asynchronously on the library's factor stream (the SA of
+        # ihs_ols_factor / ihs_gram_lookahead), kept alive until the call that
+        # joins their result (keyed by the output's address) or synchronize():
+        # torch's caching allocator does not see that stream.
+        self._keep: dict[int, tuple] = {}
+
+    def _hold(self, out: torch.Tensor, *tensors):
+        self._keep[out.data_ptr()] = (out,) + tensors
+
+    def _release(self, out) -> None:
+        if out is not None:
+            self._keep.pop(out.data_ptr() if isinstance(out, torch.Tensor) else int(out), None)
 
     def _bind(self):
         stream = torch.cuda.current_stream(self.device).cuda_stream
@@ -217,15 +232,28 @@ class Context:
         return self.h
 
     def synchronize(self):
-        _check(lib().ihs_ctx_synchronize(self._bind()), "ihs_ctx_synchronize")
+        st = lib().ihs_ctx_synchronize(self._bind())
+        self._keep.clear()
+        _check(st, "ihs_ctx_synchronize")
 
     def status(self) -> int:
         """Synchronise and return (not raise) the pending device status."""
-        return lib().ihs_ctx_synchronize(self._bind())
+        st = lib().ihs_ctx_synchronize(self._bind())
+        self._keep.clear()
+        return st
 
     @property
     def kernel_launches(self) -> int:
         return int(lib().ihs_ctx_kernel_launches(self.h))
+
+    def set_option(self, name: str, value: int):
+        """Per-context option (ihs.h: lookahead, sjlt_onepass, ols_large, fuse_max_d, pg_warm, prefetch)."""
+        _check(lib().ihs_ctx_set_option(self.h, name.encode(), int(value)), f"ihs_ctx_set_option({name})")
+
+    def get_option(self, name: str) -> int:
+        v = C.c_int64()
+        _check(lib().ihs_ctx_get_option(self.h, name.encode(), C.byref(v)), f"ihs_ctx_get_option({name})")
+        return v.value
 
     def set_profiling(self, enable: bool):
         _check(lib().ihs_ctx_set_profiling(self.h, int(enable)), "ihs_ctx_set_profiling")
@@ -288,25 +316,30 @@ def ihs_hash(spec: Spec, it: int, row_begin: int, count: int, ctx: Context | Non
 
 
 # ------------------------------------------------------------------ a2 / a5
-def ihs_sketch(A, spec: Spec, it: int, out: torch.Tensor | None = None, ctx: Context | None = None):
+def ihs_sketch(A, spec: Spec, it: int, out: torch.Tensor | None = None, ctx: Context | None = None,
+               reduce: bool = False):
+    """S^it A (m x d); reduce=True sums it over the context's communicator (ihs.h)."""
     A = as_matrix(A)
     ctx = ctx or default_context(A.device)
     SA = out if out is not None else _f64((spec.m, A.d), A.device)
     mc, sp = A.c(), spec.c()
-    _check(lib().ihs_sketch(ctx._bind(), C.byref(mc), C.byref(sp), it, _p(SA)), "ihs_sketch")
+    _check(lib().ihs_sketch(ctx._bind(), C.byref(mc), C.byref(sp), it, _p(SA), int(reduce)), "ihs_sketch")
     return SA
 
 
-def ihs_grad(A, b: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None, ctx: Context | None = None):
+def ihs_grad(A, b: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None, ctx: Context | None = None,
+             reduce: bool = False):
+    """A^T (b - A x); reduce=True sums it over the context's communicator."""
     A = as_matrix(A)
     ctx = ctx or default_context(A.device)
     g = out if out is not None else _f64(A.d, A.device)
     mc = A.c()
-    _check(lib().ihs_grad(ctx._bind(), C.byref(mc), _p(b), _p(x), _p(g)), "ihs_grad")
+    _check(lib().ihs_grad(ctx._bind(), C.byref(mc), _p(b), _p(x), _p(g), int(reduce)), "ihs_grad")
     return g
 
 
-def ihs_sketch_grad(A, spec: Spec, it: int, b, x, SA=None, g=None, ctx: Context | None = None):
+def ihs_sketch_grad(A, spec: Spec, it: int, b, x, SA=None, g=None, ctx: Context | None = None,
+                    reduce: bool = False):
     """Packed [SA | g] when SA/g are None: returns (pack, SA view, g view)."""
     A = as_matrix(A)
     ctx = ctx or default_context(A.device)
@@ -316,8 +349,8 @@ def ihs_sketch_grad(A, spec: Spec, it: int, b, x, SA=None, g=None, ctx: Context 
         SA = pack[: spec.m * A.d].view(spec.m, A.d)
         g = pack[spec.m * A.d:]
     mc, sp = A.c(), spec.c()
-    _check(lib().ihs_sketch_grad(ctx._bind(), C.byref(mc), C.byref(sp), it, _p(b), _p(x), _p(SA), _p(g)),
-           "ihs_sketch_grad")
+    _check(lib().ihs_sketch_grad(ctx._bind(), C.byref(mc), C.byref(sp), it, _p(b), _p(x), _p(SA), _p(g),
+                                 int(reduce)), "ihs_sketch_grad")
     return pack, SA, g
 
 
@@ -346,6 +379,7 @@ def ihs_ols_update(H, g, x, out=None, ctx: Context | None = None):
     ctx = ctx or default_context(H.device)
     xn = out if out is not None else torch.empty_like(x)
     _check(lib().ihs_ols_update(ctx._bind(), _p(H), _p(g), x.numel(), _p(x), _p(xn)), "ihs_ols_update")
+    ctx._release(H)
     return xn
 
 
@@ -357,6 +391,7 @@ def ihs_ols_factor(SA: torch.Tensor, scale: float = 1.0, out=None, ctx: Context 
     m, d = SA.shape
     Hinv = out if out is not None else _f64((d, d), SA.device)
     _check(lib().ihs_ols_factor(ctx._bind(), _p(SA), m, d, float(scale), _p(Hinv)), "ihs_ols_factor")
+    ctx._hold(Hinv, SA)
     return Hinv
 
 
@@ -367,6 +402,7 @@ def ihs_gram_lookahead(SA: torch.Tensor, scale: float = 1.0, out=None, ctx: Cont
     m, d = SA.shape
     H = out if out is not None else _f64((d, d), SA.device)
     _check(lib().ihs_gram_lookahead(ctx._bind(), _p(SA), m, d, float(scale), _p(H)), "ihs_gram_lookahead")
+    ctx._hold(H, SA)
     return H
 
 
@@ -375,6 +411,7 @@ def ihs_ols_apply(Hinv, g, x, out=None, ctx: Context | None = None):
     ctx = ctx or default_context(Hinv.device)
     xn = out if out is not None else torch.empty_like(x)
     _check(lib().ihs_ols_apply(ctx._bind(), _p(Hinv), _p(g), x.numel(), _p(x), _p(xn)), "ihs_ols_apply")
+    ctx._release(Hinv)
     return xn
 
 
@@ -390,11 +427,14 @@ def ihs_ols_lookahead_step(A, spec: Spec, it_next: int, b, x, Hinv, SA_next=None
     mc, sp = A.c(), spec.c()
     _check(lib().ihs_ols_lookahead_step(ctx._bind(), C.byref(mc), C.byref(sp), it_next, _p(b), _p(x), _p(Hinv),
                                         _p(SA_next), _p(Hinv_next), _p(g), _p(xn)), "ihs_ols_lookahead_step")
+    ctx._release(Hinv)
+    if Hinv_next is not None:
+        ctx._hold(Hinv_next, SA_next)
     return xn, g
 
 
-def inner_cfg(max_inner=20000, power_iters=50, inner_tol=1e-14, lip_safety=1.05) -> InnerCfg:
-    return InnerCfg(max_inner, power_iters, inner_tol, lip_safety)
+def inner_cfg(max_inner=20000, power_iters=50, inner_tol=1e-14, lip_safety=1.05, warm_power_iters=12) -> InnerCfg:
+    return InnerCfg(max_inner, power_iters, inner_tol, lip_safety, warm_power_iters, 0)
 
 
 def ihs_l1ball_update(H, g, x, radius, cfg: InnerCfg | None = None, out=None, inner=None,
@@ -404,6 +444,7 @@ def ihs_l1ball_update(H, g, x, radius, cfg: InnerCfg | None = None, out=None, in
     cfg = cfg or inner_cfg()
     _check(lib().ihs_l1ball_update(ctx._bind(), _p(H), _p(g), x.numel(), _p(x), float(radius), C.byref(cfg),
                                    _p(xn), _p(inner)), "ihs_l1ball_update")
+    ctx._release(H)
     return xn
 
 
@@ -415,6 +456,7 @@ def ihs_lasso_update(H, g, x, lam, cfg: InnerCfg | None = None, out=None, inner=
     cfg = cfg or inner_cfg()
     _check(lib().ihs_lasso_update(ctx._bind(), _p(H), _p(g), x.numel(), _p(x), float(lam), C.byref(cfg),
                                   _p(xn), _p(inner)), "ihs_lasso_update")
+    ctx._release(H)
     return xn
 
 

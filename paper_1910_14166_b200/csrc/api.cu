@@ -55,7 +55,7 @@ constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 
 enum Slot {
   S_PERM, S_HIST, S_TILES, S_GPART, S_GRAM, S_SJLT, S_CHOL, S_PACK, S_H, S_X, S_MISC, S_ERR,
-  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_PG, S_GRAMF, S_PGF, S_NSLOTS
+  S_A, S_RP, S_COL, S_B, S_XH, S_X0, S_PERM2, S_HIST2, S_TILES2, S_PG, S_GRAMF, S_PGF, S_LISTS, S_ROWS, S_NSLOTS
 };
 }  // namespace
 
@@ -72,7 +72,13 @@ struct ihs_ctx_s {
   ihs_status sticky = IHS_OK;
   // profiling: (group, start, stop) per timed launch; events reused after reset
   bool profiling = false;
-  int gather = 1;  // CountSketch gather: 0 = register-staged LDG, 1 = TMA bulk, 2 = cp.async ring (IHS_GATHER)
+  // Options (ihs_ctx_set_option; initial values from the IHS_* environment at
+  // ihs_ctx_create).  Per context, so alternatives can be compared in one process.
+  int sjlt_onepass = 1;  // dense SJLT: 1 = one read of A (sjlt_onepass.cu), 0 = s sorted CountSketch passes
+  int lookahead = -1;    // look-ahead schedules: -1 = by size (use_lookahead), 0 = off, 1 = whenever supported
+  int ols_large = 1;     // d > 160 OLS: 0 = CG only, 1 = CG + Cholesky fallback, 2 = Cholesky only
+  int fuse_max_d = 64;   // a4 + a6 in one cluster launch up to this d (<= 128)
+  int pg_warm = 1;       // warm-started power iteration across l1 / LASSO updates
   // Speculative sort of the NEXT iteration's buckets on a side stream: the
   // hash (hence the sort) depends only on (seed, iteration, row), not on x, so
   // after the gathers of iteration t the sort for t + 1 runs beside the
@@ -80,6 +86,7 @@ struct ihs_ctx_s {
   bool prefetch = true;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_side = nullptr, ev_main = nullptr;
+  cudaEvent_t ev_switch = nullptr;  // orders a newly bound stream after the old one
   bool side_pending = false;  // side work not yet waited on by the main stream
   struct SortTag {
     bool valid = false;
@@ -266,6 +273,19 @@ ihs_status ols_factor_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, do
 ihs_status wait_factor(ihs_ctx c, const double *Hinv);
 ihs_status ols_apply_impl(ihs_ctx c, const double *Hinv, const double *g, int64_t d, const double *x, double *xn);
 
+// The side stream (sort prefetch, SJLT lists), created on first use at low
+// priority: its CTAs take the slots the HBM-bound passes leave.
+ihs_status ensure_side(ihs_ctx c) {
+  if (!c->side) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    IHS_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, lo));
+    IHS_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
+    IHS_CUDA(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
+  }
+  return IHS_OK;
+}
+
 ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter,
                             const double *b, const double *x, double *SA, double *g, const LookStep *ls = nullptr) {
   const uint64_t key = iter_key(spec->seed, iter);
@@ -291,11 +311,53 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
   // plus a separate gradient pass), IHS_SJLT=tile the older per-CTA tile
   // kernel; both measured slower on B200.
   const int64_t M = m / s;
-  static const char *sjlt_env = getenv("IHS_SJLT");
-  static const int sjlt_mode = !sjlt_env ? 1 : !std::strcmp(sjlt_env, "stream") ? 0 : !std::strcmp(sjlt_env, "tile") ? 2 : 1;
-  SjltPlan sp;
-  const bool use_stream = s > 1 && sjlt_mode == 0 && sjlt_stream_plan(n, d, m, s, c->num_sms, sp);
-  const bool use_sort = cs_sort_supported(M) && !use_stream && !(s > 1 && sjlt_mode == 2);
+  SjltOnepassPlan op;
+  if (SA && s > 1 && c->sjlt_onepass && n > 0 && sjlt_onepass_plan(n, d, m, s, c->num_sms, A->values, op)) {
+    // One read of A for S A (sjlt_onepass.cu): the per-chunk bucket lists
+    // (a1) on the side stream, beside the gradient pass (a5, HBM-bound) on the
+    // ctx stream when asked for; then the column-slice sketch pass.  (The
+    // gradient beside the sketch pass instead, in 4-warp CTAs that fit next to
+    // it, measured slower: both stream through the L1/shared data pipe the
+    // sketch is bound by -- C5 28.2 + 0 vs 21.6 + 4.3 ms.)
+    join_side(c);
+    join_factor(c);
+    uint16_t *lists;
+    double *part;
+    IHS_TRY(scratch(c, S_LISTS, op.lists_bytes, &lists));
+    IHS_TRY(scratch(c, S_SJLT, op.partial_bytes, &part));
+    IHS_TRY(ensure_side(c));
+    c->pre.valid = false;
+    IHS_CUDA(cudaEventRecord(c->ev_main, st));
+    IHS_CUDA(cudaStreamWaitEvent(c->side, c->ev_main, 0));
+    {
+      Prof pr(c, IHS_K_SORT, c->side);
+      IHS_CUDA(launch_sjlt_lists(op, key, A->row_offset, lists, c->side, lc_of(c)));
+    }
+    IHS_CUDA(cudaEventRecord(c->ev_side, c->side));
+    c->side_pending = true;
+    const int64_t nbg = grad_dense_blocks(n, d, c->num_sms);
+    double *gpart = nullptr;
+    if (g) {
+      if (d > 1024) return IHS_ERR_UNSUPPORTED;
+      IHS_TRY(scratch(c, S_GPART, ((size_t)nbg * d + reduce_rows_tmp(nbg, d)) * 8, &gpart));
+      Prof pr(c, IHS_K_GRAD);
+      IHS_CUDA(launch_grad_dense(A->values, n, d, b, x, gpart, nbg, st, lc_of(c)));
+    }
+    join_side(c);
+    {
+      Prof pr(c, IHS_K_SJLT);
+      IHS_CUDA(launch_sjlt_onepass(op, A->values, lists, part, SA, spec_scale(spec), st, lc_of(c)));
+    }
+    if (g) {
+      if (ls && ls->Hinv_next) IHS_TRY(ols_factor_impl(c, SA, m, d, 1.0, ls->Hinv_next));
+      if (ls) IHS_TRY(wait_factor(c, ls->Hinv));
+      Prof pr(c, ls ? IHS_K_APPLY : IHS_K_REDUCE);
+      IHS_CUDA(launch_reduce_rows(gpart, nbg, d, g, gpart + nbg * d, reduce_counter(c), st, lc_of(c),
+                                  ls ? ls->Hinv : nullptr, ls ? ls->x : nullptr, ls ? ls->x_next : nullptr));
+    }
+    return IHS_OK;
+  }
+  const bool use_sort = cs_sort_supported(M);
   const bool fuse = SA && use_sort && g && d <= 256;
   if (SA) {
     if (use_sort) {
@@ -306,11 +368,9 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       // then share a launch with three others (C5: 35.4 -> 34.4 ms/step against
       // one wave; IHS_SJLT_NB=k overrides).  The sort buffers hold all s blocks; two sets, so
       // the next iteration's sort can be prefetched into the other set.
-      const bool tma = c->gather == 1 && cs_gather_tma_supported(d, A->values);
-      static const int nb_env = getenv("IHS_SJLT_NB") ? atoi(getenv("IHS_SJLT_NB")) : 0;
+      const bool tma = cs_gather_tma_supported(d, A->values);
       const int nb = !tma ? 1
-                     : nb_env > 0 ? (int)std::min<int64_t>(s, nb_env)
-                                  : (int)std::max<int64_t>(1, std::min<int64_t>(s, (14 * (int64_t)c->num_sms) / std::max<int64_t>(M, 1)));
+                          : (int)std::max<int64_t>(1, std::min<int64_t>(s, (14 * (int64_t)c->num_sms) / std::max<int64_t>(M, 1)));
       const int64_t hs = (int64_t)(p.hist_bytes() / 4 + 63) / 64 * 64, ts = (int64_t)(p.tiles_bytes() / 4 + 63) / 64 * 64;
       const int64_t ps = (p.n + 63) / 64 * 64;
       const bool hit = c->pre.valid && c->pre.key == key && c->pre.row_offset == A->row_offset && c->pre.n == n &&
@@ -357,30 +417,26 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       // The side-stream sort is enqueued after the first gather launch (still
       // eligible from ev_main, recorded before it), so the gather's CTAs are
       // placed first and the sort takes leftover slots: C2 0.794 -> 0.789,
-      // C4 0.859 -> 0.848, C5 36.9 -> 36.1 ms/step against enqueueing it first
-      // (IHS_PREFETCH_ORDER=before).
-      static const bool pf_after = !getenv("IHS_PREFETCH_ORDER") || std::strcmp(getenv("IHS_PREFETCH_ORDER"), "before");
+      // C4 0.859 -> 0.848, C5 36.9 -> 36.1 ms/step against enqueueing it first.
+      // The ctx records the prefetch (pre, side_pending) only once its sort is
+      // enqueued, so a failed launch before it leaves no stale tag behind.
       bool pf_pending = false;
       uint64_t pf_key = 0;
       int32_t *pf_h = nullptr, *pf_t = nullptr;
       uint32_t *pf_p = nullptr;
+      ihs_ctx_s::SortTag pf_tag;
+      int pf_set = 0;
       auto issue_prefetch = [&]() -> ihs_status {
+        pf_pending = false;
         IHS_TRY(sort_all(pf_key, pf_h, pf_t, pf_p, c->side));
         IHS_CUDA(cudaEventRecord(c->ev_side, c->side));
-        pf_pending = false;
+        c->side_pending = true;
+        c->pre = pf_tag;
+        c->pre_set = pf_set;
         return IHS_OK;
       };
       if (c->prefetch && n > 0) {
-        if (!c->side) {
-          // IHS_SIDE_PRIO=1: the sort stream at the highest priority (its CTAs
-          // take freed slots before pending gather CTAs)
-          static const bool side_hi = getenv("IHS_SIDE_PRIO") && atoi(getenv("IHS_SIDE_PRIO")) == 1;
-          int lo = 0, hi = 0;
-          cudaDeviceGetStreamPriorityRange(&lo, &hi);
-          IHS_CUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, side_hi ? hi : lo));
-          IHS_CUDA(cudaEventCreateWithFlags(&c->ev_side, cudaEventDisableTiming));
-          IHS_CUDA(cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming));
-        }
+        IHS_TRY(ensure_side(c));
         const int nset = 1 - set;
         int32_t *h2, *t2;
         uint32_t *p2;
@@ -393,16 +449,14 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
         pf_t = t2;
         pf_p = p2;
         pf_pending = true;
-        if (!pf_after) IHS_TRY(issue_prefetch());
-        c->side_pending = true;
-        c->pre.valid = true;
-        c->pre.key = key_next;
-        c->pre.row_offset = A->row_offset;
-        c->pre.n = n;
-        c->pre.M = M;
-        c->pre.s = s;
-        c->pre.A = A->values;
-        c->pre_set = nset;
+        pf_tag.valid = true;
+        pf_tag.key = key_next;
+        pf_tag.row_offset = A->row_offset;
+        pf_tag.n = n;
+        pf_tag.M = M;
+        pf_tag.s = s;
+        pf_tag.A = A->values;
+        pf_set = nset;
       }
       for (int j0 = 0; j0 < s; j0 += nb) {
         const int cnt = std::min(nb, s - j0);
@@ -423,10 +477,7 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
                                         nseg > 1 ? sapart : SAj, gp, nseg > 1 ? 1.0 : scale, st, lc_of(c), cnt, bst));
           if (nseg > 1)
             IHS_CUDA(launch_sum_splits(sapart, (int64_t)cnt * M * d, nseg, scale, SAj, st, lc_of(c)));
-        } else if (c->gather == 2 && cs_gather_async_supported(d, A->values)) {
-          IHS_CUDA(launch_cs_gather_async(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp,
-                                          scale, st, lc_of(c)));
-        } else {
+        } else {  // odd d, d > 256 or an unaligned A: the register-staged gather
           IHS_CUDA(launch_cs_gather(A->values, n, d, M, hist_j, tiles_j, p.nchunks, perm_j, b, x, SAj, gp, scale, st,
                                     lc_of(c)));
         }
@@ -439,12 +490,7 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
         IHS_CUDA(launch_reduce_rows(gpart, M * nseg, d, g, gpart + M * nseg * d, reduce_counter(c), st, lc_of(c),
                                     ls ? ls->Hinv : nullptr, ls ? ls->x : nullptr, ls ? ls->x_next : nullptr));
       }
-    } else if (use_stream) {
-      double *part;
-      IHS_TRY(scratch(c, S_SJLT, sp.partial_bytes(), &part));
-      Prof pr(c, IHS_K_SJLT);
-      IHS_CUDA(launch_sjlt_stream(sp, A->values, key, A->row_offset, part, SA, spec_scale(spec), st, lc_of(c)));
-    } else {
+    } else {  // more buckets than the counting sort handles: shared-memory tiles (sjlt_dense.cu)
       SjltPlan p;
       if (!sjlt_plan(n, d, m, s, c->num_sms, p)) return IHS_ERR_UNSUPPORTED;
       double *part;
@@ -491,7 +537,7 @@ ihs_status ols_impl(ihs_ctx c, const double *H, const double *g, int64_t d, cons
   double *sc;
   IHS_TRY(scratch(c, S_CHOL, chol_scratch_bytes(d), &sc));
   Prof pr(c, IHS_K_CHOL);
-  IHS_CUDA(launch_ols_update(H, g, d, x, xn, sc, c->d_status, c->num_sms, c->stream, lc_of(c)));
+  IHS_CUDA(launch_ols_update(H, g, d, x, xn, sc, c->d_status, c->num_sms, c->ols_large, c->stream, lc_of(c)));
   return IHS_OK;
 }
 
@@ -501,9 +547,7 @@ ihs_status ols_impl(ihs_ctx c, const double *H, const double *g, int64_t d, cons
 // the default fuses only d <= 64; IHS_FUSE=1 forces it for d <= 128, 0 never.
 ihs_status gram_ols_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, const double *g,
                          const double *x, double *xn, double *H) {
-  static const char *fe = getenv("IHS_FUSE");
-  static const int64_t fuse_max = !fe ? 64 : (!std::strcmp(fe, "0") ? 0 : 128);
-  if (d <= fuse_max && gram_ols_supported(d) && m >= 1) {
+  if (d <= c->fuse_max_d && gram_ols_supported(d) && m >= 1) {
     Prof pr(c, IHS_K_CHOL);
     const cudaError_t e = launch_gram_ols(SA, m, d, scale, g, x, xn, H, c->d_status, c->stream, lc_of(c));
     if (e == cudaSuccess) return IHS_OK;
@@ -564,12 +608,10 @@ ihs_inner_cfg default_inner();
 
 ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {
   if (m < 1 || d < 1) return IHS_ERR_INVALID_ARGUMENT;
-  static const int side_sms = getenv("IHS_LOOKAHEAD_SMS") ? std::max(1, atoi(getenv("IHS_LOOKAHEAD_SMS"))) : 16;
-  GramPlan p = gram_plan(m, d, std::min(side_sms, c->num_sms));
+  GramPlan p = gram_plan(m, d, std::min(16, c->num_sms));  // a 16-SM plan: it runs beside the update's cluster
   double *part;
   IHS_TRY(scratch(c, S_GRAMF, p.partial_bytes(), &part));  // (before factor_begin: a regrowth joins)
-  static const bool side_power = !getenv("IHS_LOOKAHEAD_POWER") || atoi(getenv("IHS_LOOKAHEAD_POWER")) != 0;
-  const bool power = side_power && pg_supported(d);
+  const bool power = pg_supported(d);
   double *ev = nullptr;
   if (power) {  // allocated on the ctx stream before the factor stream's dependency is recorded
     if (!c->d_L) IHS_CUDA(cudaMalloc(&c->d_L, 4 * sizeof(double)));
@@ -589,9 +631,10 @@ ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, dou
   if (power) {
     const ihs_inner_cfg k = default_inner();
     Prof pr(c, IHS_K_FACTOR, c->fstream);
-    const cudaError_t e = launch_l1ball_update(H, nullptr, d, nullptr, 0.0, 0, k.power_iters, k.inner_tol,
-                                               k.lip_safety, nullptr, nullptr, ev, c->d_status, c->fstream, lc_of(c),
-                                               c->pgf_warm_d == d, 0, nullptr, c->d_L + (slot - c->fac));
+    const cudaError_t e = launch_l1ball_update(H, nullptr, d, nullptr, 0.0, 0, k.power_iters, k.warm_power_iters,
+                                               k.inner_tol, k.lip_safety, nullptr, nullptr, ev, c->d_status,
+                                               c->fstream, lc_of(c), c->pgf_warm_d == d, 0, nullptr,
+                                               c->d_L + (slot - c->fac));
     if (e == cudaSuccess) {
       c->pgf_warm_d = d;
       slot->L_ready = true;
@@ -607,10 +650,9 @@ ihs_status ols_factor_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, do
   if (!gram_ols_supported(d) || m < 1) return IHS_ERR_UNSUPPORTED;
   ihs_ctx_s::Factor *slot;
   IHS_TRY(factor_begin(c, Hinv, &slot));
-  static const int max_cluster = getenv("IHS_LOOKAHEAD_CLUSTER") ? atoi(getenv("IHS_LOOKAHEAD_CLUSTER")) : 8;
   {
     Prof pr(c, IHS_K_FACTOR, c->fstream);
-    IHS_CUDA(launch_ols_factor(SA, m, d, scale, Hinv, c->d_status, max_cluster, c->fstream, lc_of(c)));
+    IHS_CUDA(launch_ols_factor(SA, m, d, scale, Hinv, c->d_status, 8, c->fstream, lc_of(c)));
   }
   return factor_end(c, Hinv, slot);
 }
@@ -637,6 +679,8 @@ ihs_inner_cfg default_inner() {
   ihs_inner_cfg k;
   k.max_inner = 20000;
   k.power_iters = 50;
+  k.warm_power_iters = 12;
+  k.reserved = 0;
   k.inner_tol = 1e-14;
   k.lip_safety = 1.05;
   return k;
@@ -646,7 +690,8 @@ ihs_inner_cfg default_inner() {
 ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const double *x, double radius,
                    const ihs_inner_cfg *cfg, double *xn, int32_t *inner, int prox = 0) {
   ihs_inner_cfg k = cfg ? *cfg : default_inner();
-  if (k.max_inner < 1 || k.power_iters < 1 || !(k.inner_tol >= 0.0) || !(k.lip_safety > 0.0))
+  if (k.max_inner < 1 || k.power_iters < 1 || k.warm_power_iters < 1 || !(k.inner_tol >= 0.0) ||
+      !(k.lip_safety > 0.0))
     return IHS_ERR_INVALID_ARGUMENT;
   if (!pg_supported(d) || (prox && !lasso_supported(d))) return IHS_ERR_UNSUPPORTED;
   IHS_TRY(wait_factor(c, H));  // a look-ahead Gram that writes H
@@ -654,18 +699,21 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
   for (auto &f : c->fac)
     if (f.L_ready && f.Hinv == H) {
       const ihs_inner_cfg k0 = default_inner();
-      if (f.L_d == d && k.power_iters == k0.power_iters && k.lip_safety == k0.lip_safety) L_in = c->d_L + (&f - c->fac);
+      if (f.L_d == d && k.power_iters == k0.power_iters && k.warm_power_iters == k0.warm_power_iters &&
+          k.lip_safety == k0.lip_safety)
+        L_in = c->d_L + (&f - c->fac);
       f.L_ready = false;
     }
-  // warm-started power iteration across calls with the same d (IHS_PG_WARM=0 off)
-  static const bool warm_env = !getenv("IHS_PG_WARM") || std::strcmp(getenv("IHS_PG_WARM"), "0") != 0;
+  // warm-started power iteration across calls with the same d (option pg_warm)
+  const bool warm_env = c->pg_warm != 0;
   double *ev = nullptr;
   if (warm_env && c->cap[S_PG] < std::max<size_t>(pg_scratch_bytes(d), 256)) c->pg_warm_d = -1;  // (re)allocation loses it
   if (warm_env) IHS_TRY(scratch(c, S_PG, pg_scratch_bytes(d), &ev));
   const bool warm = warm_env && c->pg_warm_d == d;
   Prof pr(c, IHS_K_PG);
-  IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.inner_tol, k.lip_safety, xn, inner,
-                                ev, c->d_status, c->stream, lc_of(c), warm, prox, L_in, nullptr));
+  IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.warm_power_iters, k.inner_tol,
+                                k.lip_safety, xn, inner, ev, c->d_status, c->stream, lc_of(c), warm, prox, L_in,
+                                nullptr));
   if (warm_env && !L_in) c->pg_warm_d = d;
   return IHS_OK;
 }
@@ -777,21 +825,50 @@ ihs_status pg_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_sp
 // CountSketch (an SJLT pass is s gathers, next to which the d x d work is
 // < 0.3% on C5 and the measured difference was within run-to-run noise).
 // IHS_LOOKAHEAD=0 disables it, =1 uses it whenever supported.
-bool use_lookahead(const ihs_matrix *A, const ihs_sketch_spec *spec, int32_t T) {
-  static const char *env = getenv("IHS_LOOKAHEAD");
+// `rows` is the same on every rank (rows_for_schedule), so every rank takes the
+// same schedule and issues the same collectives.
+bool use_lookahead(ihs_ctx c, const ihs_matrix *A, int64_t rows, const ihs_sketch_spec *spec, int32_t T) {
   const int64_t d = A->n_cols;
   const bool ok = A->layout == IHS_DENSE_ROW_MAJOR && gram_ols_supported(d) && spec->m >= 1 && T >= 1;
-  if (env) return ok && std::strcmp(env, "0") != 0;
-  return ok && spec->s == 1 && T >= 3 && A->n_rows * d >= (int64_t(1) << 27);
+  if (c->lookahead >= 0) return ok && c->lookahead != 0;
+  return ok && spec->s == 1 && T >= 3 && rows * d >= (int64_t(1) << 27);
 }
 
 // l1 / LASSO look-ahead (the Gram only): dense CountSketch, n d >= 2^27, T >= 3;
-// IHS_LOOKAHEAD=0 / 1 as for OLS.
-bool use_lookahead_pg(const ihs_matrix *A, const ihs_sketch_spec *spec, int32_t T) {
-  static const char *env = getenv("IHS_LOOKAHEAD");
+// the lookahead option (IHS_LOOKAHEAD=0 / 1) as for OLS.
+bool use_lookahead_pg(ihs_ctx c, const ihs_matrix *A, int64_t rows, const ihs_sketch_spec *spec, int32_t T) {
   const bool ok = A->layout == IHS_DENSE_ROW_MAJOR && spec->m >= 1 && T >= 1 && pg_supported(A->n_cols);
-  if (env) return ok && std::strcmp(env, "0") != 0;
-  return ok && spec->s == 1 && T >= 3 && A->n_rows * A->n_cols >= (int64_t(1) << 27);
+  if (c->lookahead >= 0) return ok && c->lookahead != 0;
+  return ok && spec->s == 1 && T >= 3 && rows * A->n_cols >= (int64_t(1) << 27);
+}
+
+// a3: in-place sum over the ctx communicator (no-op on one rank).
+ihs_status allreduce_impl(ihs_ctx c, double *buf, int64_t count) {
+  if (c->world <= 1 || count == 0) return IHS_OK;
+  if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
+  if (g_nccl.AllReduce(buf, buf, (size_t)count, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0) return IHS_ERR_COMM;
+  return IHS_OK;
+}
+
+// Rows per rank that the schedule decision uses: the local count on one rank;
+// with a communicator ceil(n_global / world), n_global summed over the ranks
+// (shard sizes may differ by a row, and a per-rank rule could then split the
+// ranks between two schedules with different collectives).
+ihs_status rows_for_schedule(ihs_ctx c, int64_t n_local, int64_t *rows) {
+  *rows = n_local;
+  if (c->world <= 1) return IHS_OK;
+  if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
+  double *buf;
+  IHS_TRY(scratch(c, S_ROWS, 8, &buf));
+  const double v = (double)n_local;
+  IHS_CUDA(cudaMemcpyAsync(buf, &v, 8, cudaMemcpyHostToDevice, c->stream));
+  if (g_nccl.AllReduce(buf, buf, 1, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0) return IHS_ERR_COMM;
+  double tot = 0.0;
+  IHS_CUDA(cudaMemcpyAsync(&tot, buf, 8, cudaMemcpyDeviceToHost, c->stream));
+  IHS_CUDA(cudaStreamSynchronize(c->stream));
+  const int64_t ng = (int64_t)tot;
+  *rows = (ng + c->world - 1) / c->world;
+  return IHS_OK;
 }
 
 // Shared IHS loop (a1-a7).  constraint 0 = OLS, 1 = l1 ball.
@@ -864,7 +941,10 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
   if (trace)
     for (auto &e : ev) IHS_CUDA(cudaEventCreate(&e));
   ihs_status result = IHS_OK;
-  const bool lookahead = !trace && (constraint == 0 ? use_lookahead(&A, spec, T) : use_lookahead_pg(&A, spec, T));
+  int64_t rows = n;
+  if (!trace) IHS_TRY(rows_for_schedule(c, n, &rows));
+  const bool lookahead =
+      !trace && (constraint == 0 ? use_lookahead(c, &A, rows, spec, T) : use_lookahead_pg(c, &A, rows, spec, T));
   if (lookahead && constraint == 0) IHS_TRY(ols_lookahead_loop(c, &A, spec, b, iter0, T, xh));
   if (lookahead && constraint >= 1)
     IHS_TRY(pg_lookahead_loop(c, &A, spec, b, iter0, T, xh, radius, cfg, inner_dev, constraint == 2 ? 1 : 0));
@@ -965,9 +1045,13 @@ ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
     return IHS_ERR_OUT_OF_MEMORY;
   }
   cudaMemset(c->d_status, 0, 4 * sizeof(int));
-  if (const char *e = getenv("IHS_GATHER"))
-    c->gather = !std::strcmp(e, "ldg") ? 0 : !std::strcmp(e, "async") ? 2 : 1;
+  // initial option values from the environment (ihs_ctx_set_option changes them per ctx)
   if (const char *e = getenv("IHS_PREFETCH")) c->prefetch = std::strcmp(e, "0") != 0;
+  if (const char *e = getenv("IHS_SJLT")) c->sjlt_onepass = !std::strcmp(e, "passes") ? 0 : 1;
+  if (const char *e = getenv("IHS_LOOKAHEAD")) c->lookahead = std::strcmp(e, "0") != 0 ? 1 : 0;
+  if (const char *e = getenv("IHS_OLS")) c->ols_large = !std::strcmp(e, "chol") ? 2 : !std::strcmp(e, "cg") ? 0 : 1;
+  if (const char *e = getenv("IHS_FUSE")) c->fuse_max_d = !std::strcmp(e, "0") ? 0 : 128;
+  if (const char *e = getenv("IHS_PG_WARM")) c->pg_warm = std::strcmp(e, "0") != 0;
   *out = c;
   return IHS_OK;
 }
@@ -993,6 +1077,7 @@ ihs_status ihs_ctx_destroy(ihs_ctx c) {
     if (c->slot[s]) cudaFree(c->slot[s]);
   if (c->d_status) cudaFree(c->d_status);
   if (c->d_L) cudaFree(c->d_L);
+  if (c->ev_switch) cudaEventDestroy(c->ev_switch);
   if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
   for (cudaEvent_t e : c->pool) cudaEventDestroy(e);
   delete c;
@@ -1002,8 +1087,17 @@ ihs_status ihs_ctx_destroy(ihs_ctx c) {
 ihs_status ihs_ctx_set_stream(ihs_ctx c, void *stream) {
   if (!c) return IHS_ERR_INVALID_ARGUMENT;
   // pending factor / side work stays pending: it is joined into whichever stream
-  // the ctx is bound to when a call needs it (wait_factor / join_side)
-  c->stream = (cudaStream_t)stream;
+  // the ctx is bound to when a call needs it (wait_factor / join_side).  Work
+  // already enqueued on the old stream is ordered before the new one (the ctx
+  // scratch, status word and reduction counter are shared by both).
+  cudaStream_t ns = (cudaStream_t)stream;
+  if (ns != c->stream) {
+    DevGuard g(c->device);
+    if (!c->ev_switch) IHS_CUDA(cudaEventCreateWithFlags(&c->ev_switch, cudaEventDisableTiming));
+    IHS_CUDA(cudaEventRecord(c->ev_switch, c->stream));
+    IHS_CUDA(cudaStreamWaitEvent(ns, c->ev_switch, 0));
+    c->stream = ns;
+  }
   return IHS_OK;
 }
 
@@ -1016,6 +1110,49 @@ ihs_status ihs_ctx_synchronize(ihs_ctx c) {
 }
 
 int64_t ihs_ctx_kernel_launches(ihs_ctx c) { return c ? c->launches : -1; }
+
+namespace {
+struct OptionDef {
+  const char *name;
+  int ihs_ctx_s::*field;
+  int lo, hi;
+};
+const OptionDef kOptions[] = {
+    {"lookahead", &ihs_ctx_s::lookahead, -1, 1},   {"sjlt_onepass", &ihs_ctx_s::sjlt_onepass, 0, 1},
+    {"ols_large", &ihs_ctx_s::ols_large, 0, 2},    {"fuse_max_d", &ihs_ctx_s::fuse_max_d, 0, 128},
+    {"pg_warm", &ihs_ctx_s::pg_warm, 0, 1},
+};
+}  // namespace
+
+ihs_status ihs_ctx_set_option(ihs_ctx c, const char *name, int64_t value) {
+  if (!c || !name) return IHS_ERR_INVALID_ARGUMENT;
+  if (!std::strcmp(name, "prefetch")) {
+    if (value < 0 || value > 1) return IHS_ERR_INVALID_ARGUMENT;
+    c->prefetch = value != 0;
+    return IHS_OK;
+  }
+  for (const OptionDef &o : kOptions)
+    if (!std::strcmp(name, o.name)) {
+      if (value < o.lo || value > o.hi) return IHS_ERR_INVALID_ARGUMENT;
+      c->*(o.field) = (int)value;
+      return IHS_OK;
+    }
+  return IHS_ERR_INVALID_ARGUMENT;
+}
+
+ihs_status ihs_ctx_get_option(ihs_ctx c, const char *name, int64_t *value) {
+  if (!c || !name || !value) return IHS_ERR_INVALID_ARGUMENT;
+  if (!std::strcmp(name, "prefetch")) {
+    *value = c->prefetch ? 1 : 0;
+    return IHS_OK;
+  }
+  for (const OptionDef &o : kOptions)
+    if (!std::strcmp(name, o.name)) {
+      *value = c->*(o.field);
+      return IHS_OK;
+    }
+  return IHS_ERR_INVALID_ARGUMENT;
+}
 
 ihs_status ihs_ctx_set_profiling(ihs_ctx c, int enable) {
   if (!c) return IHS_ERR_INVALID_ARGUMENT;
@@ -1075,11 +1212,8 @@ ihs_status ihs_ctx_set_comm(ihs_ctx c, int rank, int world, const void *uid) {
 
 ihs_status ihs_allreduce_sum(ihs_ctx c, double *buf, int64_t count) {
   if (!c || (!buf && count > 0) || count < 0) return IHS_ERR_INVALID_ARGUMENT;
-  if (c->world == 1 || count == 0) return IHS_OK;
-  if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
   DevGuard g(c->device);
-  if (g_nccl.AllReduce(buf, buf, (size_t)count, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0) return IHS_ERR_COMM;
-  return IHS_OK;
+  return allreduce_impl(c, buf, count);
 }
 
 ihs_status ihs_hash(ihs_ctx c, const ihs_sketch_spec *spec, uint64_t iter, int64_t row_begin, int64_t count,
@@ -1093,29 +1227,37 @@ ihs_status ihs_hash(ihs_ctx c, const ihs_sketch_spec *spec, uint64_t iter, int64
   return IHS_OK;
 }
 
-ihs_status ihs_sketch(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter, double *SA) {
+ihs_status ihs_sketch(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter, double *SA,
+                      int reduce) {
   if (!c || !SA) return IHS_ERR_INVALID_ARGUMENT;
   IHS_TRY(check_matrix(A));
   IHS_TRY(check_spec(spec));
   DevGuard g(c->device);
-  return sketch_grad_impl(c, A, spec, iter, nullptr, nullptr, SA, nullptr);
+  IHS_TRY(sketch_grad_impl(c, A, spec, iter, nullptr, nullptr, SA, nullptr));
+  return reduce ? allreduce_impl(c, SA, spec->m * A->n_cols) : IHS_OK;
 }
 
-ihs_status ihs_grad(ihs_ctx c, const ihs_matrix *A, const double *b, const double *x, double *gout) {
+ihs_status ihs_grad(ihs_ctx c, const ihs_matrix *A, const double *b, const double *x, double *gout, int reduce) {
   if (!c || !gout || !x || (!b && A && A->n_rows > 0)) return IHS_ERR_INVALID_ARGUMENT;
   IHS_TRY(check_matrix(A));
   DevGuard g(c->device);
   ihs_sketch_spec dummy{IHS_COUNTSKETCH, 1, 1, 0};
-  return sketch_grad_impl(c, A, &dummy, 0, b, x, nullptr, gout);
+  IHS_TRY(sketch_grad_impl(c, A, &dummy, 0, b, x, nullptr, gout));
+  return reduce ? allreduce_impl(c, gout, A->n_cols) : IHS_OK;
 }
 
 ihs_status ihs_sketch_grad(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter, const double *b,
-                           const double *x, double *SA, double *gout) {
+                           const double *x, double *SA, double *gout, int reduce) {
   if (!c || !SA || !gout || !x || (!b && A && A->n_rows > 0)) return IHS_ERR_INVALID_ARGUMENT;
   IHS_TRY(check_matrix(A));
   IHS_TRY(check_spec(spec));
   DevGuard g(c->device);
-  return sketch_grad_impl(c, A, spec, iter, b, x, SA, gout);
+  IHS_TRY(sketch_grad_impl(c, A, spec, iter, b, x, SA, gout));
+  if (!reduce) return IHS_OK;
+  const int64_t md = spec->m * A->n_cols;
+  if (gout == SA + md) return allreduce_impl(c, SA, md + A->n_cols);  // packed [SA | g]: one all-reduce
+  IHS_TRY(allreduce_impl(c, SA, md));
+  return allreduce_impl(c, gout, A->n_cols);
 }
 
 ihs_status ihs_ols_lookahead_step(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, uint64_t iter_next,

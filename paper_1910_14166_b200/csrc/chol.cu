@@ -474,13 +474,7 @@ void launch_blocked(const double *H, const double *g, int d, const double *x, do
 }
 }  // namespace
 
-size_t chol_large_scratch_bytes(int64_t d);
-cudaError_t launch_chol_large(const double *H, const double *g, int64_t d, const double *x, double *x_next,
-                              double *scratch, int *status, cudaStream_t st, LaunchCounter lc);
-
-size_t chol_scratch_bytes(int64_t d) {
-  return d > 160 ? std::max(chol_large_scratch_bytes(d), ols_cg_scratch_bytes(d)) : 256;
-}
+size_t chol_scratch_bytes(int64_t d) { return d > 160 ? ols_large_scratch_bytes(d) : 256; }
 
 bool gram_ols_supported(int64_t d) { return d >= 1 && d <= 128; }
 
@@ -562,7 +556,8 @@ cudaError_t launch_ols_apply(const double *Hinv, const double *g, int64_t d, con
 }
 
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,
-                              double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc) {
+                              double *scratch, int *status, int num_sms, int large_mode, cudaStream_t st,
+                              LaunchCounter lc) {
   if (d <= 160) {
     const int *run = nullptr;
     const int nblk = (int)((d + 31) / 32);
@@ -576,14 +571,10 @@ cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const
     lc.add();
     return cudaGetLastError();
   }
-  // d > 160: conjugate gradients (ols_cg.cu) unless IHS_OLS=chol
-  static const bool force_chol = getenv("IHS_OLS") && !std::strcmp(getenv("IHS_OLS"), "chol");
-  if (!force_chol && ols_cg_supported(d)) {
-    const cudaError_t e = launch_ols_cg(H, g, d, x, x_next, scratch, status, num_sms, st, lc);
-    if (e != cudaErrorCooperativeLaunchTooLarge) return e;
-    cudaGetLastError();
-  }
-  return launch_chol_large(H, g, d, x, x_next, scratch, status, st, lc);
+  // d > 160: conjugate gradients with the blocked Cholesky behind them in the
+  // same launch (ols_large.cu; large_mode 1), CG alone (0) or the Cholesky alone (2)
+  if (!ols_large_supported(d)) return cudaErrorInvalidValue;
+  return launch_ols_large(H, g, d, x, x_next, scratch, status, num_sms, large_mode, st, lc);
 }
 
 }  // namespace ihs

@@ -305,30 +305,20 @@ cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t 
                                  const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm, const double *bvec,
                                  const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
                                  LaunchCounter lc, int nbatch, GatherBatchStrides bst) {
-  // consumer warps (CW) and rows per stage (KR): IHS_GATHER_CW=1|2,
-  // IHS_GATHER_ROWS=4|8 (defaults measured on B200)
-  static const int cw_env = getenv("IHS_GATHER_CW") ? atoi(getenv("IHS_GATHER_CW")) : 0;
-  static const int kr_env = getenv("IHS_GATHER_ROWS") ? atoi(getenv("IHS_GATHER_ROWS")) : 0;
-  // A's bulk copies carry an L2 evict_first hint (IHS_GATHER_HINT=0: none): the
-  // 4 GiB stream then leaves the sort arrays, b and the partials in L2 (C2 gather
-  // with the next sort beside it 0.746 -> 0.724 ms; 0.714 with the scatter's
-  // evict_last perm stores, cs_sort.cu)
-  static const int hint_env = getenv("IHS_GATHER_HINT") ? atoi(getenv("IHS_GATHER_HINT")) : 1;
-  bst.hint = hint_env;
+  // A's bulk copies carry an L2 evict_first hint: the 4 GiB stream then leaves
+  // the sort arrays, b and the partials in L2 (C2 gather with the next sort
+  // beside it 0.746 -> 0.724 ms; 0.714 with the scatter's evict_last perm
+  // stores, cs_sort.cu).  Two consumer warps and 4-row stages (one warp and
+  // 8-row stages measured slower).
+  bst.hint = 1;
   const bool f = gpart != nullptr;
-  const int CWv = cw_env == 1 || cw_env == 2 ? cw_env : kDefaultCW;
-  const int KRv = kr_env == 4 || kr_env == 8 ? kr_env : kDefaultRows;
-  // ring depth: ~kRingBytes of rows in flight per CTA, 2..kMaxStages stages
+  const int CWv = kDefaultCW;
+  const int KRv = kDefaultRows;
   // Bytes of rows in flight per CTA, measured per shape on B200 (step time):
   // the fused single-block gather (C2, d = 128) 16 KiB 0.688 / 24 KiB 0.738 /
   // 12 KiB 0.705 / 20 KiB 0.703 ms; d = 256 (C4) 40 KiB 0.771 / 32 KiB 0.775 /
   // 24 KiB 0.784; SJLT batches (C5, d = 96) 24 KiB 34.6 / 12 KiB 35.6 ms.
-  // IHS_GATHER_RING=<KiB> overrides.
-  static const int ring_env = getenv("IHS_GATHER_RING") ? atoi(getenv("IHS_GATHER_RING")) : 0;  // KiB
-  const int64_t ring = ring_env > 0                        ? (int64_t)ring_env * 1024
-                       : d >= 192                          ? 40 * 1024
-                       : (f && nbatch == 1 && d <= 128)    ? 16 * 1024
-                                                           : kRingBytes;
+  const int64_t ring = d >= 192 ? 40 * 1024 : (f && nbatch == 1 && d <= 128) ? 16 * 1024 : kRingBytes;
   const int nst = (int)std::max<int64_t>(2, std::min<int64_t>(kMaxStages, ring / (KRv * d * 8)));
   const size_t smem = (size_t)nst * KRv * d * 8 + (size_t)nst * KRv * 8 * (1 + CWv) + 2 * kMaxStages * 8 +
                       kMaxStages * KRv * 8 + 64;
@@ -347,15 +337,7 @@ cudaError_t launch_cs_gather_tma(const double *A, int64_t n, int64_t d, int64_t 
     IHS_TMA(4, CW, KR);      \
   else                       \
     IHS_TMA(8, CW, KR);
-  if (CWv == 2 && KRv == 4) {
-    IHS_TMA_NC(2, 4)
-  } else if (CWv == 2) {
-    IHS_TMA_NC(2, 8)
-  } else if (KRv == 4) {
-    IHS_TMA_NC(1, 4)
-  } else {
-    IHS_TMA_NC(1, 8)
-  }
+  IHS_TMA_NC(kDefaultCW, kDefaultRows)
 #undef IHS_TMA_NC
 #undef IHS_TMA
   lc.add();

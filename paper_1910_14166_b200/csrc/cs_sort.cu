@@ -262,15 +262,14 @@ CsSortPlan cs_sort_plan(int64_t n, int64_t m) {
 // perm stores carry an L2 evict_last hint (IHS_SCATTER_KEEP=0: none): a sector
 // of perm is written by ~2 CTAs in 4-byte pieces; kept in L2 it is completed
 // there (and read there by the next gather) instead of partially written back
-static const int keep_env = getenv("IHS_SCATTER_KEEP") ? atoi(getenv("IHS_SCATTER_KEEP")) : 1;
+constexpr int keep_env = 1;
 
 cudaError_t launch_cs_sort(const CsSortPlan &p, uint64_t key, int64_t row_offset, uint32_t jb, uint32_t sb, int32_t *hist,
                            int32_t *tile_sums, uint32_t *perm, cudaStream_t st, LaunchCounter lc) {
   const uint32_t m = (uint32_t)p.m;
   size_t hsmem = 4 * (size_t)m;
   IHS_SMEM_ATTR(cs_hist_kernel, hsmem);
-  static const int sort_ctas = getenv("IHS_SORT_CTAS") ? atoi(getenv("IHS_SORT_CTAS")) : 0;
-  const unsigned grid = (unsigned)(sort_ctas > 0 ? std::min<int64_t>(sort_ctas, p.nchunks) : p.nchunks);
+  const unsigned grid = (unsigned)p.nchunks;
   cs_hist_kernel<<<grid, kHistThreads, hsmem, st>>>(p.n, p.chunk, p.nchunks, m, key, row_offset, jb, sb,
                                                                     hist);
   scan_tiles_kernel<<<(unsigned)p.ntiles, 1024, 0, st>>>(hist, p.entries, tile_sums);

@@ -12,14 +12,14 @@ namespace ihs {
 namespace {
 constexpr int kWarps = 8;
 
-template <int NV, int U>
-__global__ void __launch_bounds__(kWarps * 32) grad_dense_kernel(const double *__restrict__ A, int64_t n, int d,
+template <int NV, int U, int W>
+__global__ void __launch_bounds__(W * 32) grad_dense_kernel(const double *__restrict__ A, int64_t n, int d,
                                                                  const double *__restrict__ bvec,
                                                                  const double *__restrict__ x,
                                                                  double *__restrict__ gpart, int64_t rows_per_warp) {
-  extern __shared__ double red[];  // kWarps x d
+  extern __shared__ double red[];  // W x d
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t gw = (int64_t)blockIdx.x * kWarps + warp;
+  const int64_t gw = (int64_t)blockIdx.x * W + warp;
   const int64_t r0 = min(n, gw * rows_per_warp);
   const int64_t r1 = min(n, r0 + rows_per_warp);
   // unpredicated loads from clamped addresses (see cs_gather.cu); clamped
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kWarps * 32) grad_dense_kernel(const double *_
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     double s = 0.0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += red[w * d + c];
+    for (int w = 0; w < W; ++w) s += red[w * d + c];
     gpart[(int64_t)blockIdx.x * d + c] = s;
   }
 }
@@ -181,15 +181,15 @@ __global__ void axpy_diff_kernel(const double *__restrict__ a, const double *__r
   if (c < d) out[c] = b ? a[c] - b[c] : a[c];
 }
 
-template <int NV, int U>
+template <int NV, int U, int W = kWarps>
 void launch_grad_t(const double *A, int64_t n, int d, const double *bvec, const double *x, double *gpart,
                    int64_t nblocks, cudaStream_t st) {
-  const int64_t warps = nblocks * kWarps;
+  const int64_t warps = nblocks * W;
   int64_t rpw = (n + warps - 1) / warps;
   rpw = (rpw + U - 1) / U * U;
-  size_t smem = (size_t)kWarps * d * 8;
-  IHS_SMEM_ATTR((grad_dense_kernel<NV, U>), smem);
-  grad_dense_kernel<NV, U><<<(unsigned)nblocks, kWarps * 32, smem, st>>>(A, n, d, bvec, x, gpart, rpw);
+  size_t smem = (size_t)W * d * 8;
+  IHS_SMEM_ATTR((grad_dense_kernel<NV, U, W>), smem);
+  grad_dense_kernel<NV, U, W><<<(unsigned)nblocks, W * 32, smem, st>>>(A, n, d, bvec, x, gpart, rpw);
 }
 
 template <int NV, int U>
@@ -230,6 +230,21 @@ cudaError_t launch_grad_dense(const double *A, int64_t n, int64_t d, const doubl
   if (d > 1024) return cudaErrorInvalidValue;
   const int nv = (int)((d + 31) / 32);
 #define CALL(NV, U) launch_grad_t<NV, U>(A, n, (int)d, bvec, x, gpart, nblocks, st)
+  IHS_NV_DISPATCH(nv, CALL)
+#undef CALL
+  lc.add();
+  return cudaGetLastError();
+}
+
+// The same pass as a 4-warp CTA per SM (nblocks = the SM count): small enough
+// (<= ~13 K registers, 3 KiB of shared memory for d = 96) to sit beside a
+// one-CTA-per-SM kernel -- the one-read SJLT sketch -- and stream A from HBM
+// while that kernel is bound by shared memory (api.cu).
+cudaError_t launch_grad_dense_corun(const double *A, int64_t n, int64_t d, const double *bvec, const double *x,
+                                    double *gpart, int64_t nblocks, cudaStream_t st, LaunchCounter lc) {
+  if (d > 1024) return cudaErrorInvalidValue;
+  const int nv = (int)((d + 31) / 32);
+#define CALL(NV, U) launch_grad_t<NV, U, 4>(A, n, (int)d, bvec, x, gpart, nblocks, st)
   IHS_NV_DISPATCH(nv, CALL)
 #undef CALL
   lc.add();

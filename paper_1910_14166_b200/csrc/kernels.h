@@ -43,13 +43,6 @@ cudaError_t launch_cs_gather(const double *A, int64_t n, int64_t d, int64_t m, c
                              const double *x, double *SA, double *gpart, double scale, cudaStream_t st,
                              LaunchCounter lc);
 
-// cp.async-fed variant (per-warp shared-memory ring).  Requires even d <= 256
-// and a 16-byte aligned A.
-bool cs_gather_async_supported(int64_t d, const void *A);
-cudaError_t launch_cs_gather_async(const double *A, int64_t n, int64_t d, int64_t m, const int32_t *hist,
-                                   const int32_t *tile_sums, int64_t nchunks, const uint32_t *perm,
-                                   const double *bvec, const double *x, double *SA, double *gpart, double scale,
-                                   cudaStream_t st, LaunchCounter lc);
 // TMA-fed variant: one CTA per bucket, bulk copies of whole rows into a smem
 // ring.  Requires even d <= 256 and a 16-byte aligned A.  A batch of nbatch
 // SJLT blocks runs in one launch (grid.y): entry y uses hist + y*bst.hist,
@@ -83,10 +76,20 @@ struct SjltPlan {
 bool sjlt_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, SjltPlan &p);
 cudaError_t launch_sjlt_dense(const SjltPlan &p, const double *A, uint64_t key, int64_t row_offset,
                               double *partials, double *SA, double scale, cudaStream_t st, LaunchCounter lc);
-// Single-pass variant: 4-column slices, warp j applies block j (2 <= s <= 16, s | m).
-bool sjlt_stream_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, SjltPlan &p);
-cudaError_t launch_sjlt_stream(const SjltPlan &p, const double *A, uint64_t key, int64_t row_offset,
-                               double *partials, double *SA, double scale, cudaStream_t st, LaunchCounter lc);
+// One-read SJLT (2 <= s <= 8, m / s <= 512, even d, 16-byte aligned A;
+// sjlt_onepass.cu): per-chunk bucket lists (a1, hashed once per iteration),
+// then one pass of column-slice CTAs with register accumulators.
+struct SjltOnepassPlan {
+  int64_t n = 0, d = 0, m = 0, M = 0, nchunks = 0;
+  int s = 0, nslices = 0, ngroups = 0, grid = 0;
+  size_t lists_bytes = 0, partial_bytes = 0, smem = 0;
+};
+bool sjlt_onepass_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, const void *A, SjltOnepassPlan &p);
+cudaError_t launch_sjlt_lists(const SjltOnepassPlan &p, uint64_t key, int64_t row_offset, uint16_t *lists,
+                              cudaStream_t st, LaunchCounter lc);
+// SA = scale * S A from the lists (partials: p.partial_bytes of scratch)
+cudaError_t launch_sjlt_onepass(const SjltOnepassPlan &p, const double *A, const uint16_t *lists, double *partials,
+                                double *SA, double scale, cudaStream_t st, LaunchCounter lc);
 // SA[e] = scale * sum_{k < nsplit} partials[k * count + e], k ascending.
 cudaError_t launch_sum_splits(const double *partials, int64_t count, int nsplit, double scale, double *SA,
                               cudaStream_t st, LaunchCounter lc);
@@ -103,6 +106,10 @@ cudaError_t launch_scale(double *buf, int64_t count, double scale, cudaStream_t 
 int64_t grad_dense_blocks(int64_t n, int64_t d, int num_sms);
 cudaError_t launch_grad_dense(const double *A, int64_t n, int64_t d, const double *bvec, const double *x,
                               double *gpart, int64_t nblocks, cudaStream_t st, LaunchCounter lc);
+// 4-warp CTAs (one per SM, nblocks = SMs) that can co-reside with a
+// one-CTA-per-SM kernel; same gpart layout.
+cudaError_t launch_grad_dense_corun(const double *A, int64_t n, int64_t d, const double *bvec, const double *x,
+                                    double *gpart, int64_t nblocks, cudaStream_t st, LaunchCounter lc);
 // out[c] = sum_{r < rows} part[r*d + c] (fixed order), c < d.
 constexpr int64_t kReduceRowsPerCta = 64;
 // scratch doubles launch_reduce_rows needs in tmp
@@ -132,9 +139,13 @@ cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, doubl
                         cudaStream_t st, LaunchCounter lc);
 
 // ---- a6 OLS: Cholesky solve ----------------------------------------------------
+// d <= 160: blocked Cholesky in one CTA (chol.cu); d > 160: ols_large.cu with
+// large_mode 0 = conjugate gradients only, 1 = CG and, when CG does not finish,
+// the blocked Cholesky in the same cooperative launch, 2 = the Cholesky only.
 size_t chol_scratch_bytes(int64_t d);
 cudaError_t launch_ols_update(const double *H, const double *g, int64_t d, const double *x, double *x_next,
-                              double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc);
+                              double *scratch, int *status, int num_sms, int large_mode, cudaStream_t st,
+                              LaunchCounter lc);
 
 // a4 + a6 fused (d <= 128): H = scale^2 SA^T SA and x_next = x + H^{-1} g in one
 // cluster launch; H_out (optional) receives H.
@@ -147,11 +158,11 @@ cudaError_t launch_ols_apply(const double *Hinv, const double *g, int64_t d, con
 bool gram_ols_supported(int64_t d);
 cudaError_t launch_gram_ols(const double *SA, int64_t m, int64_t d, double scale, const double *g, const double *x,
                             double *x_next, double *H_out, int *status, cudaStream_t st, LaunchCounter lc);
-// d > 160 default: Jacobi-preconditioned CG in one cooperative launch (ols_cg.cu).
-bool ols_cg_supported(int64_t d);
-size_t ols_cg_scratch_bytes(int64_t d);
-cudaError_t launch_ols_cg(const double *H, const double *g, int64_t d, const double *x, double *x_next,
-                          double *scratch, int *status, int num_sms, cudaStream_t st, LaunchCounter lc);
+bool ols_large_supported(int64_t d);
+size_t ols_large_scratch_bytes(int64_t d);
+cudaError_t launch_ols_large(const double *H, const double *g, int64_t d, const double *x, double *x_next,
+                             double *scratch, int *status, int num_sms, int mode, cudaStream_t st,
+                             LaunchCounter lc);
 
 // ---- a6 l1 ball: projected gradient -----------------------------------------
 size_t pg_scratch_bytes(int64_t d);
@@ -163,7 +174,8 @@ int pg_cluster_size(int64_t d);
 // the penalised form (NEXT-2), radius is lambda and the projection becomes the
 // soft threshold at lambda / L (d <= 256 only: cudaErrorNotSupported beyond).
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
-                                 int max_inner, int power_iters, double tol, double safety, double *x_next,
+                                 int max_inner, int power_iters, int warm_power_iters, double tol, double safety,
+                                 double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
                                  LaunchCounter lc, bool warm_start = false, int prox = 0,
                                  const double *L_in = nullptr, double *L_out = nullptr);

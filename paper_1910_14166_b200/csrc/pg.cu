@@ -543,15 +543,15 @@ bool pg_supported(int64_t d) { return pg_cluster_size(d) > 0 || (size_t)5 * d * 
 size_t pg_scratch_bytes(int64_t d) { return (size_t)d * 8; }
 
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
-                                 int max_inner, int power_iters, double tol, double safety, double *x_next,
-                                 int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
+                                 int max_inner, int power_iters, int warm_power_iters, double tol, double safety,
+                                 double *x_next, int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
                                  LaunchCounter lc, bool warm_start, int prox, const double *L_in, double *L_out) {
-  static const bool use_cluster = !getenv("IHS_PG_SINGLE");
-  static const bool warp_version = !getenv("IHS_PG_CTA");
-  const int cs = use_cluster ? pg_cluster_size(d) : 0;
+  // d <= 256: the warp-per-iterate cluster kernel; larger d: the CTA-level
+  // cluster kernel while H fits the cluster's shared memory, else one CTA
+  const int cs = pg_cluster_size(d);
   if (cs > 0) {
     const int64_t R = (d + cs - 1) / cs;
-    const bool wv = warp_version && d <= 256;
+    const bool wv = d <= 256;
     const size_t smem =
         std::max(wv ? (size_t)(R * d + R + 2 * d) * 8 : (size_t)(R * d + 6 * d) * 8, kExclusiveSmem);
     auto wkern = d <= 32 ? pg_warp_kernel<1> : d <= 64 ? pg_warp_kernel<2> : d <= 128 ? pg_warp_kernel<4>
@@ -577,14 +577,12 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
       return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
                                 x_next, inner_iters, status);
     }
-    // accel bit 0: FISTA (IHS_PG_PLAIN=1: off); bit 1: warm-started projection
-    // threshold (IHS_PG_THETA_WARM=0: off)
-    static const int accel = ((getenv("IHS_PG_PLAIN") && std::strcmp(getenv("IHS_PG_PLAIN"), "0") != 0) ? 0 : 1) |
-                             ((getenv("IHS_PG_THETA_WARM") && !std::strcmp(getenv("IHS_PG_THETA_WARM"), "0")) ? 0 : 2);
+    // accel bit 0: FISTA with restart; bit 1: warm-started projection threshold
+    constexpr int accel = 3;
     // warm start (scratch = d doubles holding the last eigenvector estimate):
-    // a dozen power steps from it instead of power_iters from 1/sqrt(d)
+    // warm_power_iters steps from it instead of power_iters from 1/sqrt(d)
     const bool warm_ok = warm_start && scratch;
-    const int piters = warm_ok ? std::min(power_iters, 12) : power_iters;
+    const int piters = warm_ok ? warm_power_iters : power_iters;
     return cudaLaunchKernelEx(&cfg, wkern, H, g, (int)d, x, radius, max_inner, piters, tol, safety, x_next,
                               inner_iters, status, accel, scratch, warm_ok ? 1 : 0, prox, L_in, L_out);
   }

@@ -77,16 +77,19 @@ class CudaOps:
         return P.ihs_pred_err2(A, X, xref, ctx=self.ctx)
 
 
-def lookahead_default(A, d: int, spec: P.Spec, constraint: str = "ols") -> bool:
+def lookahead_default(A, d: int, spec: P.Spec, constraint: str = "ols", rows: int | None = None) -> bool:
     """The look-ahead schedule pays when one pass over A is long next to the
-    d x d work it hides (dense, CountSketch, n d >= 2^27 on this rank; OLS:
-    d <= 128); IHS_LOOKAHEAD=0/1 overrides (the rule of ihs_solve_*, api.cu)."""
+    d x d work it hides (dense, CountSketch, rows * d >= 2^27 per rank; OLS:
+    d <= 128); IHS_LOOKAHEAD=0/1 overrides (the rule of ihs_solve_*, api.cu).
+    `rows` must be the same on every rank (ceil(n_global / world), see
+    ShardedIHS): a per-rank size could put ranks on different schedules, whose
+    collectives differ."""
     import os
     env = os.environ.get("IHS_LOOKAHEAD")
     if env is not None:  # forced: any matrix (OLS with d > 128 or CSR: the Gram-only form)
         return d >= 1 and env != "0"
     ok = isinstance(A, P.Dense) and d >= 1 and (d <= 128 or constraint != "ols")
-    return ok and spec.s == 1 and A.n * d >= (1 << 27)
+    return ok and spec.s == 1 and (A.n if rows is None else rows) * d >= (1 << 27)
 
 
 class ShardedIHS:
@@ -127,7 +130,12 @@ class ShardedIHS:
         self.H = torch.empty((d, d), dtype=torch.float64, device=dev)
         self.inner = torch.zeros(1, dtype=torch.int32, device=dev)
         if lookahead is None:
-            lookahead = lookahead_default(A, d, spec, constraint)
+            # the same decision on every rank: rows per rank from the global n
+            nt = torch.tensor([float(A.n)], dtype=torch.float64, device=dev)
+            if not self._solo:
+                self.allreduce(nt)
+            rows = -(-int(nt.item()) // world)
+            lookahead = lookahead_default(A, d, spec, constraint, rows=rows)
         # Gram-only look-ahead (H_{t+1} formed ahead, the update then solves with
         # H_t): the l1 / LASSO updates, and OLS where the fused H^{-1} factor does
         # not apply (d > 128 or a CSR matrix: the conjugate-gradient update)
@@ -138,21 +146,24 @@ class ShardedIHS:
         if self.lookahead:
             self.packs = torch.empty((2, m * d + d), dtype=torch.float64, device=dev)
             self.Hinv = torch.empty((2, d, d), dtype=torch.float64, device=dev)  # H^{-1} (OLS) or H
-            self._la_cur = 0
+            self._la_cur = 1  # the first prime() fills slot 0
 
     def prime(self, t: int) -> None:
         """Look-ahead prologue: S^t A (all-reduced) and its H^{-1}, so that step(t) is one pass."""
         if not self.lookahead or self._la_t == t:
             return
         m, d = self.m, self.d
-        pk = self.packs[0]
+        # into the slot the last update read (its factor was joined by that
+        # update); the other slot may still be read by a pending factor / Gram
+        k = 1 - self._la_cur
+        pk = self.packs[k]
         self.ops.sketch(self.A, self.spec, t, pk[: m * d].view(m, d))
         self.allreduce(pk[: m * d])
         if self.la_gram_only:
-            self.ops.gram_lookahead(pk[: m * d].view(m, d), self.Hinv[0])
+            self.ops.gram_lookahead(pk[: m * d].view(m, d), self.Hinv[k])
         else:
-            self.ops.ols_factor(pk[: m * d].view(m, d), self.Hinv[0])
-        self._la_t, self._la_cur = t, 0
+            self.ops.ols_factor(pk[: m * d].view(m, d), self.Hinv[k])
+        self._la_t, self._la_cur = t, k
 
     def step(self, t: int, x: torch.Tensor, xn: torch.Tensor) -> torch.Tensor:
         """x^{t+1} from x^t: a1-a2+a5 (local), a3 (all-reduce), a4, a6 (replicated)."""

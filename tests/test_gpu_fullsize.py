@@ -151,3 +151,24 @@ def test_csr_full_size(P, oracle_mod):
     assert rel_fro(S.H.cpu().numpy(), H_o) <= 1e-12
     xo = oracle_mod.ols_step(S.H.cpu().numpy(), S.g.cpu().numpy(), xh)
     assert oracle_mod.pred_rel_err(xn.cpu().numpy(), xo, csr=(rph, clh, vlh), d=d) <= 1e-9
+
+
+@pytest.mark.parametrize("name", ["C4", "C4P"])
+def test_solve_pg_default_schedule_full_size(P, oracle_mod, name):
+    """ihs_solve_l1ball (C4) / ihs_solve_lasso (C4P) at FULL size through the C
+    ABI with trace=NULL, T = 5: the default look-ahead schedule
+    (pg_lookahead_loop: the Gram of S^{t+1} A and its step bound on the factor
+    stream, the warm-started power chain) against the oracle's IHS at every t."""
+    cfg, prob = dense_full(name)
+    radius = prob["tau"] if cfg.constraint == "l1ball" else prob["lam"]
+    ctx = P.Context(0)
+    assert ctx.get_option("lookahead") == -1  # by size: n d = 2^29 >= 2^27, T >= 3 -> look-ahead
+    T = 5
+    fn = P.ihs_solve_l1ball if cfg.constraint == "l1ball" else P.ihs_solve_lasso
+    out = fn(P.Dense(prob["A"]), prob["b"], radius, P.Spec(m=cfg.m), T, ctx=ctx)
+    assert ctx.status() == P.OK
+    xh = out["x_hist"].cpu().numpy()
+    A, b = prob["A"].cpu().numpy(), prob["b"].cpu().numpy()
+    xo, _ = oracle_mod.ihs_solve(A, b, m=cfg.m, s=1, T=T, constraint=cfg.constraint, tau=radius)
+    for t in range(1, T + 1):
+        assert oracle_mod.pred_rel_err(xh[t], xo[t], A) <= 1e-9, t

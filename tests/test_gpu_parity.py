@@ -510,3 +510,156 @@ def test_deterministic_rerun(P):
     H1 = P.ihs_gram(a)
     H2 = P.ihs_gram(b)
     assert torch.equal(H1, H2)
+
+
+# ---------------------------------------------------------------- round 2: the C-ABI defaults and the large-d OLS
+def test_ctx_options(P):
+    ctx = P.Context(0)
+    for name, vals in {"lookahead": (-1, 0, 1), "sjlt_onepass": (0, 1), "ols_large": (0, 1, 2),
+                       "fuse_max_d": (0, 64, 128), "pg_warm": (0, 1), "prefetch": (0, 1)}.items():
+        for v in vals:
+            ctx.set_option(name, v)
+            assert ctx.get_option(name) == v
+    with pytest.raises(P.IhsError):
+        ctx.set_option("no_such_option", 1)
+    with pytest.raises(P.IhsError):
+        ctx.set_option("ols_large", 3)
+
+
+@pytest.mark.parametrize("constraint", ["l1ball", "lasso"])
+def test_solve_pg_lookahead_c_abi_scaled(P, oracle_mod, constraint):
+    """ihs_solve_l1ball / ihs_solve_lasso through the C ABI with trace=NULL and
+    the look-ahead forced (option lookahead = 1): pg_lookahead_loop (the
+    default schedule at full C4 / C4P), its warm-started power chain and the
+    look-ahead step bound, against the oracle at every t (reading R8)."""
+    name = "C4" if constraint == "l1ball" else "C4P"
+    cfg = synthetic.CONFIGS[name].scaled(1 << 15)
+    prob = synthetic.problem(cfg, "cpu")
+    A, b = prob["A"].numpy(), prob["b"].numpy()
+    radius = prob["tau"] if constraint == "l1ball" else cfg.lam
+    T = 6
+    for la in (1, 0):
+        ctx = P.Context(0)
+        ctx.set_option("lookahead", la)
+        fn = P.ihs_solve_l1ball if constraint == "l1ball" else P.ihs_solve_lasso
+        out = fn(prob["A"].to(DEV), prob["b"].to(DEV), radius, P.Spec(m=cfg.m), T, iter0=1, ctx=ctx)
+        assert ctx.status() == P.OK
+        xo, _ = oracle_mod.ihs_solve(A, b, m=cfg.m, s=1, T=T, iter0=1, constraint=constraint, tau=radius)
+        assert iterate_parity(A, out["x_hist"].cpu().numpy(), xo, oracle_mod) <= 1e-9, la
+
+
+def spd_kappa(rng, d, kappa):
+    Q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    H = (Q * np.geomspace(1.0, kappa, d)) @ Q.T
+    return 0.5 * (H + H.T)
+
+
+@pytest.mark.parametrize("d", [256, 1024])
+@pytest.mark.parametrize("kappa", [1e4, 1e8])
+def test_ols_large_high_kappa(P, oracle_mod, d, kappa):
+    """d > 160 OLS step at high condition number (reading R22) against the
+    oracle's Cholesky step, for the default (CG, then the Cholesky in the same
+    launch when CG does not finish) and the Cholesky-only option.  Bar: the
+    forward error of a backward-stable solve, 1e-15 kappa d relative."""
+    rng = np.random.default_rng(d + int(np.log10(kappa)))
+    H = spd_kappa(rng, d, kappa)
+    g = rng.standard_normal(d)
+    x = rng.standard_normal(d)
+    xo = oracle_mod.ols_step(H, g, x)
+    uo = xo - x
+    for mode in (1, 2):
+        ctx = P.Context(0)
+        ctx.set_option("ols_large", mode)
+        xn = P.ihs_ols_update(torch.from_numpy(H).to(DEV), torch.from_numpy(g).to(DEV), torch.from_numpy(x).to(DEV),
+                              ctx=ctx)
+        assert ctx.status() == P.OK, mode
+        u = xn.cpu().numpy() - x
+        assert np.linalg.norm(u - uo) <= max(1e-12, 1e-15 * kappa * d) * np.linalg.norm(uo), mode
+
+
+def test_ols_large_cg_cap(P, oracle_mod):
+    """The CG cap min(2000, 4d): CG alone (option ols_large = 0) on a kappa = 1e8
+    matrix stops there with IHS_ERR_NOT_CONVERGED and x + (its last u); the
+    default continues with the Cholesky and returns the oracle's step."""
+    d = 256
+    rng = np.random.default_rng(11)
+    H = spd_kappa(rng, d, 1e8)
+    g = rng.standard_normal(d)
+    x = np.zeros(d)
+    Hd, gd, xd = (torch.from_numpy(v).to(DEV) for v in (H, g, x))
+    ctx = P.Context(0)
+    ctx.set_option("ols_large", 0)
+    xn = P.ihs_ols_update(Hd, gd, xd, ctx=ctx)
+    assert ctx.status() == P.ERR_NOT_CONVERGED
+    u = xn.cpu().numpy()
+    assert np.all(np.isfinite(u)) and np.linalg.norm(H @ u - g) < np.linalg.norm(g)  # a partial solve
+    ctx.set_option("ols_large", 1)
+    xn = P.ihs_ols_update(Hd, gd, xd, ctx=ctx)
+    assert ctx.status() == P.OK
+    uo = oracle_mod.ols_step(H, g, x)
+    assert np.linalg.norm(xn.cpu().numpy() - uo) <= 1e-15 * 1e8 * d * np.linalg.norm(uo)
+
+
+@pytest.mark.parametrize("d", [300, 1024])
+def test_ols_large_indefinite_g_in_positive_space(P, oracle_mod, d):
+    """An indefinite H with a positive diagonal and g inside the positive
+    eigenspace, where CG can finish without meeting p.Hp <= 0 (reading R22: CG
+    certifies definiteness only on the Krylov space it explores).  The
+    Cholesky-only option reports IHS_ERR_NOT_SPD and leaves x, as the oracle
+    does; the default returns either that or a solution of H u = g."""
+    rng = np.random.default_rng(d)
+    Q, _ = np.linalg.qr(rng.standard_normal((d, d)))
+    ev = np.geomspace(1.0, 10.0, d)
+    ev[:3] = -0.5
+    H = (Q * ev) @ Q.T
+    H = 0.5 * (H + H.T)
+    assert np.diag(H).min() > 0
+    g = Q[:, 3:] @ rng.standard_normal(d - 3)
+    x = rng.standard_normal(d)
+    with pytest.raises(oracle_mod.OracleError):
+        oracle_mod.ols_step(H, g, x)
+    Hd, gd, xd = (torch.from_numpy(v).to(DEV) for v in (H, g, x))
+    ctx = P.Context(0)
+    ctx.set_option("ols_large", 2)
+    xn = P.ihs_ols_update(Hd, gd, xd, ctx=ctx)
+    assert ctx.status() == P.ERR_NOT_SPD
+    assert torch.equal(xn, xd)
+    ctx.set_option("ols_large", 1)
+    xn = P.ihs_ols_update(Hd, gd, xd, ctx=ctx)
+    st = ctx.status()
+    if st == P.OK:
+        u = xn.cpu().numpy() - x
+        assert np.linalg.norm(H @ u - g) <= 1e-12 * np.linalg.norm(g)
+    else:
+        assert st == P.ERR_NOT_SPD and torch.equal(xn, xd)
+
+
+def test_reduce_argument_single_rank(P):
+    """ihs_sketch / ihs_grad / ihs_sketch_grad with reduce = 1 on one rank: the
+    all-reduce is a no-op, results equal reduce = 0 (ihs.h)."""
+    rng = np.random.default_rng(3)
+    A = torch.from_numpy(rng.standard_normal((20_000, 64))).to(DEV)
+    b = torch.from_numpy(rng.standard_normal(20_000)).to(DEV)
+    x = torch.from_numpy(rng.standard_normal(64)).to(DEV)
+    for spec in (P.Spec(m=512), P.Spec(m=512, s=4)):
+        assert torch.equal(P.ihs_sketch(A, spec, 2, reduce=True), P.ihs_sketch(A, spec, 2))
+        p1, _, _ = P.ihs_sketch_grad(A, spec, 2, b, x, reduce=True)
+        p0, _, _ = P.ihs_sketch_grad(A, spec, 2, b, x)
+        assert torch.equal(p1, p0)
+    assert torch.equal(P.ihs_grad(A, b, x, reduce=True), P.ihs_grad(A, b, x))
+
+
+def test_sjlt_onepass_vs_passes(P, oracle_mod):
+    """The one-read SJLT sketch against the s sorted passes (bit-identical to the
+    oracle) and the oracle, with a ragged last chunk and d not a multiple of 4."""
+    rng = np.random.default_rng(8)
+    for n, d, m, s in [(70_001, 98, 4096, 8), (9_999, 10, 256, 2), (4_097, 6, 2048, 4)]:
+        A = rng.standard_normal((n, d))
+        Ad = torch.from_numpy(A).to(DEV)
+        c1, c0 = P.Context(0), P.Context(0)
+        c0.set_option("sjlt_onepass", 0)
+        one = P.ihs_sketch(Ad, P.Spec(m=m, s=s), 3, ctx=c1).cpu().numpy()
+        two = P.ihs_sketch(Ad, P.Spec(m=m, s=s), 3, ctx=c0).cpu().numpy()
+        ref = oracle_mod.sketch_dense(A, 0, 3, m, s)
+        np.testing.assert_array_equal(two, ref)
+        assert rel_fro(one, ref) <= 1e-12
