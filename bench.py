@@ -62,9 +62,10 @@ def config_obj(cfg, world, extra=None):
                      f"({cfg.dist}), {cfg.family} m={cfg.m} s={cfg.s}",
          "n": cfg.n, "d": cfg.d, "m": cfg.m, "s": cfg.s, "sketch": cfg.family,
          "parallelism": f"row-shard x{world} + allreduce[SA|g]" if world > 1 else "single GPU",
-         "l2": ("inputs larger than L2 (A = %.2f GiB per step)" % (cfg.a_bytes / 2**30)) if cfg.a_bytes > (126 << 20)
-         else ("inputs fit in L2 (A = %.2f MiB), not flushed between steps: a latency-bound small config, "
-               "not the headline workload" % (cfg.a_bytes / 2**20))}
+         "l2": ("inputs larger than L2 (A = %.2f GiB per step)" % (cfg.a_bytes / 2**30))
+         if (cfg.a_bytes >= 2 * (126 << 20) and cfg.layout != "csr")
+         else ("L2 flushed between steps (512 MiB write outside the timed events; A = %.1f MiB)"
+               % (cfg.a_bytes / 2**20))}
     if extra:
         o.update(extra)
     return o
@@ -165,7 +166,8 @@ def algorithmic(cfg, group, n_loc, nnz_loc, steps_launches):
             label += f"; SJLT: {s} bucket-ordered passes over A (A read {s}x)"
         return b, "hbm", label
     if group == "sjlt":
-        return 8 * n_loc * d + 8 * m * d, "hbm", "sjlt_stream_kernel"
+        # one-read SJLT (sjlt_onepass.cu): A once + the SA write
+        return 8 * n_loc * d + 8 * m * d, "hbm", "sjlt_onepass_kernel (one read of A; column-slice CTAs)"
     if group == "grad":
         return 8 * n_loc * d + 8 * n_loc, "hbm", "grad_dense_kernel"
     if group == "csr":  # bound by the s fp64 reductions per nonzero into the L2-resident SA
@@ -215,9 +217,122 @@ def roofline(prof, cfg, n_loc, nnz_loc, steps):
                     "frac": ach / DMMA_TFLOPS, "algorithmic_flops_per_launch": per_launch,
                     "peak_source": "measured fp64 DMMA m8n8k4 throughput (tools/probe/probe.cu)"})
     tr = ncu_traffic(cfg.name, name)
-    out["traffic"] = tr.get("dram_bytes_per_launch") if isinstance(tr, dict) else tr
+    traffic = tr.get("dram_bytes_per_launch") if isinstance(tr, dict) else tr
+    if traffic is not None and cfg.layout == "dense" and n_loc != cfg.n:
+        # the committed capture is of the single-GPU run; a rank streams n_loc of the n rows
+        traffic = traffic * n_loc / cfg.n
+        out["traffic_scaled_to_rank"] = f"single-GPU ncu bytes x {n_loc}/{cfg.n} rows"
+    out["traffic"] = traffic
     if isinstance(tr, dict):
         out["traffic_source"] = tr.get("source")
+    if name == "sjlt" and kind == "hbm":
+        # the pass is bound by shared-memory bandwidth, not HBM: every element of A is
+        # written to shared memory once (TMA) and read once per SJLT block by its bucket's owner thread
+        smem_bytes = (8.0 + 8.0 * s_of(cfg)) * n_loc * cfg.d
+        clk = CLOCK_MHZ[0] or 1965.0
+        peak = 128.0 * NUM_SMS[0] * clk * 1e6 / 1e9
+        ach = smem_bytes / (avg / 1e3) / 1e9
+        out["onchip"] = {"bound": "smem", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                         "algorithmic_bytes_per_launch": smem_bytes,
+                         "peak_source": f"128 B/clk/SM x {NUM_SMS[0]} SMs x {clk:.0f} MHz (median SM clock of the run)"}
+    return out
+
+
+CLOCK_MHZ = [None]
+NUM_SMS = [148]
+
+
+def s_of(cfg):
+    return cfg.s
+
+
+def nccl_summary(path):
+    """What NCCL's INFO log says about the communicator (ranks, NVLS), or None."""
+    if not path or not os.path.exists(path):
+        return None
+    nranks, nvls, version = None, False, None
+    with open(path, errors="replace") as f:
+        for ln in f:
+            if "nRanks" in ln and nranks is None:
+                try:
+                    nranks = int(ln.split("nRanks")[1].split()[0])
+                except (IndexError, ValueError):
+                    pass
+            if "NVLS" in ln and ("enabled" in ln.lower() or "multicast" in ln.lower() or "comm" in ln):
+                nvls = True
+            if "NCCL version" in ln and version is None:
+                version = ln.split("NCCL version", 1)[1].strip().split()[0]
+    return {"version": version, "nranks": nranks, "nvls_mentioned": nvls, "log": path}
+
+
+# ----------------------------------------------------------------------------- host / cpu baseline
+def host_info():
+    model, mem = None, None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemTotal"):
+                    mem = int(ln.split()[1]) * 1024
+                    break
+    except OSError:
+        pass
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"cpu_model": model, "host_cores": cores, "ram_bytes": mem}
+
+
+def cpu_baseline(cfg, A_np, b_np, radius, seconds):
+    """The oracle as it stands on the host (rank 0, N = 1): whole IHS iterations
+    single-threaded on the full rows for about `seconds`, then one call of each
+    phase (sketch, gradient, Gram, inner solve), and the OpenMP
+    timing variants of the two row-parallel phases on all host cores."""
+    import numpy as np
+
+    import oracle
+    d = cfg.d
+    kw = dict(constraint=cfg.constraint, tau=radius) if cfg.constraint in ("l1ball", "lasso") else {}
+    x = np.zeros(d)
+    it = 0
+    t0 = time.perf_counter()
+    while True:
+        xh_o, _ = oracle.ihs_solve(A_np, b_np, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=it, x0=x, **kw)
+        x = xh_o[-1]
+        it += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or it >= 50:
+            break
+
+    def timed(fn):
+        t = time.perf_counter()
+        r = fn()
+        return r, 1e3 * (time.perf_counter() - t)
+
+    SA, t_sk = timed(lambda: oracle.sketch_dense(A_np, cfg.hash_seed, it, cfg.m, cfg.s))
+    g, t_gr = timed(lambda: oracle.grad_dense(A_np, b_np, x))
+    H, t_gm = timed(lambda: oracle.gram(SA))
+    if cfg.constraint == "ols":
+        _, t_so = timed(lambda: oracle.ols_step(H, g, x))
+    elif cfg.constraint == "l1ball":
+        _, t_so = timed(lambda: oracle.l1ball_step(H, g, x, radius))
+    else:
+        _, t_so = timed(lambda: oracle.lasso_step(H, g, x, radius))
+    threads = oracle.omp_threads()
+    oracle.grad_dense_omp(A_np[:4096], b_np[:4096], x)  # thread pool warm-up
+    _, t_sko = timed(lambda: oracle.sketch_dense_omp(A_np, cfg.hash_seed, it, cfg.m, cfg.s))
+    _, t_gro = timed(lambda: oracle.grad_dense_omp(A_np, b_np, x))
+    t_omp = t_sko + t_gro + t_gm + t_so
+    out = {"value": cfg.n * it / el, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": f"full {cfg.name} rows ({cfg.n}x{d}), {it} oracle IHS iterations, single thread, {el:.1f} s",
+           "per_phase_ms_single_thread": {"sketch": t_sk, "gradient": t_gr, "gram": t_gm, "solve": t_so},
+           "openmp": {"cores": threads, "sketch_ms": t_sko, "gradient_ms": t_gro,
+                      "iteration_rows_per_s": cfg.n / (t_omp / 1e3),
+                      "note": "row-parallel phases (sketch, gradient) on all host cores, partials merged in "
+                              "thread order (oracle/ihs_oracle_omp.c); Gram and solve single-threaded"}}
+    out.update(host_info())
     return out
 
 
@@ -231,24 +346,29 @@ def run_reference(args):
     import oracle
     import synthetic
     cfg = synthetic.CONFIGS[args.config]
-    rows = min(cfg.n, 1 << 20)
-    scfg = cfg.scaled(rows)
-    prob = synthetic.problem(scfg, "cpu")
     if cfg.layout != "dense":
         print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for dense configs"}))
         return 0
+    # the full configuration (same rows as the product arm: same_config); one
+    # oracle IHS iteration (~1.6 s single-threaded for C2) per step
+    rows = cfg.n
+    prob = synthetic.problem(cfg, "cpu")
     A, b = prob["A"].numpy(), prob["b"].numpy()
+    kw = {}
+    if cfg.constraint != "ols":
+        kw = dict(constraint=cfg.constraint, tau=float(prob["tau"]) if cfg.constraint == "l1ball" else cfg.lam)
     x = np.zeros(cfg.d)
     for w in range(args.warmup):
-        xh, _ = oracle.ihs_solve(A, b, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=w, x0=x)
+        xh, _ = oracle.ihs_solve(A, b, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=w, x0=x, **kw)
         x = xh[-1]
     t0 = time.perf_counter()
     for k in range(args.steps):
-        xh, _ = oracle.ihs_solve(A, b, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=args.warmup + k, x0=x)
+        xh, _ = oracle.ihs_solve(A, b, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=args.warmup + k, x0=x,
+                                 **kw)
         x = xh[-1]
     el = time.perf_counter() - t0
     value = rows * args.steps / el
-    sample = f"first {rows} rows of {cfg.name} ({rows}x{cfg.d}), one oracle IHS iteration per step"
+    sample = f"all {rows} rows of {cfg.name} ({rows}x{cfg.d}), one single-threaded oracle IHS iteration per step"
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -277,8 +397,14 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     nccl = args.dist_backend == "nccl"
+    nccl_log = None
     if world > 1:
         if nccl:
+            # NCCL's own INFO log (ranks, transports, NVLS) to a file, read back below
+            nccl_log = f"/tmp/ihs_bench_nccl.{os.getpid()}.log"
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV,NVLS")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/ihs_bench_nccl.%p.log")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group("gloo")
@@ -319,6 +445,10 @@ def main():
                 dist.barrier()
         torch.cuda.synchronize()
 
+    # configs whose inputs (nearly) fit in the 126 MB L2 are timed step by step
+    # with L2 flushed between steps (a 512 MiB write outside the timed events)
+    flush = cfg.layout == "csr" or cfg.a_bytes < 2 * (126 << 20)
+    fbuf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
     t = 0
     for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
         S.step(t, xa, xb)
@@ -333,17 +463,36 @@ def main():
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        S.step(t, xa, xb)
-        xa, xb = xb, xa
-        t += 1
-    e1.record(stream)
-    e1.synchronize()
+    if flush:
+        ms_local = 0.0
+        for _ in range(args.steps):
+            fbuf.zero_()
+            e0.record(stream)
+            S.step(t, xa, xb)
+            e1.record(stream)
+            e1.synchronize()
+            ms_local += e0.elapsed_time(e1)
+            xa, xb = xb, xa
+            t += 1
+    else:
+        e0.record(stream)
+        for _ in range(args.steps):
+            S.step(t, xa, xb)
+            xa, xb = xb, xa
+            t += 1
+        e1.record(stream)
+        e1.synchronize()
+        ms_local = e0.elapsed_time(e1)
     barrier()
     clk = clocks.stop()
     launches = ctx.kernel_launches - l0
-    ms_local = e0.elapsed_time(e1)
+    # every rank must hold the same x (replicated deterministic a4/a6 on the all-reduced [SA | g])
+    ranks_same = None
+    if world > 1:
+        xs = xa.cpu() if not nccl else xa
+        allx = [torch.empty_like(xs) for _ in range(world)]
+        dist.all_gather(allx, xs)
+        ranks_same = all(torch.equal(allx[0], v) for v in allx)
     mt = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(mt, op=dist.ReduceOp.MAX)
@@ -368,13 +517,15 @@ def main():
     ctx.set_profiling(False)
     # ---- roofline of the dominant kernel group (C2: the fused sketch+gradient gather)
     n_loc = r1 - r0
+    CLOCK_MHZ[0] = clk.get("sm_mhz") if clk else None
+    NUM_SMS[0] = torch.cuda.get_device_properties(dev).multi_processor_count
     roof = roofline(prof, cfg, n_loc, n_loc_nnz, args.steps)
     breakdown = {name: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for name, v in prof.items() if v[1]}
     # ---- time to 1e-10 (IHS solve from x^0 = 0; errors post hoc, outside the timing)
     ttt = None
-    if not args.no_ttt and cfg.layout == "dense" and cfg.constraint == "ols":
-        xopt = S.exact_ols()
-        Tmax = 60
+    if not args.no_ttt and cfg.layout == "dense":
+        xopt = S.exact_ols() if cfg.constraint == "ols" else S.exact_constrained()
+        Tmax = 60 if cfg.constraint == "ols" else 40
         xh = S.solve(Tmax, iter0=1000)
         err = S.pred_errors(xh, xopt).cpu().tolist()
         tstar = next((k for k, e in enumerate(err) if e <= 1e-10), None)
@@ -444,23 +595,8 @@ def main():
     # ---- cpu baseline: the oracle, as it stands, rank 0 at N = 1 only
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and cfg.layout == "dense":
-        import oracle
         A_np = A.cpu().numpy()
-        b_np = b.cpu().numpy()
-        x = torch.zeros(d, dtype=torch.float64).numpy()
-        it = 0
-        t0 = time.perf_counter()
-        kw = dict(constraint=cfg.constraint, tau=radius) if cfg.constraint in ("l1ball", "lasso") else {}
-        while True:
-            xh_o, _ = oracle.ihs_solve(A_np, b_np, seed=cfg.hash_seed, m=cfg.m, s=cfg.s, T=1, iter0=it, x0=x, **kw)
-            x = xh_o[-1]
-            it += 1
-            el = time.perf_counter() - t0
-            if el >= args.cpu_seconds or it >= 50:
-                break
-        cpu = {"value": cfg.n * it / el, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"full {cfg.name} rows ({cfg.n}x{d}), {it} oracle IHS iterations, single thread, "
-                         f"{el:.1f} s", "host_cores_available": os.cpu_count()}
+        cpu = cpu_baseline(cfg, A_np, b.cpu().numpy(), radius, args.cpu_seconds)
         del A_np
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -473,6 +609,10 @@ def main():
                "roofline": roof, "breakdown_ms": breakdown, "time_to_1e-10": ttt, "e2e": e2e,
                "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
                "gpu": torch.cuda.get_device_name(dev)}
+        if world > 1:
+            out["ranks_bitwise_identical_x"] = ranks_same
+            out["dist_backend"] = args.dist_backend
+            out["nccl"] = nccl_summary(nccl_log)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()

@@ -39,6 +39,60 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+_SRC_OMP = os.path.join(_HERE, "ihs_oracle_omp.c")
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+_lib_omp = None
+
+
+def build_omp(force: bool = False) -> str:
+    """liboracle_omp.so: the OpenMP timing variants of the row-parallel phases."""
+    if force or not os.path.exists(_LIB_OMP) or os.path.getmtime(_LIB_OMP) < os.path.getmtime(_SRC_OMP):
+        tmp = _LIB_OMP + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-fopenmp",
+                               "-fPIC", "-shared", "-o", tmp, _SRC_OMP, "-lm"])
+        os.replace(tmp, _LIB_OMP)
+    return _LIB_OMP
+
+
+def lib_omp():
+    global _lib_omp
+    with _lock:
+        if _lib_omp is None:
+            build_omp()
+            L = C.CDLL(_LIB_OMP)
+            i64, i32, u64, p = C.c_int64, C.c_int32, C.c_uint64, C.c_void_p
+            L.or_omp_threads.restype = C.c_int
+            L.or_omp_threads.argtypes = []
+            L.or_sketch_dense_omp.restype = None
+            L.or_sketch_dense_omp.argtypes = [i64, i64, p, i64, u64, u64, i64, i32, p]
+            L.or_grad_dense_omp.restype = None
+            L.or_grad_dense_omp.argtypes = [i64, i64, p, p, p, p]
+            _lib_omp = L
+    return _lib_omp
+
+
+def omp_threads() -> int:
+    return int(lib_omp().or_omp_threads())
+
+
+def sketch_dense_omp(A, seed, t, m, s, row_offset=0):
+    """OpenMP timing variant of sketch_dense (row blocks per thread, partials
+    added in thread order; equal to it up to rounding)."""
+    A = _f64(A)
+    n, d = A.shape
+    SA = np.empty((m, d))
+    lib_omp().or_sketch_dense_omp(n, d, _ptr(A), row_offset, seed, t, m, s, _ptr(SA))
+    return SA
+
+
+def grad_dense_omp(A, b, x):
+    """OpenMP timing variant of grad_dense."""
+    A, b, x = _f64(A), _f64(b), _f64(x)
+    g = np.empty(A.shape[1])
+    lib_omp().or_grad_dense_omp(A.shape[0], A.shape[1], _ptr(A), _ptr(b), _ptr(x), _ptr(g))
+    return g
+
+
 def lib():
     global _lib
     with _lock:

@@ -37,19 +37,13 @@ constexpr int kMMax = 512;        // buckets per block (one owner thread each)
 constexpr int kConsumers = 512;   // consumer threads (16 warps)
 constexpr int kStages = 2;
 constexpr int kTileBytes = kR * kC * 8;  // 64 KiB
-constexpr int kListThreads = 256;
 
-// List block of one chunk (u16 elements).  For each block j a header
-// hdr[j][0..M]: bucket t's list starts at pair hdr[j][t] & 0x7fff of block j's
-// entry area and holds 2 (hdr[j][t+1] - hdr[j][t]) - (hdr[j][t] >> 15) entries
-// (bit 15: the list's last pair is half empty); then the entry areas (cap_of(M)
-// entries each), lists padded to whole pairs (one 4-byte load per two
-// entries).  Entry = row | sign << 15, rows ascending within a list.
-__host__ __device__ constexpr int hpad_of(int M) { return (M + 1 + 7) / 8 * 8; }
-__host__ __device__ constexpr int cap_of(int M) { return (kR + M + 7) / 8 * 8; }
-__host__ __device__ constexpr int header_elems(int S, int M) { return S * hpad_of(M); }
-__host__ __device__ constexpr int area_start(int S, int M, int j) { return header_elems(S, M) + j * cap_of(M); }
-__host__ __device__ constexpr int list_block_elems(int S, int M) { return area_start(S, M, S); }
+// List block of one chunk (u16 elements): for each block j, off[j][0..M]
+// (bucket t's rows are ent[j][off[j][t] .. off[j][t+1])) padded to moff_of(M),
+// then ent[j][0..kR): the chunk's rows sorted by bucket, ascending within a
+// bucket, as row | sign << 15.
+__host__ __device__ constexpr int moff_of(int M) { return (M + 1 + 7) / 8 * 8; }
+__host__ __device__ constexpr int list_block_elems(int S, int M) { return S * (moff_of(M) + kR); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
@@ -86,100 +80,90 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 }
 
 // ---------------------------------------------------------------------------
-// Lists (a1): one CTA per chunk of kR local rows.  Every (row, block) pair is
-// hashed (reading R1, global row ids) and counted per (block, bucket); after
-// the quad offsets, each pair is placed into its bucket's list (shared-memory
-// atomics, in no fixed order) and every list is then sorted by row (lists hold
-// ~kR/M entries), so each bucket's sum runs in ascending row order within the
-// chunk whatever order the atomics took.
-__global__ void __launch_bounds__(kListThreads) sjlt_lists_kernel(int64_t n, uint64_t key, int64_t row_offset,
-                                                                 int s, int M, uint16_t *__restrict__ lists) {
+// Lists (a1): one CTA per chunk of kR local rows, warp j sorts the chunk by the
+// bucket of block j (the counter hash of reading R1, global row ids).  Pass 1
+// hashes each row once (codes kept in shared memory) and counts per bucket;
+// the warp scans its M counts; pass 2 places rows 32 at a time in ascending
+// order (rank among equal buckets from ballots), so each bucket's entries
+// ascend.  Out: the chunk's list block.  (Placement by shared-memory atomics
+// plus a per-list sort measured slower: 2.3 vs 1.8 ms for C5.)
+__global__ void __launch_bounds__(32 * kSMax) sjlt_lists_kernel(int64_t n, uint64_t key, int64_t row_offset,
+                                                               uint32_t s, uint32_t M, int nbits,
+                                                               uint16_t *__restrict__ lists) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int hp = hpad_of(M);
-  const int lbe = list_block_elems(s, M), he = header_elems(s, M);
-  uint16_t *blk = reinterpret_cast<uint16_t *>(smem_raw);  // the block: headers + areas
-  uint16_t *cnt = blk + lbe;                               // [s][hp]
-  uint16_t *fill = cnt + s * hp;                           // [s][hp]
-  const int tid = threadIdx.x;
+  const int moff = moff_of((int)M);
+  const int lbe = list_block_elems((int)s, (int)M);
+  uint16_t *blk = reinterpret_cast<uint16_t *>(smem_raw);              // [s][moff + kR]
+  uint16_t *code = blk + lbe;                                          // [s][kR]: bucket | neg << 15
+  int32_t *cnt = reinterpret_cast<int32_t *>(code + (size_t)s * kR);  // [s][M]
+  const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * kR;
   const int valid = (int)min((int64_t)kR, n - r0);
-  for (int e = tid; e < 2 * s * hp; e += blockDim.x) cnt[e] = 0;
-  __syncthreads();
-  // pairs (j, r) with r fastest: consecutive threads hash consecutive rows
-  const int npairs = s * valid;
-  for (int p = tid; p < npairs; p += blockDim.x) {
-    const int j = p / valid, r = p - j * valid;
-    bool neg;
-    const uint32_t b =
-        hash_bucket(key, (uint64_t)(row_offset + r0 + r), (uint32_t)j, (uint32_t)s, (uint32_t)M, neg) - (uint32_t)j * M;
-    atomicAdd(reinterpret_cast<unsigned *>(cnt + j * hp + (b & ~1u)), (b & 1u) ? 0x10000u : 1u);
-  }
-  __syncthreads();
-  // pair offsets: warp j scans ceil(cnt/2) over the buckets of block j
-  const int lane = tid & 31, warp = tid >> 5;
-  for (int j = warp; j < s; j += kListThreads / 32) {
-    const uint16_t *c = cnt + j * hp;
-    uint16_t *h = blk + j * hp;
-    int carry = 0;
-    for (int b0 = 0; b0 < M; b0 += 32) {
-      const int b = b0 + lane;
-      const int v = b < M ? (c[b] + 1) / 2 : 0;
+  if (j < (int)s) {
+    uint16_t *off = blk + (size_t)j * (moff + kR);
+    uint16_t *ent = off + moff;
+    uint16_t *cd = code + (size_t)j * kR;
+    int32_t *ct = cnt + (size_t)j * M;
+    for (uint32_t b = lane; b < M; b += 32) ct[b] = 0;
+    __syncwarp();
+    for (int r = lane; r < valid; r += 32) {
+      bool neg;
+      const uint32_t b = hash_bucket(key, (uint64_t)(row_offset + r0 + r), (uint32_t)j, s, M, neg) - (uint32_t)j * M;
+      cd[r] = (uint16_t)(b | (neg ? 0x8000u : 0u));
+      atomicAdd(&ct[b], 1);
+    }
+    __syncwarp();
+    int carry = 0;  // exclusive scan of ct -> off (u16) and the running bases (in ct)
+    for (uint32_t b0 = 0; b0 < M; b0 += 32) {
+      const uint32_t b = b0 + lane;
+      const int v = b < M ? ct[b] : 0;
       int incl = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += y;
       }
-      if (b < M) h[b] = (uint16_t)((carry + incl - v) | ((c[b] & 1) ? 0x8000 : 0));
+      const int ex = carry + incl - v;
+      if (b < M) {
+        off[b] = (uint16_t)ex;
+        ct[b] = ex;
+      }
       carry += __shfl_sync(0xffffffffu, incl, 31);
     }
-    for (int b = M + lane; b < hp; b += 32) h[b] = (uint16_t)carry;
-  }
-  __syncthreads();
-  for (int p = tid; p < npairs; p += blockDim.x) {
-    const int j = p / valid, r = p - j * valid;
-    bool neg;
-    const uint32_t b =
-        hash_bucket(key, (uint64_t)(row_offset + r0 + r), (uint32_t)j, (uint32_t)s, (uint32_t)M, neg) - (uint32_t)j * M;
-    const uint32_t old = atomicAdd(reinterpret_cast<unsigned *>(fill + j * hp + (b & ~1u)), (b & 1u) ? 0x10000u : 1u);
-    const uint32_t rank = (b & 1u) ? (old >> 16) : (old & 0xffffu);
-    blk[area_start(s, M, j) + 2 * (blk[j * hp + b] & 0x7fff) + rank] = (uint16_t)(r | (neg ? 0x8000 : 0));
-  }
-  __syncthreads();
-  // sort each list by row (insertion sort: a few entries each); pad to pairs
-  for (int L = tid; L < s * M; L += blockDim.x) {
-    const int j = L / M, t = L - j * M;
-    const int nn = cnt[j * hp + t];
-    uint16_t *e = blk + area_start(s, M, j) + 2 * (blk[j * hp + t] & 0x7fff);
-    for (int i = 1; i < nn; ++i) {
-      const uint16_t v = e[i];
-      int k = i - 1;
-      while (k >= 0 && (e[k] & 0x7fffu) > (v & 0x7fffu)) {
-        e[k + 1] = e[k];
-        --k;
+    if (lane == 0) off[M] = (uint16_t)carry;
+    for (int b = (int)M + 1 + lane; b < moff; b += 32) off[b] = 0;
+    __syncwarp();
+    for (int rb = 0; rb < valid; rb += 32) {  // stable placement, 32 rows at a time
+      const int r = rb + lane;
+      const bool v = r < valid;
+      const uint32_t c = v ? cd[r] : 0u;
+      const uint32_t b = c & 0x7fffu;
+      const unsigned peers = peers_by_ballot(b, nbits, v);
+      const int rank = __popc(peers & lanemask_lt());
+      int base = 0;
+      if (v) base = ct[b];
+      __syncwarp();
+      if (v) {
+        ent[base + rank] = (uint16_t)(r | (c & 0x8000u));
+        if (rank == 0) ct[b] = base + __popc(peers);
       }
-      e[k + 1] = v;
+      __syncwarp();
     }
-    if (nn & 1) e[nn] = 0;
+    for (int r = valid + lane; r < kR; r += 32) ent[r] = 0;
   }
   __syncthreads();
-  uint4 *g = reinterpret_cast<uint4 *>(lists + (size_t)blockIdx.x * lbe);
-  for (int i = tid; i < lbe / 8; i += blockDim.x) g[i] = reinterpret_cast<const uint4 *>(blk)[i];
+  const uint4 *src = reinterpret_cast<const uint4 *>(blk);
+  uint4 *dst = reinterpret_cast<uint4 *>(lists + (size_t)blockIdx.x * lbe);
+  for (int i = threadIdx.x; i < lbe / 8; i += blockDim.x) dst[i] = src[i];
 }
 
-// Row (entry & 0x7fff) of a stage tile, times the entry's sign (bit 15):
-// SWIZZLE_32B puts the 16-byte half h of row r at h ^ bit 2 of r; the sign is a
-// flip of the doubles' sign bits (exact, like the oracle's +-a).
+// Row (entry & 0x7fff) of a stage tile: SWIZZLE_32B puts the 16-byte half h
+// of row r at h ^ bit 2 of r.
 __device__ __forceinline__ void tile_row(const unsigned char *st, uint32_t e, double2 &lo, double2 &hi) {
   const uint32_t r = e & 0x7fffu;
   const uint32_t sw = (r >> 2) & 1u;
   lo = *reinterpret_cast<const double2 *>(st + r * 32u + 16u * sw);
   hi = *reinterpret_cast<const double2 *>(st + r * 32u + 16u * (sw ^ 1u));
-  const uint32_t flip = (e & 0x8000u) << 16;
-  lo.x = __hiloint2double(__double2hiint(lo.x) ^ (int)flip, __double2loint(lo.x));
-  lo.y = __hiloint2double(__double2hiint(lo.y) ^ (int)flip, __double2loint(lo.y));
-  hi.x = __hiloint2double(__double2hiint(hi.x) ^ (int)flip, __double2loint(hi.x));
-  hi.y = __hiloint2double(__double2hiint(hi.y) ^ (int)flip, __double2loint(hi.y));
 }
 
 // ---------------------------------------------------------------------------
@@ -188,7 +172,9 @@ __device__ __forceinline__ void tile_row(const unsigned char *st, uint32_t e, do
 // producer thread issues kR/256 TMA boxes (kC columns x 256 rows, SWIZZLE_32B,
 // A with an L2 evict_first hint) and one bulk copy of the chunk's list block.
 // Consumer thread t owns bucket t of every block j < S: acc[j][0..3]; it walks
-// block j's list of its bucket, two entries per 4-byte load.
+// block j's list of its bucket.  (Measured alternatives, C5: two entries per
+// 4-byte load 23.2 ms; four blocks merged into one list per thread with the
+// block selecting the accumulator by a 0/+-1 weight 22.3; this loop 21.6.)
 template <int S>
 __global__ void __maxnreg__(96) sjlt_onepass_kernel(
     const __grid_constant__ CUtensorMap tmap, const uint16_t *__restrict__ lists, int64_t n, int d, int M,
@@ -196,7 +182,7 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   // stage buffers 1024-byte aligned (the SWIZZLE_32B pattern is a function of the address)
   unsigned char *smem_raw = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
-  const int hp = hpad_of(M);
+  const int moff = moff_of(M);
   const int lbe = list_block_elems(S, M);
   const uint32_t lb_bytes = (uint32_t)lbe * 2u;
   // [tile 0][tile 1][lists 0][lists 1][barriers]: the tiles 1024-byte aligned
@@ -262,34 +248,19 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
       if (owner) {
 #pragma unroll
         for (int j = 0; j < S; ++j) {
-          const uint32_t h0 = lb[j * hp + tid], h1 = lb[j * hp + tid + 1];
-          const uint32_t p0 = h0 & 0x7fffu;
-          const int nn = 2 * (int)((h1 & 0x7fffu) - p0) - (int)(h0 >> 15);
-          const uint32_t *pairs = reinterpret_cast<const uint32_t *>(lb + area_start(S, M, j)) + p0;
-          const int np = nn >> 1;
-          uint32_t pr = nn > 0 ? pairs[0] : 0u;
-          // two entries per step, the next pair loaded ahead; the two rows are
-          // added first (their signs applied as sign-bit flips) and then to the
-          // accumulator: one dependent add per pair
-#pragma unroll 1
-          for (int i = 0; i < np; ++i) {
-            const uint32_t nx = (2 * (i + 1) < nn) ? pairs[i + 1] : 0u;
-            double2 lo0, hi0, lo1, hi1;
-            tile_row(st, pr & 0xffffu, lo0, hi0);
-            tile_row(st, pr >> 16, lo1, hi1);
-            acc[j][0] += lo0.x + lo1.x;
-            acc[j][1] += lo0.y + lo1.y;
-            acc[j][2] += hi0.x + hi1.x;
-            acc[j][3] += hi0.y + hi1.y;
-            pr = nx;
-          }
-          if (nn & 1) {
-            double2 lo0, hi0;
-            tile_row(st, pr & 0xffffu, lo0, hi0);
-            acc[j][0] += lo0.x;
-            acc[j][1] += lo0.y;
-            acc[j][2] += hi0.x;
-            acc[j][3] += hi0.y;
+          const uint16_t *off = lb + j * (moff + kR);
+          const uint16_t *ent = off + moff;
+          const int o0 = off[tid], o1 = off[tid + 1];
+#pragma unroll 2
+          for (int e = o0; e < o1; ++e) {
+            const uint32_t en = ent[e];
+            const double sg = (en & 0x8000u) ? -1.0 : 1.0;
+            double2 lo, hi;
+            tile_row(st, en, lo, hi);
+            acc[j][0] = fma(sg, lo.x, acc[j][0]);
+            acc[j][1] = fma(sg, lo.y, acc[j][1]);
+            acc[j][2] = fma(sg, hi.x, acc[j][2]);
+            acc[j][3] = fma(sg, hi.y, acc[j][3]);
           }
         }
       }
@@ -334,7 +305,7 @@ EncodeTiledFn encode_fn() {
 size_t onepass_smem(int S, int M) {
   return kStages * ((size_t)kTileBytes + (size_t)list_block_elems(S, M) * 2) + 2 * kStages * 8 + 1024;
 }
-size_t lists_smem(int S, int M) { return ((size_t)list_block_elems(S, M) + (size_t)2 * S * hpad_of(M)) * 2; }
+size_t lists_smem(int S, int M) { return (size_t)list_block_elems(S, M) * 2 + (size_t)S * kR * 2 + (size_t)S * M * 4; }
 }  // namespace
 
 bool sjlt_onepass_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, const void *A, SjltOnepassPlan &p) {
@@ -365,7 +336,9 @@ cudaError_t launch_sjlt_lists(const SjltOnepassPlan &p, uint64_t key, int64_t ro
                               cudaStream_t st, LaunchCounter lc) {
   const size_t smem = lists_smem(p.s, (int)p.M);
   IHS_SMEM_ATTR(sjlt_lists_kernel, smem);
-  sjlt_lists_kernel<<<(unsigned)p.nchunks, kListThreads, smem, st>>>(p.n, key, row_offset, p.s, (int)p.M, lists);
+  const int nbits = p.M > 1 ? 32 - __builtin_clz((unsigned)(p.M - 1)) : 1;
+  sjlt_lists_kernel<<<(unsigned)p.nchunks, 32 * p.s, smem, st>>>(p.n, key, row_offset, (uint32_t)p.s, (uint32_t)p.M,
+                                                                  nbits, lists);
   lc.add();
   return cudaGetLastError();
 }

@@ -592,7 +592,7 @@ def test_ols_large_cg_cap(P, oracle_mod):
     xn = P.ihs_ols_update(Hd, gd, xd, ctx=ctx)
     assert ctx.status() == P.ERR_NOT_CONVERGED
     u = xn.cpu().numpy()
-    assert np.all(np.isfinite(u)) and np.linalg.norm(H @ u - g) < np.linalg.norm(g)  # a partial solve
+    assert np.all(np.isfinite(u)) and 0.5 * u @ H @ u - g @ u < 0.0  # a partial solve: CG lowers the energy
     ctx.set_option("ols_large", 1)
     xn = P.ihs_ols_update(Hd, gd, xd, ctx=ctx)
     assert ctx.status() == P.OK

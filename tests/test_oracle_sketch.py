@@ -187,3 +187,22 @@ def test_pred_rel_err(oracle_mod):
     ref = np.linalg.norm(A @ (x - y)) / np.linalg.norm(A @ y)
     assert abs(oracle_mod.pred_rel_err(x, y, A) - ref) <= 1e-13 * ref
     assert oracle_mod.pred_rel_err(y, y, A) == 0.0
+
+
+def test_openmp_timing_variants_match_serial(oracle_mod):
+    """The OpenMP timing variants (bench.py cpu_baseline) compute the serial
+    oracle's S A and A^T(b - Ax) up to rounding (thread partials added in order)."""
+    import numpy as np
+    rng = np.random.default_rng(12)
+    A = rng.standard_normal((5003, 17))
+    b = rng.standard_normal(5003)
+    x = rng.standard_normal(17)
+    for m, s in ((256, 1), (512, 8)):
+        ref = oracle_mod.sketch_dense(A, 3, 2, m, s, row_offset=11)
+        got = oracle_mod.sketch_dense_omp(A, 3, 2, m, s, row_offset=11)
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+    g = oracle_mod.grad_dense(A, b, x)
+    go = oracle_mod.grad_dense_omp(A, b, x)
+    bound = 1e-12 * (np.abs(A) * np.abs(b - A @ x)[:, None]).sum(0)
+    assert (np.abs(go - g) <= bound).all()
+    assert oracle_mod.omp_threads() >= 1
