@@ -131,6 +131,9 @@ int64_t ihs_ctx_kernel_launches(ihs_ctx ctx);
  *                  only (positive definiteness certified exactly, reading R22) [IHS_OLS]
  *   "fuse_max_d"   a4 + a6 in one cluster launch up to this d (0..128, default 64) [IHS_FUSE]
  *   "pg_warm"      1 (default) warm-started power iteration across l1 / LASSO updates [IHS_PG_WARM]
+ *   "small_step"   1 (default) ihs_solve_ols on one rank runs each iteration of a small dense
+ *                  problem (d <= 32, n <= 32768, its working set in one CTA's shared memory)
+ *                  as ONE launch of one CTA; 0 the general multi-kernel path
  *   "prefetch"     1 (default) the next iteration's sort on the side stream   [IHS_PREFETCH] */
 ihs_status ihs_ctx_set_option(ihs_ctx ctx, const char *name, int64_t value);
 ihs_status ihs_ctx_get_option(ihs_ctx ctx, const char *name, int64_t *value);
@@ -253,6 +256,17 @@ ihs_status ihs_ols_lookahead_step(ihs_ctx ctx, const ihs_matrix *A, const ihs_sk
                                   uint64_t iter_next, const double *b, const double *x,
                                   const double *Hinv, double *SA_next, double *Hinv_next,
                                   double *g, double *x_next);
+
+/* a1-a6 of one OLS iteration of a small dense problem in ONE launch of one CTA
+ * (small_step.cu; the path of ihs_solve_ols for such problems, option
+ * "small_step"): SA = S^(iter) A (s blocks, 1/sqrt(s)), g = A^T (b - A x),
+ * H = SA^T SA, x_next = x + H^{-1} g (Cholesky).  d <= 32, n <= 32768 and the
+ * working set within one CTA's shared memory, else IHS_ERR_UNSUPPORTED.
+ * SA_out (m x d), g_out (d), H_out (d x d) may be NULL.  One rank (the local
+ * rows only: no all-reduce).  Statuses as for ihs_ols_update. */
+ihs_status ihs_small_step(ihs_ctx ctx, const ihs_matrix *A, const double *b, const ihs_sketch_spec *spec,
+                          uint64_t iter, const double *x, double *x_next, double *SA_out, double *g_out,
+                          double *H_out);
 
 /* a6, OLS: x_next = x + H^{-1} g (Eq. (2) with C = R^d; the
  * QP "solved exactly").  d <= 160: blocked Cholesky in one

@@ -84,6 +84,8 @@ _EXPORTS = {
     "ihs_sketch_grad": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.POINTER(SketchSpec), C.c_uint64, C.c_void_p,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]),
     "ihs_gram": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p]),
+    "ihs_small_step": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.c_void_p, C.POINTER(SketchSpec), C.c_uint64,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ihs_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "ihs_gram_ols_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_double, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p]),
@@ -361,6 +363,21 @@ def ihs_gram(SA: torch.Tensor, scale: float = 1.0, out=None, ctx: Context | None
     H = out if out is not None else _f64((d, d), SA.device)
     _check(lib().ihs_gram(ctx._bind(), _p(SA), m, d, float(scale), _p(H)), "ihs_gram")
     return H
+
+
+def ihs_small_step(A, b, spec: Spec, it: int, x, out=None, intermediates: bool = False, ctx: Context | None = None):
+    """One OLS IHS iteration of a small dense problem in one launch (ihs.h);
+    returns x_next, or (x_next, SA, g, H) with intermediates=True."""
+    A = as_matrix(A)
+    ctx = ctx or default_context(A.device)
+    xn = out if out is not None else torch.empty_like(x)
+    SA = _f64((spec.m, A.d), A.device) if intermediates else None
+    g = _f64(A.d, A.device) if intermediates else None
+    H = _f64((A.d, A.d), A.device) if intermediates else None
+    mc, sp = A.c(), spec.c()
+    _check(lib().ihs_small_step(ctx._bind(), C.byref(mc), _p(b), C.byref(sp), it, _p(x), _p(xn), _p(SA), _p(g),
+                                _p(H)), "ihs_small_step")
+    return (xn, SA, g, H) if intermediates else xn
 
 
 # ------------------------------------------------------------------ a6

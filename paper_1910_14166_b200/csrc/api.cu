@@ -79,6 +79,7 @@ struct ihs_ctx_s {
   int ols_large = 1;     // d > 160 OLS: 0 = CG only, 1 = CG + Cholesky fallback, 2 = Cholesky only
   int fuse_max_d = 64;   // a4 + a6 in one cluster launch up to this d (<= 128)
   int pg_warm = 1;       // warm-started power iteration across l1 / LASSO updates
+  int small_step = 1;    // small dense OLS solves: one launch per iteration (small_step.cu)
   // Speculative sort of the NEXT iteration's buckets on a side stream: the
   // hash (hence the sort) depends only on (seed, iteration, row), not on x, so
   // after the gathers of iteration t the sort for t + 1 runs beside the
@@ -608,7 +609,11 @@ ihs_inner_cfg default_inner();
 
 ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {
   if (m < 1 || d < 1) return IHS_ERR_INVALID_ARGUMENT;
-  GramPlan p = gram_plan(m, d, std::min(16, c->num_sms));  // a 16-SM plan: it runs beside the update's cluster
+  // d <= 256 (the l1 / LASSO updates): a 16-SM plan, beside the update's
+  // cluster; larger d (OLS with the CG update, e.g. C3): a full plan reading
+  // SA evict_first, beside the CG solve and the next pass's L2 reductions
+  const bool wide = d > 256;
+  GramPlan p = gram_plan(m, d, wide ? c->num_sms : std::min(16, c->num_sms));
   double *part;
   IHS_TRY(scratch(c, S_GRAMF, p.partial_bytes(), &part));  // (before factor_begin: a regrowth joins)
   const bool power = pg_supported(d);
@@ -622,7 +627,7 @@ ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, dou
   IHS_TRY(factor_begin(c, H, &slot));
   {
     Prof pr(c, IHS_K_FACTOR, c->fstream);
-    IHS_CUDA(launch_gram(p, SA, scale, part, H, c->fstream, lc_of(c)));
+    IHS_CUDA(launch_gram(p, SA, scale, part, H, c->fstream, lc_of(c), wide ? 1 : 0));
   }
   // ... and the PG step bound L = 1.05 lambda_max(H) (R10's power iteration,
   // warm-started along the chain of look-ahead Grams exactly as the update
@@ -948,7 +953,39 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
   if (lookahead && constraint == 0) IHS_TRY(ols_lookahead_loop(c, &A, spec, b, iter0, T, xh));
   if (lookahead && constraint >= 1)
     IHS_TRY(pg_lookahead_loop(c, &A, spec, b, iter0, T, xh, radius, cfg, inner_dev, constraint == 2 ? 1 : 0));
-  for (int32_t t = 0; !lookahead && t < T; ++t) {
+  // a small dense OLS problem on one rank: each iteration is one launch of one
+  // CTA (small_step.cu; launch latency dominates the multi-kernel path there)
+  const bool small = !lookahead && c->small_step && c->world == 1 && constraint == 0 &&
+                     A.layout == IHS_DENSE_ROW_MAJOR && small_step_supported(n, d, m, spec->s);
+  for (int32_t t = 0; small && t < T; ++t) {
+    const double *x = xh + (int64_t)t * d;
+    double *xn = xh + (int64_t)(t + 1) * d;
+    if (trace) cudaEventRecord(ev[0], st);
+    {
+      Prof pr(c, IHS_K_CHOL);
+      IHS_CUDA(launch_small_step(A.values, n, d, b, x, iter_key(spec->seed, iter0 + (uint64_t)t), A.row_offset, m,
+                                 spec->s, spec_scale(spec), xn, nullptr, nullptr, nullptr, c->d_status, st,
+                                 lc_of(c)));
+    }
+    if (trace) {
+      cudaEventRecord(ev[1], st);
+      IHS_CUDA(cudaEventSynchronize(ev[1]));
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0], ev[1]);
+      ihs_iter_record &r = trace[t];
+      r.t_sketch_grad = ms;  // the whole iteration is one launch
+      r.t_comm = r.t_gram = r.t_solve = 0.0;
+      r.inner_iters = 0;
+      ihs_status s2 = sync_status(c);
+      r.status = s2;
+      if (s2 != IHS_OK) {
+        result = s2;
+        T = t + 1;
+        break;
+      }
+    }
+  }
+  for (int32_t t = 0; !lookahead && !small && t < T; ++t) {
     const double *x = xh + (int64_t)t * d;
     double *xn = xh + (int64_t)(t + 1) * d;
     if (trace) cudaEventRecord(ev[0], st);
@@ -1120,7 +1157,7 @@ struct OptionDef {
 const OptionDef kOptions[] = {
     {"lookahead", &ihs_ctx_s::lookahead, -1, 1},   {"sjlt_onepass", &ihs_ctx_s::sjlt_onepass, 0, 1},
     {"ols_large", &ihs_ctx_s::ols_large, 0, 2},    {"fuse_max_d", &ihs_ctx_s::fuse_max_d, 0, 128},
-    {"pg_warm", &ihs_ctx_s::pg_warm, 0, 1},
+    {"pg_warm", &ihs_ctx_s::pg_warm, 0, 1},       {"small_step", &ihs_ctx_s::small_step, 0, 1},
 };
 }  // namespace
 
@@ -1272,6 +1309,21 @@ ihs_status ihs_ols_lookahead_step(ihs_ctx c, const ihs_matrix *A, const ihs_sket
   DevGuard g(c->device);
   const LookStep ls{Hinv, x, xn, Hinv_next};
   return sketch_grad_impl(c, A, spec, iter_next, b, x, SA_next, gout, &ls);
+}
+
+ihs_status ihs_small_step(ihs_ctx c, const ihs_matrix *A, const double *b, const ihs_sketch_spec *spec, uint64_t iter,
+                          const double *x, double *xn, double *SA_out, double *g_out, double *H_out) {
+  if (!c || !x || !xn || (!b && A && A->n_rows > 0)) return IHS_ERR_INVALID_ARGUMENT;
+  IHS_TRY(check_matrix(A));
+  IHS_TRY(check_spec(spec));
+  if (A->layout != IHS_DENSE_ROW_MAJOR || !small_step_supported(A->n_rows, A->n_cols, spec->m, spec->s))
+    return IHS_ERR_UNSUPPORTED;
+  DevGuard g(c->device);
+  Prof pr(c, IHS_K_CHOL);
+  IHS_CUDA(launch_small_step(A->values, A->n_rows, A->n_cols, b, x, iter_key(spec->seed, iter), A->row_offset,
+                             spec->m, spec->s, spec_scale(spec), xn, SA_out, g_out, H_out, c->d_status, c->stream,
+                             lc_of(c)));
+  return IHS_OK;
 }
 
 ihs_status ihs_gram(ihs_ctx c, const double *SA, int64_t m, int64_t d, double scale, double *H) {

@@ -150,10 +150,19 @@ __device__ __forceinline__ void cp_async16(double *smem, const double *gmem, boo
   int sz = pred ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(sz));
 }
+// The same with an L2 eviction policy (the look-ahead Gram beside a CSR pass
+// reads SA evict_first, so the pass's L2-resident reductions stay in L2).
+__device__ __forceinline__ void cp_async16_hint(double *smem, const double *gmem, bool pred, uint64_t pol) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;" ::"r"(sa), "l"(gmem), "r"(sz),
+               "l"(pol));
+}
 
 __global__ void __launch_bounds__(128) gram_streamk_kernel(const double *__restrict__ SA, int64_t m, int d,
                                                            int tiles, int ntri, int kch, int ipc,
-                                                           double *__restrict__ partials, int *__restrict__ slot_tile) {
+                                                           double *__restrict__ partials, int *__restrict__ slot_tile,
+                                                           int hint) {
   extern __shared__ double sm[];
   double *Xp = sm;                 // [2][KC][LDS]
   double *Xq = sm + 2 * KC * LDS;  // [2][KC][LDS]
@@ -162,6 +171,8 @@ __global__ void __launch_bounds__(128) gram_streamk_kernel(const double *__restr
   const int64_t total = (int64_t)ntri * kch;
   const int64_t i0 = (int64_t)blockIdx.x * ipc, i1 = min(total, i0 + ipc);
   if (tid == 0) slot_tile[2 * blockIdx.x] = slot_tile[2 * blockIdx.x + 1] = -1;
+  uint64_t pol = 0;
+  if (hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   double acc[4][4][2];
   int cur = -1, slot = 0;
   auto flush = [&]() {
@@ -201,9 +212,15 @@ __global__ void __launch_bounds__(128) gram_streamk_kernel(const double *__restr
         const int64_t row = kb + r;
         const bool rin = row < k1;
         const int cp = P * GT + c, cq = Q * GT + c;
-        cp_async16(&Xp[(buf * KC + r) * LDS + c], SA + (rin ? row : 0) * d + (cp < d ? cp : 0), rin && cp < d);
-        if (!diag)
-          cp_async16(&Xq[(buf * KC + r) * LDS + c], SA + (rin ? row : 0) * d + (cq < d ? cq : 0), rin && cq < d);
+        const double *gp = SA + (rin ? row : 0) * d + (cp < d ? cp : 0);
+        const double *gq = SA + (rin ? row : 0) * d + (cq < d ? cq : 0);
+        if (hint) {
+          cp_async16_hint(&Xp[(buf * KC + r) * LDS + c], gp, rin && cp < d, pol);
+          if (!diag) cp_async16_hint(&Xq[(buf * KC + r) * LDS + c], gq, rin && cq < d, pol);
+        } else {
+          cp_async16(&Xp[(buf * KC + r) * LDS + c], gp, rin && cp < d);
+          if (!diag) cp_async16(&Xq[(buf * KC + r) * LDS + c], gq, rin && cq < d);
+        }
       }
       cp_async_commit();
     };
@@ -305,13 +322,13 @@ GramPlan gram_plan(int64_t m, int64_t d, int num_sms) {
 }
 
 cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
-                        cudaStream_t st, LaunchCounter lc) {
+                        cudaStream_t st, LaunchCounter lc, int hint) {
   const size_t smem = (size_t)4 * KC * LDS * 8;
   if (p.ncta > 0 && (reinterpret_cast<uintptr_t>(SA) % 16) == 0) {
     IHS_SMEM_ATTR(gram_streamk_kernel, smem);
     int *slot_tile = reinterpret_cast<int *>(partials + (size_t)p.ncta * 2 * GT * GT);
     gram_streamk_kernel<<<p.ncta, 128, smem, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kch, p.ipc, partials,
-                                                   slot_tile);
+                                                   slot_tile, hint);
     gram_streamk_reduce_kernel<<<dim3(p.ntri, (GT * GT) / 256), 256, 0, st>>>(partials, slot_tile, (int)p.d, p.tiles,
                                                                                p.kch, p.ipc, scale * scale, H);
     lc.add(2);

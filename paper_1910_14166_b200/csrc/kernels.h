@@ -135,8 +135,9 @@ struct GramPlan {
   }
 };
 GramPlan gram_plan(int64_t m, int64_t d, int num_sms);
+// hint = 1: SA is read with an L2 evict_first policy (stream-K plans only)
 cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
-                        cudaStream_t st, LaunchCounter lc);
+                        cudaStream_t st, LaunchCounter lc, int hint = 0);
 
 // ---- a6 OLS: Cholesky solve ----------------------------------------------------
 // d <= 160: blocked Cholesky in one CTA (chol.cu); d > 160: ols_large.cu with
@@ -181,6 +182,15 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
                                  const double *L_in = nullptr, double *L_out = nullptr);
 // (L_in: use this step bound, no power iteration; L_out: power iteration only,
 // the bound written there -- the look-ahead, api.cu; warp kernel only)
+
+// ---- a1-a6 in one launch for small dense OLS problems (small_step.cu) --------
+size_t small_step_smem(int64_t n, int64_t d, int64_t m, int s);
+bool small_step_supported(int64_t n, int64_t d, int64_t m, int s);
+// x_next = x + H^{-1} g for H = (S A)^T S A, g = A^T (b - A x), S from key;
+// SA_out / g_out / H_out (optional) receive the intermediates.
+cudaError_t launch_small_step(const double *A, int64_t n, int64_t d, const double *b, const double *x, uint64_t key,
+                              int64_t row_offset, int64_t m, int s, double scale, double *x_next, double *SA_out,
+                              double *g_out, double *H_out, int *status, cudaStream_t st, LaunchCounter lc);
 
 // ---- a7 error norms ----------------------------------------------------------
 cudaError_t launch_pred_err2(int layout, int64_t n, int64_t d, const double *values, const int64_t *row_ptr,

@@ -663,3 +663,45 @@ def test_sjlt_onepass_vs_passes(P, oracle_mod):
         ref = oracle_mod.sketch_dense(A, 0, 3, m, s)
         np.testing.assert_array_equal(two, ref)
         assert rel_fro(one, ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n,d,m,s", [(2000, 10, 200, 1), (3001, 32, 512, 4), (500, 1, 7, 1), (40, 5, 64, 8)])
+def test_small_step_solve(P, oracle_mod, n, d, m, s):
+    """ihs_solve_ols on a small dense problem: one launch per iteration
+    (small_step.cu) against the oracle and against the general path."""
+    rng = np.random.default_rng(n + d)
+    A = rng.standard_normal((n, d))
+    b = A @ rng.standard_normal(d) + rng.standard_normal(n)
+    T = 6
+    xo, _ = oracle_mod.ihs_solve(A, b, m=m, s=s, T=T, iter0=2)
+    outs = []
+    for small in (1, 0):
+        ctx = P.Context(0)
+        ctx.set_option("small_step", small)
+        out = P.ihs_solve_ols(torch.from_numpy(A).to(DEV), torch.from_numpy(b).to(DEV), P.Spec(m=m, s=s), T, iter0=2,
+                              ctx=ctx)
+        assert ctx.status() == P.OK
+        xh = out["x_hist"].cpu().numpy()
+        assert iterate_parity(A, xh, xo, oracle_mod) <= 1e-9, small
+        outs.append(xh)
+    assert np.abs(outs[0] - outs[1]).max() <= 1e-10 * max(1.0, np.abs(outs[1]).max())
+
+
+@pytest.mark.parametrize("n,d,m,s", [(2000, 10, 200, 1), (40, 5, 64, 8), (3001, 32, 256, 4), (500, 1, 7, 1)])
+def test_small_step_intermediates(P, oracle_mod, n, d, m, s):
+    """ihs_small_step's SA (bit-exact for CountSketch), g, H and step against the oracle."""
+    rng = np.random.default_rng(n * d)
+    A = rng.standard_normal((n, d))
+    b = rng.standard_normal(n)
+    x = rng.standard_normal(d) * 0.1
+    xn, SA, g, H = P.ihs_small_step(torch.from_numpy(A).to(DEV), torch.from_numpy(b).to(DEV), P.Spec(m=m, s=s), 3,
+                                    torch.from_numpy(x).to(DEV), intermediates=True)
+    SAo = oracle_mod.sketch_dense(A, 0, 3, m, s)
+    assert rel_fro(SA.cpu().numpy(), SAo) <= 1e-12
+    if s == 1:
+        np.testing.assert_array_equal(SA.cpu().numpy(), SAo)
+    assert (np.abs(g.cpu().numpy() - oracle_mod.grad_dense(A, b, x)) <= grad_bound(A, b, x)).all()
+    Ho = oracle_mod.gram(SAo)
+    assert rel_fro(H.cpu().numpy(), Ho) <= 1e-12
+    xo = oracle_mod.ols_step(Ho, oracle_mod.grad_dense(A, b, x), x)
+    assert np.linalg.norm(xn.cpu().numpy() - xo) <= 1e-11 * np.linalg.norm(xo - x)
