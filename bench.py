@@ -630,9 +630,12 @@ def main():
                           "call, L2 flushed before it)") if solve_mode else
                          ("K steps, device events per step, L2 flushed between steps" if flush else
                           "K consecutive steps between two device events"),
-               "config": config_obj(cfg, world, {"per_gpu_rows": n_loc, "ols_schedule": (
+               "config": config_obj(cfg, world, {"per_gpu_rows": n_loc, "schedule": (
+                   "one-launch small step per iteration (small_step.cu)" if solve_mode else
+                   "look-ahead Gram (H_{t+1} beside the update of t and the next pass; DESIGN.md section 9)"
+                   if S.lookahead and S.la_gram_only else
                    "look-ahead (H^-1 of the next sketch beside the pass; DESIGN.md section 9)" if S.lookahead
-                   else "plain") if cfg.constraint == "ols" else None}),
+                   else "plain")}),
                "hbm_GBps_step": (cfg.a_bytes / world) / (ms_step / 1e3) / 1e9,
                "roofline": roof, "breakdown_ms": breakdown, "time_to_1e-10": ttt, "e2e": e2e,
                "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,

@@ -80,6 +80,7 @@ struct ihs_ctx_s {
   int fuse_max_d = 64;   // a4 + a6 in one cluster launch up to this d (<= 128)
   int pg_warm = 1;       // warm-started power iteration across l1 / LASSO updates
   int small_step = 1;    // small dense OLS solves: one launch per iteration (small_step.cu)
+  int pg_cluster = 0;    // PG cluster size for d <= 256 (0: the smallest that holds H)
   // Speculative sort of the NEXT iteration's buckets on a side stream: the
   // hash (hence the sort) depends only on (seed, iteration, row), not on x, so
   // after the gathers of iteration t the sort for t + 1 runs beside the
@@ -639,7 +640,7 @@ ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, dou
     const cudaError_t e = launch_l1ball_update(H, nullptr, d, nullptr, 0.0, 0, k.power_iters, k.warm_power_iters,
                                                k.inner_tol, k.lip_safety, nullptr, nullptr, ev, c->d_status,
                                                c->fstream, lc_of(c), c->pgf_warm_d == d, 0, nullptr,
-                                               c->d_L + (slot - c->fac));
+                                               c->d_L + (slot - c->fac), c->pg_cluster);
     if (e == cudaSuccess) {
       c->pgf_warm_d = d;
       slot->L_ready = true;
@@ -718,7 +719,7 @@ ihs_status l1_impl(ihs_ctx c, const double *H, const double *g, int64_t d, const
   Prof pr(c, IHS_K_PG);
   IHS_CUDA(launch_l1ball_update(H, g, d, x, radius, k.max_inner, k.power_iters, k.warm_power_iters, k.inner_tol,
                                 k.lip_safety, xn, inner, ev, c->d_status, c->stream, lc_of(c), warm, prox, L_in,
-                                nullptr));
+                                nullptr, c->pg_cluster));
   if (warm_env && !L_in) c->pg_warm_d = d;
   return IHS_OK;
 }
@@ -790,9 +791,10 @@ ihs_status ols_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_s
   return IHS_OK;
 }
 
-// Look-ahead for the l1 ball / LASSO (constraint 1 / 2): the Gram of S^{t+1} A
-// (formed by pass t with g^t) runs on the factor stream beside the PG update of
-// iteration t; the update of t + 1 then finds H_{t+1} ready.  T + 1 passes.
+// Look-ahead for the l1 ball / LASSO (prox 0 / 1), and the Gram-only form for
+// OLS with d > 256 (prox -1): the Gram of S^{t+1} A (formed by pass t with g^t)
+// runs on the factor stream beside the update of iteration t and the next
+// pass; the update of t + 1 then finds H_{t+1} ready.  T + 1 passes.
 ihs_status pg_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, const double *b,
                              uint64_t iter0, int32_t T, double *xh, double radius, const ihs_inner_cfg *cfg,
                              int32_t *inner_dev, int prox) {
@@ -819,7 +821,10 @@ ihs_status pg_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_sp
     IHS_TRY(sketch_grad_impl(c, A, spec, iter0 + (uint64_t)t + 1, b, x, more ? SAn : nullptr, gn));
     IHS_TRY(more ? allreduce(SAn, pk) : allreduce(gn, d));
     if (more) IHS_TRY(gram_side_impl(c, SAn, m, d, 1.0, H + nxt * d * d));
-    IHS_TRY(l1_impl(c, H + cur * d * d, gn, d, x, radius, cfg, xh + (int64_t)(t + 1) * d, inner_dev + t, prox));
+    if (prox < 0)  // OLS with the Gram-only look-ahead (d > 256: the CG / Cholesky update)
+      IHS_TRY(ols_impl(c, H + cur * d * d, gn, d, x, xh + (int64_t)(t + 1) * d));
+    else
+      IHS_TRY(l1_impl(c, H + cur * d * d, gn, d, x, radius, cfg, xh + (int64_t)(t + 1) * d, inner_dev + t, prox));
   }
   return IHS_OK;
 }
@@ -853,6 +858,16 @@ ihs_status allreduce_impl(ihs_ctx c, double *buf, int64_t count) {
   if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
   if (g_nccl.AllReduce(buf, buf, (size_t)count, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0) return IHS_ERR_COMM;
   return IHS_OK;
+}
+
+// OLS with d > 256 (a CG / Cholesky update, e.g. C3): only the Gram looks
+// ahead, when it is long (m d^2 >= 2^32 multiply-adds: C3 0.30 ms).  Measured
+// on C3: 0.776 -> 0.699 ms/step (the Gram beside the CG and the next CSR pass).
+bool use_lookahead_gram_ols(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spec *spec, int32_t T) {
+  const int64_t d = A->n_cols;
+  const bool ok = d > 256 && spec->m >= 1 && T >= 1 && ols_large_supported(d);
+  if (c->lookahead >= 0) return ok && c->lookahead != 0;
+  return ok && T >= 3 && (double)spec->m * (double)d * (double)d >= 4294967296.0;
 }
 
 // Rows per rank that the schedule decision uses: the local count on one rank;
@@ -950,12 +965,14 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
   if (!trace) IHS_TRY(rows_for_schedule(c, n, &rows));
   const bool lookahead =
       !trace && (constraint == 0 ? use_lookahead(c, &A, rows, spec, T) : use_lookahead_pg(c, &A, rows, spec, T));
+  const bool la_gram_ols = !trace && constraint == 0 && !lookahead && use_lookahead_gram_ols(c, &A, spec, T);
+  if (la_gram_ols) IHS_TRY(pg_lookahead_loop(c, &A, spec, b, iter0, T, xh, 0.0, cfg, nullptr, -1));
   if (lookahead && constraint == 0) IHS_TRY(ols_lookahead_loop(c, &A, spec, b, iter0, T, xh));
   if (lookahead && constraint >= 1)
     IHS_TRY(pg_lookahead_loop(c, &A, spec, b, iter0, T, xh, radius, cfg, inner_dev, constraint == 2 ? 1 : 0));
   // a small dense OLS problem on one rank: each iteration is one launch of one
   // CTA (small_step.cu; launch latency dominates the multi-kernel path there)
-  const bool small = !lookahead && c->small_step && c->world == 1 && constraint == 0 &&
+  const bool small = !lookahead && !la_gram_ols && c->small_step && c->world == 1 && constraint == 0 &&
                      A.layout == IHS_DENSE_ROW_MAJOR && small_step_supported(n, d, m, spec->s);
   for (int32_t t = 0; small && t < T; ++t) {
     const double *x = xh + (int64_t)t * d;
@@ -985,7 +1002,7 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
       }
     }
   }
-  for (int32_t t = 0; !lookahead && !small && t < T; ++t) {
+  for (int32_t t = 0; !lookahead && !la_gram_ols && !small && t < T; ++t) {
     const double *x = xh + (int64_t)t * d;
     double *xn = xh + (int64_t)(t + 1) * d;
     if (trace) cudaEventRecord(ev[0], st);
@@ -1089,6 +1106,7 @@ ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
   if (const char *e = getenv("IHS_OLS")) c->ols_large = !std::strcmp(e, "chol") ? 2 : !std::strcmp(e, "cg") ? 0 : 1;
   if (const char *e = getenv("IHS_FUSE")) c->fuse_max_d = !std::strcmp(e, "0") ? 0 : 128;
   if (const char *e = getenv("IHS_PG_WARM")) c->pg_warm = std::strcmp(e, "0") != 0;
+  if (const char *e = getenv("IHS_PG_CLUSTER")) c->pg_cluster = atoi(e);
   *out = c;
   return IHS_OK;
 }
@@ -1158,6 +1176,7 @@ const OptionDef kOptions[] = {
     {"lookahead", &ihs_ctx_s::lookahead, -1, 1},   {"sjlt_onepass", &ihs_ctx_s::sjlt_onepass, 0, 1},
     {"ols_large", &ihs_ctx_s::ols_large, 0, 2},    {"fuse_max_d", &ihs_ctx_s::fuse_max_d, 0, 128},
     {"pg_warm", &ihs_ctx_s::pg_warm, 0, 1},       {"small_step", &ihs_ctx_s::small_step, 0, 1},
+    {"pg_cluster", &ihs_ctx_s::pg_cluster, 0, 16},
 };
 }  // namespace
 

@@ -179,7 +179,7 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
                                  double *x_next,
                                  int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
                                  LaunchCounter lc, bool warm_start = false, int prox = 0,
-                                 const double *L_in = nullptr, double *L_out = nullptr);
+                                 const double *L_in = nullptr, double *L_out = nullptr, int cluster_pref = 0);
 // (L_in: use this step bound, no power iteration; L_out: power iteration only,
 // the bound written there -- the look-ahead, api.cu; warp kernel only)
 

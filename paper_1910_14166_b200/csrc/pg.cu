@@ -545,10 +545,15 @@ size_t pg_scratch_bytes(int64_t d) { return (size_t)d * 8; }
 cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, const double *x, double radius,
                                  int max_inner, int power_iters, int warm_power_iters, double tol, double safety,
                                  double *x_next, int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
-                                 LaunchCounter lc, bool warm_start, int prox, const double *L_in, double *L_out) {
+                                 LaunchCounter lc, bool warm_start, int prox, const double *L_in, double *L_out,
+                                 int cluster_pref) {
   // d <= 256: the warp-per-iterate cluster kernel; larger d: the CTA-level
-  // cluster kernel while H fits the cluster's shared memory, else one CTA
-  const int cs = pg_cluster_size(d);
+  // cluster kernel while H fits the cluster's shared memory, else one CTA.
+  // cluster_pref (2..16, a power of two): a wider cluster for the warp kernel
+  // -- fewer rows of the H v product per warp, one more barrier participant
+  int cs = pg_cluster_size(d);
+  if (cs > 0 && d <= 256 && cluster_pref > cs && (cluster_pref & (cluster_pref - 1)) == 0 && cluster_pref <= 16)
+    cs = cluster_pref;
   if (cs > 0) {
     const int64_t R = (d + cs - 1) / cs;
     const bool wv = d <= 256;

@@ -88,6 +88,8 @@ def lookahead_default(A, d: int, spec: P.Spec, constraint: str = "ols", rows: in
     env = os.environ.get("IHS_LOOKAHEAD")
     if env is not None:  # forced: any matrix (OLS with d > 128 or CSR: the Gram-only form)
         return d >= 1 and env != "0"
+    if constraint == "ols" and d > 256:  # the Gram-only look-ahead, when the Gram is long (C3; api.cu)
+        return spec.m * d * d >= (1 << 32)
     ok = isinstance(A, P.Dense) and d >= 1 and (d <= 128 or constraint != "ols")
     return ok and spec.s == 1 and (A.n if rows is None else rows) * d >= (1 << 27)
 

@@ -133,7 +133,7 @@ def test_csr_full_size(P, oracle_mod):
     ctx = P.Context(0)
     from paper_1910_14166_b200.dist import CudaOps, ShardedIHS
     spec = P.Spec(m=cfg.m, s=cfg.s)
-    S = ShardedIHS(P.Csr(rp, cl, vl, d), prob["b"], spec, ops=CudaOps(ctx))
+    S = ShardedIHS(P.Csr(rp, cl, vl, d), prob["b"], spec, ops=CudaOps(ctx), lookahead=False)
     x = torch.from_numpy(np.random.default_rng(1).standard_normal(d) * 0.1).to(DEV)
     xn = torch.empty_like(x)
     S.step(t, x, xn)
