@@ -225,6 +225,12 @@ def roofline(prof, cfg, n_loc, nnz_loc, steps):
     out["traffic"] = traffic
     if isinstance(tr, dict):
         out["traffic_source"] = tr.get("source")
+    if name == "csr" and kind == "l2_red":
+        # the same pass against HBM: the CSR stream (8 B row_ptr + 8 B b per row, 12 B per nonzero), x and the SA write
+        hb = 16.0 * n_loc + 12.0 * nnz_loc + 8.0 * cfg.m * cfg.d
+        ach_h = hb / (avg / 1e3) / 1e9
+        out["hbm"] = {"achieved": ach_h, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": ach_h / peaks["hbm_gbs"],
+                      "algorithmic_bytes_per_launch": hb}
     if name == "sjlt" and kind == "hbm":
         # the pass is bound by shared-memory bandwidth, not HBM: every element of A is
         # written to shared memory once (TMA) and read once per SJLT block by its bucket's owner thread

@@ -12,6 +12,7 @@ namespace {
 constexpr int GT = 64;       // CTA tile edge
 constexpr int KC = 32;       // rows of SA per smem stage
 constexpr int LDS = GT + 4;  // padded row stride (== 4 mod 16 doubles: conflict-free fragments)
+constexpr int kStagesK = 2;  // stream-K kernel: double-buffered stages (3 measured slower on C3: 0.333 vs 0.324 ms)
 
 __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -164,8 +165,8 @@ __global__ void __launch_bounds__(128) gram_streamk_kernel(const double *__restr
                                                            double *__restrict__ partials, int *__restrict__ slot_tile,
                                                            int hint) {
   extern __shared__ double sm[];
-  double *Xp = sm;                 // [2][KC][LDS]
-  double *Xq = sm + 2 * KC * LDS;  // [2][KC][LDS]
+  double *Xp = sm;                         // [kStagesK][KC][LDS]
+  double *Xq = sm + kStagesK * KC * LDS;  // [kStagesK][KC][LDS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;
   const int64_t total = (int64_t)ntri * kch;
@@ -325,10 +326,11 @@ cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, doubl
                         cudaStream_t st, LaunchCounter lc, int hint) {
   const size_t smem = (size_t)4 * KC * LDS * 8;
   if (p.ncta > 0 && (reinterpret_cast<uintptr_t>(SA) % 16) == 0) {
-    IHS_SMEM_ATTR(gram_streamk_kernel, smem);
+    const size_t smem_sk = (size_t)2 * kStagesK * KC * LDS * 8;
+    IHS_SMEM_ATTR(gram_streamk_kernel, smem_sk);
     int *slot_tile = reinterpret_cast<int *>(partials + (size_t)p.ncta * 2 * GT * GT);
-    gram_streamk_kernel<<<p.ncta, 128, smem, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kch, p.ipc, partials,
-                                                   slot_tile, hint);
+    gram_streamk_kernel<<<p.ncta, 128, smem_sk, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kch, p.ipc, partials,
+                                                      slot_tile, hint);
     gram_streamk_reduce_kernel<<<dim3(p.ntri, (GT * GT) / 256), 256, 0, st>>>(partials, slot_tile, (int)p.d, p.tiles,
                                                                                p.kch, p.ipc, scale * scale, H);
     lc.add(2);

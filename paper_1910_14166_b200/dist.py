@@ -131,6 +131,10 @@ class ShardedIHS:
         self.g = self.pack[m * d:]
         self.H = torch.empty((d, d), dtype=torch.float64, device=dev)
         self.inner = torch.zeros(1, dtype=torch.int32, device=dev)
+        if lookahead is None and hasattr(self.ops, "ctx"):  # the context's option (ihs_ctx_set_option), if set
+            opt = self.ops.ctx.get_option("lookahead")
+            if opt >= 0:
+                lookahead = bool(opt)
         if lookahead is None:
             # the same decision on every rank: rows per rank from the global n
             nt = torch.tensor([float(A.n)], dtype=torch.float64, device=dev)

@@ -16,7 +16,7 @@ import json
 import subprocess
 import sys
 
-OURS = ("cs_", "scan_", "gram", "chol", "potrf", "trsm", "syrk", "backsolve", "aug_fill", "reduce_rows", "sjlt",
+OURS = ("cs_", "scan_", "gram", "chol", "potrf", "trsm", "syrk", "backsolve", "aug_fill", "reduce_rows", "sjlt", "small_",
         "sum_splits", "csr_", "pg_", "grad_", "scale_", "sqnorm", "hash_", "ols_", "axpy")
 
 
