@@ -40,6 +40,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "ihs.h"))
     objs, jobs = [], []
+    live = {os.path.basename(src)[:-3] + ".o" for src in sources()}
+    for f in os.listdir(OBJ):  # objects of deleted sources (never linked; keep SASS summaries honest)
+        if f.endswith(".o") and f not in live:
+            os.remove(os.path.join(OBJ, f))
     for src in sources():
         obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)

@@ -308,10 +308,8 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
   // dense.  CountSketch (s = 1): a stable counting sort of the rows by bucket
   // and one bucket-ordered gather, with the gradient riding on the same read
   // of A.  SJLT (s > 1): the same per block j (s stacked
-  // CountSketches; s reads of A, bit-identical to the oracle).  IHS_SJLT=stream
-  // selects one streaming pass of shared-memory tiles over A (sjlt_stream.cu,
-  // plus a separate gradient pass), IHS_SJLT=tile the older per-CTA tile
-  // kernel; both measured slower on B200.
+  // CountSketches; s reads of A, bit-identical to the oracle) when the
+  // "sjlt_onepass" option is 0; by default one read of A (below).
   const int64_t M = m / s;
   SjltOnepassPlan op;
   if (SA && s > 1 && c->sjlt_onepass && n > 0 && sjlt_onepass_plan(n, d, m, s, c->num_sms, A->values, op)) {
@@ -368,7 +366,7 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
       // that a launch has about two waves of bucket CTAs (7 per SM resident)
       // even when M = m / s is small: the gradient-carrying block's slower CTAs
       // then share a launch with three others (C5: 35.4 -> 34.4 ms/step against
-      // one wave; IHS_SJLT_NB=k overrides).  The sort buffers hold all s blocks; two sets, so
+      // one wave).  The sort buffers hold all s blocks; two sets, so
       // the next iteration's sort can be prefetched into the other set.
       const bool tma = cs_gather_tma_supported(d, A->values);
       const int nb = !tma ? 1

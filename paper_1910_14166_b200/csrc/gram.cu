@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) gram_streamk_reduce_kernel(const double *
 
 }  // namespace
 
-GramPlan gram_plan(int64_t m, int64_t d, int num_sms) {
+GramPlan gram_plan(int64_t m, int64_t d, int num_sms, int ctas_per_sm) {
   GramPlan p;
   p.m = m;
   p.d = d;
@@ -301,7 +301,7 @@ GramPlan gram_plan(int64_t m, int64_t d, int num_sms) {
   // stream-K for many tiles: 2 CTAs per SM, k-chunks per tile chosen so that
   // the items divide as evenly as possible over the CTAs (>= 64 rows a chunk)
   if (p.ntri >= 16 && d % 2 == 0 && m >= 256) {
-    const int64_t ncta = 2 * (int64_t)num_sms;
+    const int64_t ncta = (int64_t)ctas_per_sm * num_sms;
     const int64_t kmin = std::max<int64_t>(1, (2 * ncta + p.ntri - 1) / p.ntri);
     const int64_t kmax = std::max<int64_t>(kmin, m / 64);
     int64_t best = kmin;

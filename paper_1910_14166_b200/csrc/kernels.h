@@ -134,7 +134,7 @@ struct GramPlan {
     return std::max((size_t)nsplit * ntri * 64 * 64 * 8, sk);
   }
 };
-GramPlan gram_plan(int64_t m, int64_t d, int num_sms);
+GramPlan gram_plan(int64_t m, int64_t d, int num_sms, int ctas_per_sm = 2);
 // hint = 1: SA is read with an L2 evict_first policy (stream-K plans only)
 cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
                         cudaStream_t st, LaunchCounter lc, int hint = 0);

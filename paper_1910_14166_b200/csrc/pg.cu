@@ -307,6 +307,50 @@ __global__ void __launch_bounds__(kCT) pg_cluster_kernel(const double *__restric
 // so an inner step has no CTA barrier, only the one cluster barrier after the
 // z rows are exchanged.  The GEMV interleaves a warp's rows (independent fp64
 // chains) and reduces them with one transpose-reduce.
+#ifdef IHS_PG_TIMING
+// tools/probe/pg_timing.cu only (never in the library build): per-phase clock
+// sums of the inner loop, measured by thread 0 of cluster rank 0.
+__device__ long long g_pg_timing[8];
+#define PGT_MARK(v) long long v = clock64()
+#define PGT_ADD(i, a, b) \
+  if (rank == 0 && tid == 0) g_pg_timing[i] += (b) - (a)
+#else
+#define PGT_MARK(v)
+#define PGT_ADD(i, a, b)
+#endif
+
+// The z exchange without a cluster barrier: every owner lane sends its row
+// value to each CTA with st.async, which completes bytes on the RECEIVING
+// CTA's mbarrier for that buffer; a CTA waits on its own mbarrier only (d * 8
+// bytes per step, armed by its thread 0).  Reuse of buffer par two steps later
+// is safe: a CTA can only send step k+2 rows after its step k+1 wait, which
+// needs every CTA's step k+1 rows, which each CTA sends only after it has read
+// its step k z.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_f64(uint32_t addr, double v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(addr),
+               "l"(__double_as_longlong(v)), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void zbar_arm(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void zbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "ZW_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra ZW_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 template <int K>
 __device__ __forceinline__ double wsum_k(const double (&v)[K]) {
   double t = 0.0;
@@ -332,7 +376,13 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
   double *Hs = sm;                   // R x d (my rows)
   double *gs = Hs + (size_t)R * d;   // R (my rows of g)
   double *zb = gs + R;               // 2 x d : z (or H v), double-buffered by step parity
+  uint64_t *zbar = reinterpret_cast<uint64_t *>(zb + 2 * d);  // 2 mbarriers: zb[0], zb[1] complete
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&zbar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&zbar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   load_rows(Hs, H + (int64_t)r0 * d, (int64_t)(r1 - r0) * d, tid, kCT);
   for (int i = tid; i < r1 - r0; i += kCT) gs[i] = g ? g[r0 + i] : 0.0;
   double xv[K], yv[K], vv[K], wv[K];
@@ -348,9 +398,11 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
   }
   cluster.sync();
   int par = 0;
+  uint32_t zph = 0;  // bit b: the phase parity of zbar[b]
   // rows p of this warp: out_p = pg ? y_p - ((H w)_p - g_p) / L : (H w)_p,
-  // written into every CTA's zb[par]; then the cluster barrier.
+  // sent into every CTA's zb[par]; then this CTA's wait for all d rows.
   auto gemv_bcast = [&](bool pg_step, double L) {
+    if (tid == 0) zbar_arm(&zbar[par], (uint32_t)d * 8u);
     for (int pb = r0 + 8 * warp; pb < r1; pb += 8 * kCW) {
       double acc[8];
 #pragma unroll
@@ -380,10 +432,16 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
         if (p < r1) val = yp - (val - gs[p - r0]) / L;
       }
       // the row's owner lane publishes it to every CTA of the cluster
-      if (owner_lane_of_row<8>(u) == lane && p < r1)
-        for (int r = 0; r < cs; ++r) cluster.map_shared_rank(zb + par * d, r)[p] = val;
+      if (owner_lane_of_row<8>(u) == lane && p < r1) {
+        const uint32_t za = smem_addr(zb + par * d + p), ba = smem_addr(&zbar[par]);
+        for (int r = 0; r < cs; ++r) st_async_f64(cluster_addr(za, r), val, cluster_addr(ba, r));
+      }
     }
-    cluster.sync();
+    PGT_MARK(tw0);
+    zbar_wait(&zbar[par], (zph >> par) & 1u);
+    PGT_MARK(tw1);
+    PGT_ADD(1, tw0, tw1);
+    zph ^= 1u << par;
   };
   // L_in: the step bound was formed beside the previous pass (look-ahead,
   // api.cu) -- no power iteration here
@@ -424,9 +482,11 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
   double tk = 1.0;  // FISTA momentum parameter (accel) -- plain PG keeps vv = yv
   double theta_prev = 0.0;  // the last projection threshold (warm start; IHS_PG_THETA_WARM=0: off)
   while (kk < max_inner) {
+    PGT_MARK(ts0);
 #pragma unroll
     for (int k = 0; k < K; ++k) wv[k] = vv[k] - xv[k];
     gemv_bcast(true, L);
+    PGT_MARK(ts1);
     const double *z = zb + par * d;
     double zv[K], av[K];
 #pragma unroll
@@ -472,6 +532,7 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
       }
       theta_prev = theta;
     }
+    PGT_MARK(ts2);
     double dn[K], yy[K], rs[K], ynv[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -507,6 +568,11 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
     for (int k = 0; k < K; ++k) yv[k] = ynv[k];
     par ^= 1;
     ++kk;
+    PGT_MARK(ts3);
+    PGT_ADD(0, ts0, ts1);
+    PGT_ADD(2, ts1, ts2);
+    PGT_ADD(3, ts2, ts3);
+    PGT_ADD(4, ts0, ts3);
     if (sqrt(dnn) <= tol * fmax(1.0, sqrt(yyy))) {
       converged = true;
       break;
@@ -560,7 +626,7 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     const int64_t R = (d + cs - 1) / cs;
     const bool wv = d <= 256;
     const size_t smem =
-        std::max(wv ? (size_t)(R * d + R + 2 * d) * 8 : (size_t)(R * d + 6 * d) * 8, kExclusiveSmem);
+        std::max(wv ? (size_t)(R * d + R + 2 * d) * 8 + 16 : (size_t)(R * d + 6 * d) * 8, kExclusiveSmem);
     auto wkern = d <= 32 ? pg_warp_kernel<1> : d <= 64 ? pg_warp_kernel<2> : d <= 128 ? pg_warp_kernel<4>
                                                                              : pg_warp_kernel<8>;
     const void *kern = wv ? (const void *)wkern : (const void *)pg_cluster_kernel;

@@ -649,20 +649,25 @@ def test_reduce_argument_single_rank(P):
     assert torch.equal(P.ihs_grad(A, b, x, reduce=True), P.ihs_grad(A, b, x))
 
 
-def test_sjlt_onepass_vs_passes(P, oracle_mod):
-    """The one-read SJLT sketch against the s sorted passes (bit-identical to the
-    oracle) and the oracle, with a ragged last chunk and d not a multiple of 4."""
-    rng = np.random.default_rng(8)
-    for n, d, m, s in [(70_001, 98, 4096, 8), (9_999, 10, 256, 2), (4_097, 6, 2048, 4)]:
-        A = rng.standard_normal((n, d))
-        Ad = torch.from_numpy(A).to(DEV)
-        c1, c0 = P.Context(0), P.Context(0)
-        c0.set_option("sjlt_onepass", 0)
-        one = P.ihs_sketch(Ad, P.Spec(m=m, s=s), 3, ctx=c1).cpu().numpy()
-        two = P.ihs_sketch(Ad, P.Spec(m=m, s=s), 3, ctx=c0).cpu().numpy()
-        ref = oracle_mod.sketch_dense(A, 0, 3, m, s)
-        np.testing.assert_array_equal(two, ref)
-        assert rel_fro(one, ref) <= 1e-12
+@pytest.mark.parametrize("n,d,m,s", [(70_001, 98, 4096, 8), (9_999, 10, 256, 2), (4_097, 6, 2048, 4),
+                                     (30_001, 34, 1536, 8), (5_000, 18, 384, 4), (12_345, 66, 1152, 6),
+                                     (3_000, 12, 3 * 170, 3), (1_025, 2, 16, 8), (2_049, 100, 4096, 8)])
+def test_sjlt_onepass_vs_passes(P, oracle_mod, n, d, m, s):
+    """The one-read SJLT sketch against the s sorted passes (bit-identical to
+    the oracle) and the oracle: ragged last chunks, d not a multiple of 4, the
+    M = m / s range 2 .. 512, s in 2 .. 8."""
+    rng = np.random.default_rng(n + d)
+    A = rng.standard_normal((n, d))
+    Ad = torch.from_numpy(A).to(DEV)
+    ref = oracle_mod.sketch_dense(A, 0, 3, m, s)
+    outs = {}
+    for opt in (0, 1):
+        ctx = P.Context(0)
+        ctx.set_option("sjlt_onepass", opt)
+        outs[opt] = P.ihs_sketch(Ad, P.Spec(m=m, s=s), 3, ctx=ctx).cpu().numpy()
+        assert ctx.status() == P.OK
+    np.testing.assert_array_equal(outs[0], ref)
+    assert rel_fro(outs[1], ref) <= 1e-12
 
 
 @pytest.mark.parametrize("n,d,m,s", [(2000, 10, 200, 1), (3001, 32, 512, 4), (500, 1, 7, 1), (40, 5, 64, 8)])
