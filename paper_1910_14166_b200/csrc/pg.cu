@@ -8,6 +8,7 @@
 // Michelot's fixed-point iteration, which reaches the same theta as the sorted
 // rule of the oracle (R8) in exact arithmetic.
 #include <algorithm>
+#include <type_traits>
 #include <cstdlib>
 #include <cstring>
 
@@ -312,8 +313,7 @@ __global__ void __launch_bounds__(kCT) pg_cluster_kernel(const double *__restric
 // sums of the inner loop, measured by thread 0 of cluster rank 0.
 __device__ long long g_pg_timing[8];
 #define PGT_MARK(v) long long v = clock64()
-#define PGT_ADD(i, a, b) \
-  if (rank == 0 && tid == 0) g_pg_timing[i] += (b) - (a)
+#define PGT_ADD(i, a, b) pgt_acc[i] += (b) - (a)
 #else
 #define PGT_MARK(v)
 #define PGT_ADD(i, a, b)
@@ -351,6 +351,40 @@ __device__ __forceinline__ void zbar_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
 }
 
+// FISTA momentum (t_{j+1} = (1 + sqrt(1 + 4 t_j^2)) / 2 from t_0 = 1, coef_j =
+// (t_j - 1) / t_{j+1}), tabulated at compile time for the first kFistaTab steps
+// after a (re)start; later steps compute it.
+constexpr int kFistaTab = 128;
+constexpr double cx_sqrt(double x) {
+  double r = x > 1.0 ? x : 1.0;
+  for (int i = 0; i < 200; ++i) r = 0.5 * (r + x / r);
+  return r;
+}
+struct FistaTab {
+  double c[kFistaTab];
+  double t_last;
+  constexpr FistaTab() : c(), t_last(1.0) {
+    double t = 1.0;
+    for (int j = 0; j < kFistaTab; ++j) {
+      const double tn = 0.5 * (1.0 + cx_sqrt(1.0 + 4.0 * t * t));
+      c[j] = (t - 1.0) / tn;
+      t = tn;
+    }
+    t_last = t;
+  }
+};
+__constant__ FistaTab kFista = FistaTab();
+__device__ __forceinline__ double fista_coef(int j) {
+  if (j < kFistaTab) return kFista.c[j];
+  double t = kFista.t_last;  // (rare: > 128 steps without a restart)
+  double tn = t;
+  for (int i = kFistaTab; i <= j; ++i) {
+    tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t * t));
+    if (i < j) t = tn;
+  }
+  return (t - 1.0) / tn;
+}
+
 template <int K>
 __device__ __forceinline__ double wsum_k(const double (&v)[K]) {
   double t = 0.0;
@@ -359,8 +393,14 @@ __device__ __forceinline__ double wsum_k(const double (&v)[K]) {
   return warp_sum(t);
 }
 
+// 4 warps (one per SM sub-partition): every warp repeats the projection and
+// the norms on the whole iterate, so more warps only share issue slots (8 warps
+// measured 2665 cycles per LASSO step at d = 256 on 8 CTAs).
+constexpr int kWT = 128;
+constexpr int kWW = kWT / 32;
+
 template <int K>
-__global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restrict__ H, const double *__restrict__ g,
+__global__ void __launch_bounds__(kWT, 1) pg_warp_kernel(const double *__restrict__ H, const double *__restrict__ g,
                                                       int d, const double *__restrict__ x, double radius,
                                                       int max_inner, int power_iters, double tol, double safety,
                                                       double *x_next, int32_t *inner_iters, int *status, int accel,
@@ -383,8 +423,8 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&zbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  load_rows(Hs, H + (int64_t)r0 * d, (int64_t)(r1 - r0) * d, tid, kCT);
-  for (int i = tid; i < r1 - r0; i += kCT) gs[i] = g ? g[r0 + i] : 0.0;
+  load_rows(Hs, H + (int64_t)r0 * d, (int64_t)(r1 - r0) * d, tid, kWT);
+  for (int i = tid; i < r1 - r0; i += kWT) gs[i] = g ? g[r0 + i] : 0.0;
   double xv[K], yv[K], vv[K], wv[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
@@ -399,14 +439,20 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
   cluster.sync();
   int par = 0;
   uint32_t zph = 0;  // bit b: the phase parity of zbar[b]
+#ifdef IHS_PG_TIMING
+  long long pgt_acc[5] = {0, 0, 0, 0, 0};
+#endif
   // rows p of this warp: out_p = pg ? y_p - ((H w)_p - g_p) / L : (H w)_p,
-  // sent into every CTA's zb[par]; then this CTA's wait for all d rows.
-  auto gemv_bcast = [&](bool pg_step, double L) {
-    if (tid == 0) zbar_arm(&zbar[par], (uint32_t)d * 8u);
-    for (int pb = r0 + 8 * warp; pb < r1; pb += 8 * kCW) {
-      double acc[8];
+  // sent into every CTA's zb[par]; then this CTA's wait for all d rows.  U
+  // rows per warp pass, U = R / (warps) when that is 2, 4 or 8, so that every
+  // warp of the CTA takes part (R = 32 at d = 256 on 8 CTAs: 8 rows a warp).
+  const int U_sel = R >= 8 * kWW ? 8 : R >= 4 * kWW ? 4 : R >= 2 * kWW ? 2 : 1;
+  auto gemv_rows = [&](auto uc, bool pg_step, double invL) {
+    constexpr int U = decltype(uc)::value;
+    for (int pb = r0 + U * warp; pb < r1; pb += U * kWW) {
+      double acc[U];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < U; ++u) {
         const int p = pb + u;
         const double *hr = Hs + (size_t)(min(p, r1 - 1) - r0) * d;
         double a = 0.0;
@@ -417,8 +463,8 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
         }
         acc[u] = a;
       }
-      transpose_reduce<8>(acc, lane);
-      const int u = reduced_row_of_lane<8>(lane);
+      transpose_reduce<U>(acc, lane);
+      const int u = reduced_row_of_lane<U>(lane);
       const int p = pb + u;
       double val = acc[0];
       if (pg_step) {  // warp-uniform; the shuffles run in every lane
@@ -429,14 +475,21 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
           const double t = __shfl_sync(0xffffffffu, vv[k], p & 31);
           if ((p >> 5) == k) yp = t;
         }
-        if (p < r1) val = yp - (val - gs[p - r0]) / L;
+        if (p < r1) val = fma(-(val - gs[p - r0]), invL, yp);
       }
       // the row's owner lane publishes it to every CTA of the cluster
-      if (owner_lane_of_row<8>(u) == lane && p < r1) {
+      if (owner_lane_of_row<U>(u) == lane && p < r1) {
         const uint32_t za = smem_addr(zb + par * d + p), ba = smem_addr(&zbar[par]);
         for (int r = 0; r < cs; ++r) st_async_f64(cluster_addr(za, r), val, cluster_addr(ba, r));
       }
     }
+  };
+  auto gemv_bcast = [&](bool pg_step, double invL) {
+    if (tid == 0) zbar_arm(&zbar[par], (uint32_t)d * 8u);
+    if (U_sel == 8) gemv_rows(std::integral_constant<int, 8>(), pg_step, invL);
+    else if (U_sel == 4) gemv_rows(std::integral_constant<int, 4>(), pg_step, invL);
+    else if (U_sel == 2) gemv_rows(std::integral_constant<int, 2>(), pg_step, invL);
+    else gemv_rows(std::integral_constant<int, 1>(), pg_step, invL);
     PGT_MARK(tw0);
     zbar_wait(&zbar[par], (zph >> par) & 1u);
     PGT_MARK(tw1);
@@ -465,6 +518,7 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
     par ^= 1;
   }
   const double L = L_in ? *L_in : (lam > 0.0) ? safety * lam : 1.0;
+  const double invL = 1.0 / L;
   if (!L_in && evec && rank == 0 && warp == 0 && lam > 0.0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -479,13 +533,13 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
   }
   int kk = 0;
   bool converged = false;
-  double tk = 1.0;  // FISTA momentum parameter (accel) -- plain PG keeps vv = yv
+  int tj = 0;  // FISTA: steps since the last restart (accel) -- plain PG keeps vv = yv
   double theta_prev = 0.0;  // the last projection threshold (warm start; IHS_PG_THETA_WARM=0: off)
   while (kk < max_inner) {
     PGT_MARK(ts0);
 #pragma unroll
     for (int k = 0; k < K; ++k) wv[k] = vv[k] - xv[k];
-    gemv_bcast(true, L);
+    gemv_bcast(true, invL);
     PGT_MARK(ts1);
     const double *z = zb + par * d;
     double zv[K], av[K];
@@ -510,16 +564,16 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
       theta = warm_th ? theta_prev : (n1 - radius) / (double)d;
       double cprev = warm_th ? -1.0 : (double)d;
       for (int guard = 0; guard <= d + 1; ++guard) {
-        double Sv = 0.0, cv = 0.0;
+        double Sv = 0.0;
+        int ci = 0;  // the active count from ballots (exact; no shuffle chain)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-          if (av[k] > theta) {
-            Sv += av[k];
-            cv += 1.0;
-          }
+          const bool act = av[k] > theta;
+          if (act) Sv += av[k];
+          ci += __popc(__ballot_sync(0xffffffffu, act));
         }
         Sv = warp_sum(Sv);
-        cv = warp_sum(cv);
+        const double cv = (double)ci;
         if (cv == 0.0 && warm_th) {  // started above every |z|: cold start instead
           warm_th = false;
           theta = (n1 - radius) / (double)d;
@@ -533,7 +587,10 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
       theta_prev = theta;
     }
     PGT_MARK(ts2);
-    double dn[K], yy[K], rs[K], ynv[K];
+    // ||y+ - y||^2, ||y||^2 and the restart test in ONE interleaved warp
+    // reduction; FISTA's momentum from a table (no sqrt / divide on the step's
+    // critical path); convergence compared in squares.
+    double ynv[K], s3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       double yn = zv[k];
@@ -542,24 +599,26 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
         yn = a > 0.0 ? (zv[k] < 0.0 ? -a : a) : 0.0;
       }
       const double e = yn - yv[k];
-      dn[k] = e * e;
-      yy[k] = yv[k] * yv[k];
-      rs[k] = (vv[k] - yn) * e;  // gradient-based restart test (O'Donoghue & Candes)
+      s3[0] = fma(e, e, s3[0]);
+      s3[1] = fma(yv[k], yv[k], s3[1]);
+      s3[2] = fma(vv[k] - yn, e, s3[2]);  // gradient-based restart test (O'Donoghue & Candes)
       ynv[k] = yn;
     }
-    const double dnn = wsum_k(dn), yyy = wsum_k(yy);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) s3[i] += __shfl_xor_sync(0xffffffffu, s3[i], o);
+    const double dnn = s3[0], yyy = s3[1];
     if (accel & 1) {
-      const double rsum = wsum_k(rs);
       double coef = 0.0;
-      if (rsum > 0.0) {
-        tk = 1.0;  // restart: the next step is a plain projected-gradient step
+      if (s3[2] > 0.0) {
+        tj = 0;  // restart: the next step is a plain projected-gradient step
       } else {
-        const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * tk * tk));
-        coef = (tk - 1.0) / tn;
-        tk = tn;
+        coef = fista_coef(tj);
+        ++tj;
       }
 #pragma unroll
-      for (int k = 0; k < K; ++k) vv[k] = ynv[k] + coef * (ynv[k] - yv[k]);
+      for (int k = 0; k < K; ++k) vv[k] = fma(coef, ynv[k] - yv[k], ynv[k]);
     } else {
 #pragma unroll
       for (int k = 0; k < K; ++k) vv[k] = ynv[k];
@@ -573,12 +632,16 @@ __global__ void __launch_bounds__(kCT, 1) pg_warp_kernel(const double *__restric
     PGT_ADD(2, ts1, ts2);
     PGT_ADD(3, ts2, ts3);
     PGT_ADD(4, ts0, ts3);
-    if (sqrt(dnn) <= tol * fmax(1.0, sqrt(yyy))) {
+    if (dnn <= tol * tol * fmax(1.0, yyy)) {  // ||y+ - y|| <= tol max(1, ||y||)
       converged = true;
       break;
     }
   }
   cluster.sync();  // no CTA may exit while others can still write into its shared memory
+#ifdef IHS_PG_TIMING
+  if (rank == 0 && tid == 0)
+    for (int i = 0; i < 5; ++i) g_pg_timing[i] = pgt_acc[i];
+#endif
   if (rank == 0 && warp == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -620,7 +683,8 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
   int cs = pg_cluster_size(d);
   // default for 128 < d <= 256: 8 CTAs (C4, d = 256: 4 -> 8 CTAs measured PG 0.0475 -> 0.0413 ms per IHS
   // iteration, C4P 0.102 -> 0.087)
-  const int pref = cluster_pref > 0 ? cluster_pref : (d > 128 && d <= 256 ? 8 : 0);
+  // (and 4 CTAs for 64 < d <= 128: LASSO d = 128 measured 2.14 -> 1.49 us per inner step against one CTA)
+  const int pref = cluster_pref > 0 ? cluster_pref : (d > 128 && d <= 256 ? 8 : d > 64 && d <= 128 ? 4 : 0);
   if (cs > 0 && d <= 256 && pref > cs && (pref & (pref - 1)) == 0 && pref <= 16) cs = pref;
   if (cs > 0) {
     const int64_t R = (d + cs - 1) / cs;
@@ -634,7 +698,7 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(kCT);
+    cfg.blockDim = dim3(wv ? kWT : kCT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
