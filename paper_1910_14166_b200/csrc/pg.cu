@@ -393,13 +393,17 @@ __device__ __forceinline__ double wsum_k(const double (&v)[K]) {
   return warp_sum(t);
 }
 
-// 4 warps (one per SM sub-partition): every warp repeats the projection and
-// the norms on the whole iterate, so more warps only share issue slots (8 warps
-// measured 2665 cycles per LASSO step at d = 256 on 8 CTAs).
+// 4 warps (one per SM sub-partition: every warp repeats the projection and
+// the norms on the whole iterate, and 8 warps share the fp64 pipe for that:
+// measured +250 cycles per step); warp w of cluster rank c holds rows
+// c R + w U .. + U - 1 of H in registers (U x K doubles per lane, U K <= 32),
+// so the H v product of an inner step reads no shared memory (with H in
+// shared memory a step read R d doubles through the 128 B/clk pipe: ~512
+// cycles of the ~1290-cycle product at d = 256 on 8 CTAs).
 constexpr int kWT = 128;
 constexpr int kWW = kWT / 32;
 
-template <int K>
+template <int K, int U>
 __global__ void __launch_bounds__(kWT, 1) pg_warp_kernel(const double *__restrict__ H, const double *__restrict__ g,
                                                       int d, const double *__restrict__ x, double radius,
                                                       int max_inner, int power_iters, double tol, double safety,
@@ -413,9 +417,8 @@ __global__ void __launch_bounds__(kWT, 1) pg_warp_kernel(const double *__restric
   const int R = (d + cs - 1) / cs;
   const int r0 = rank * R, r1 = min(d, r0 + R);
   extern __shared__ double sm[];
-  double *Hs = sm;                   // R x d (my rows)
-  double *gs = Hs + (size_t)R * d;   // R (my rows of g)
-  double *zb = gs + R;               // 2 x d : z (or H v), double-buffered by step parity
+  double *gs = sm;      // R (my rows of g)
+  double *zb = gs + R;  // 2 x d : z (or H v), double-buffered by step parity
   uint64_t *zbar = reinterpret_cast<uint64_t *>(zb + 2 * d);  // 2 mbarriers: zb[0], zb[1] complete
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
@@ -423,7 +426,15 @@ __global__ void __launch_bounds__(kWT, 1) pg_warp_kernel(const double *__restric
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&zbar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  load_rows(Hs, H + (int64_t)r0 * d, (int64_t)(r1 - r0) * d, tid, kWT);
+  const int pw = r0 + U * warp;  // this warp's first row
+  double hreg[U][K];
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int q = lane + 32 * k;
+      hreg[u][k] = (pw + u < r1 && q < d) ? __ldg(H + (int64_t)(pw + u) * d + q) : 0.0;
+    }
   for (int i = tid; i < r1 - r0; i += kWT) gs[i] = g ? g[r0 + i] : 0.0;
   double xv[K], yv[K], vv[K], wv[K];
 #pragma unroll
@@ -440,56 +451,39 @@ __global__ void __launch_bounds__(kWT, 1) pg_warp_kernel(const double *__restric
   int par = 0;
   uint32_t zph = 0;  // bit b: the phase parity of zbar[b]
 #ifdef IHS_PG_TIMING
-  long long pgt_acc[5] = {0, 0, 0, 0, 0};
+  long long pgt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
   // rows p of this warp: out_p = pg ? y_p - ((H w)_p - g_p) / L : (H w)_p,
-  // sent into every CTA's zb[par]; then this CTA's wait for all d rows.  U
-  // rows per warp pass, U = R / (warps) when that is 2, 4 or 8, so that every
-  // warp of the CTA takes part (R = 32 at d = 256 on 8 CTAs: 8 rows a warp).
-  const int U_sel = R >= 8 * kWW ? 8 : R >= 4 * kWW ? 4 : R >= 2 * kWW ? 2 : 1;
-  auto gemv_rows = [&](auto uc, bool pg_step, double invL) {
-    constexpr int U = decltype(uc)::value;
-    for (int pb = r0 + U * warp; pb < r1; pb += U * kWW) {
-      double acc[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int p = pb + u;
-        const double *hr = Hs + (size_t)(min(p, r1 - 1) - r0) * d;
-        double a = 0.0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int q = lane + 32 * k;
-          if (q < d) a = fma(hr[q], wv[k], a);
-        }
-        acc[u] = a;
-      }
-      transpose_reduce<U>(acc, lane);
-      const int u = reduced_row_of_lane<U>(lane);
-      const int p = pb + u;
-      double val = acc[0];
-      if (pg_step) {  // warp-uniform; the shuffles run in every lane
-        // y_p is held by lane p % 32 as element p / 32 of every warp's copy
-        double yp = 0.0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const double t = __shfl_sync(0xffffffffu, vv[k], p & 31);
-          if ((p >> 5) == k) yp = t;
-        }
-        if (p < r1) val = fma(-(val - gs[p - r0]), invL, yp);
-      }
-      // the row's owner lane publishes it to every CTA of the cluster
-      if (owner_lane_of_row<U>(u) == lane && p < r1) {
-        const uint32_t za = smem_addr(zb + par * d + p), ba = smem_addr(&zbar[par]);
-        for (int r = 0; r < cs; ++r) st_async_f64(cluster_addr(za, r), val, cluster_addr(ba, r));
-      }
-    }
-  };
+  // sent into every CTA's zb[par]; then this CTA's wait for all d rows.
   auto gemv_bcast = [&](bool pg_step, double invL) {
     if (tid == 0) zbar_arm(&zbar[par], (uint32_t)d * 8u);
-    if (U_sel == 8) gemv_rows(std::integral_constant<int, 8>(), pg_step, invL);
-    else if (U_sel == 4) gemv_rows(std::integral_constant<int, 4>(), pg_step, invL);
-    else if (U_sel == 2) gemv_rows(std::integral_constant<int, 2>(), pg_step, invL);
-    else gemv_rows(std::integral_constant<int, 1>(), pg_step, invL);
+    double acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      double a = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) a = fma(hreg[u][k], wv[k], a);
+      acc[u] = a;
+    }
+    transpose_reduce<U>(acc, lane);
+    const int u = reduced_row_of_lane<U>(lane);
+    const int p = pw + u;
+    double val = acc[0];
+    if (pg_step) {  // warp-uniform; the shuffles run in every lane
+      // y_p is held by lane p % 32 as element p / 32 of every warp's copy
+      double yp = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const double t = __shfl_sync(0xffffffffu, vv[k], p & 31);
+        if ((p >> 5) == k) yp = t;
+      }
+      if (p < r1) val = fma(-(val - gs[p - r0]), invL, yp);
+    }
+    // the row's owner lane publishes it to every CTA of the cluster
+    if (owner_lane_of_row<U>(u) == lane && p < r1) {
+      const uint32_t za = smem_addr(zb + par * d + p), ba = smem_addr(&zbar[par]);
+      for (int r = 0; r < cs; ++r) st_async_f64(cluster_addr(za, r), val, cluster_addr(ba, r));
+    }
     PGT_MARK(tw0);
     zbar_wait(&zbar[par], (zph >> par) & 1u);
     PGT_MARK(tw1);
@@ -564,15 +558,15 @@ __global__ void __launch_bounds__(kWT, 1) pg_warp_kernel(const double *__restric
       theta = warm_th ? theta_prev : (n1 - radius) / (double)d;
       double cprev = warm_th ? -1.0 : (double)d;
       for (int guard = 0; guard <= d + 1; ++guard) {
-        double Sv = 0.0;
+        double Sh[2] = {0.0, 0.0};
         int ci = 0;  // the active count from ballots (exact; no shuffle chain)
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           const bool act = av[k] > theta;
-          if (act) Sv += av[k];
+          Sh[k & 1] += act ? av[k] : 0.0;
           ci += __popc(__ballot_sync(0xffffffffu, act));
         }
-        Sv = warp_sum(Sv);
+        const double Sv = warp_sum(Sh[0] + Sh[1]);
         const double cv = (double)ci;
         if (cv == 0.0 && warm_th) {  // started above every |z|: cold start instead
           warm_th = false;
@@ -590,28 +584,33 @@ __global__ void __launch_bounds__(kWT, 1) pg_warp_kernel(const double *__restric
     // ||y+ - y||^2, ||y||^2 and the restart test in ONE interleaved warp
     // reduction; FISTA's momentum from a table (no sqrt / divide on the step's
     // critical path); convergence compared in squares.
-    double ynv[K], s3[3] = {0.0, 0.0, 0.0};
+    // y+ = sign(z) max(|z| - theta, 0) (theta = 0: y+ = z), branch-free so the
+    // K elements' dependent chains interleave; each sum as two half chains.
+    double ynv[K], s3[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};
+    const double th = proj ? theta : 0.0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      double yn = zv[k];
-      if (proj) {
-        const double a = av[k] - theta;
-        yn = a > 0.0 ? (zv[k] < 0.0 ? -a : a) : 0.0;
-      }
+      const double yn = copysign(fmax(av[k] - th, 0.0), zv[k]);
       const double e = yn - yv[k];
-      s3[0] = fma(e, e, s3[0]);
-      s3[1] = fma(yv[k], yv[k], s3[1]);
-      s3[2] = fma(vv[k] - yn, e, s3[2]);  // gradient-based restart test (O'Donoghue & Candes)
+      double *t3 = s3[k & 1];
+      t3[0] = fma(e, e, t3[0]);
+      t3[1] = fma(yv[k], yv[k], t3[1]);
+      t3[2] = fma(vv[k] - yn, e, t3[2]);  // gradient-based restart test (O'Donoghue & Candes)
       ynv[k] = yn;
     }
+    double s3s[3] = {s3[0][0] + s3[1][0], s3[0][1] + s3[1][1], s3[0][2] + s3[1][2]};
+    PGT_MARK(tn0);
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1)
 #pragma unroll
-      for (int i = 0; i < 3; ++i) s3[i] += __shfl_xor_sync(0xffffffffu, s3[i], o);
-    const double dnn = s3[0], yyy = s3[1];
+      for (int i = 0; i < 3; ++i) s3s[i] += __shfl_xor_sync(0xffffffffu, s3s[i], o);
+    const double dnn = s3s[0], yyy = s3s[1];
+    PGT_MARK(tn1);
+    PGT_ADD(5, ts2, tn0);
+    PGT_ADD(6, tn0, tn1);
     if (accel & 1) {
       double coef = 0.0;
-      if (s3[2] > 0.0) {
+      if (s3s[2] > 0.0) {
         tj = 0;  // restart: the next step is a plain projected-gradient step
       } else {
         coef = fista_coef(tj);
@@ -640,7 +639,7 @@ __global__ void __launch_bounds__(kWT, 1) pg_warp_kernel(const double *__restric
   cluster.sync();  // no CTA may exit while others can still write into its shared memory
 #ifdef IHS_PG_TIMING
   if (rank == 0 && tid == 0)
-    for (int i = 0; i < 5; ++i) g_pg_timing[i] = pgt_acc[i];
+    for (int i = 0; i < 8; ++i) g_pg_timing[i] = pgt_acc[i];
 #endif
   if (rank == 0 && warp == 0) {
 #pragma unroll
@@ -665,9 +664,9 @@ int pg_cluster_size(int64_t d) {
   return 0;
 }
 
-bool lasso_supported(int64_t d) { return d <= 256 && pg_cluster_size(d) > 0; }
+bool lasso_supported(int64_t d) { return d >= 1 && d <= 256; }
 
-bool pg_supported(int64_t d) { return pg_cluster_size(d) > 0 || (size_t)5 * d * 8 <= 200 * 1024; }
+bool pg_supported(int64_t d) { return d <= 256 || pg_cluster_size(d) > 0 || (size_t)5 * d * 8 <= 200 * 1024; }
 
 size_t pg_scratch_bytes(int64_t d) { return (size_t)d * 8; }
 
@@ -676,29 +675,39 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
                                  double *x_next, int32_t *inner_iters, double *scratch, int *status, cudaStream_t st,
                                  LaunchCounter lc, bool warm_start, int prox, const double *L_in, double *L_out,
                                  int cluster_pref) {
-  // d <= 256: the warp-per-iterate cluster kernel; larger d: the CTA-level
-  // cluster kernel while H fits the cluster's shared memory, else one CTA.
-  // cluster_pref (2..16, a power of two): a wider cluster for the warp kernel
-  // -- fewer rows of the H v product per warp, one more barrier participant
-  int cs = pg_cluster_size(d);
-  // default for 128 < d <= 256: 8 CTAs (C4, d = 256: 4 -> 8 CTAs measured PG 0.0475 -> 0.0413 ms per IHS
-  // iteration, C4P 0.102 -> 0.087)
-  // (and 4 CTAs for 64 < d <= 128: LASSO d = 128 measured 2.14 -> 1.49 us per inner step against one CTA)
-  const int pref = cluster_pref > 0 ? cluster_pref : (d > 128 && d <= 256 ? 8 : d > 64 && d <= 128 ? 4 : 0);
-  if (cs > 0 && d <= 256 && pref > cs && (pref & (pref - 1)) == 0 && pref <= 16) cs = pref;
-  if (cs > 0) {
+  // d <= 256: the warp-per-iterate cluster kernel with H in registers; larger
+  // d: the CTA-level cluster kernel while H fits the cluster's shared memory,
+  // else one CTA.
+  if (d <= 256) {
+    // K doubles of the iterate per lane; U rows of H per warp (4 warps a CTA):
+    // the smallest cluster with U <= 8 and U K <= 32 -- d = 256: 16 CTAs (U = 4),
+    // d = 128: 4 (U = 8), d = 64: 2 (U = 8), d <= 32: 1.  cluster_pref (a power
+    // of two <= 16) overrides when its U satisfies the same bounds.
+    const int K = d <= 32 ? 1 : d <= 64 ? 2 : d <= 128 ? 4 : 8;
+    auto u_of = [&](int c) {
+      const int64_t rows = (d + c - 1) / c, per = (rows + kWW - 1) / kWW;
+      return per <= 1 ? 1 : per <= 2 ? 2 : per <= 4 ? 4 : per <= 8 ? 8 : 16;
+    };
+    int cs = 1;
+    while (cs < 16 && (u_of(cs) > 8 || u_of(cs) * K > 32)) cs *= 2;
+    if (cluster_pref > 0 && cluster_pref <= 16 && (cluster_pref & (cluster_pref - 1)) == 0 &&
+        u_of(cluster_pref) <= 8 && u_of(cluster_pref) * K <= 32)
+      cs = cluster_pref;
+    const int U = u_of(cs);
     const int64_t R = (d + cs - 1) / cs;
-    const bool wv = d <= 256;
-    const size_t smem =
-        std::max(wv ? (size_t)(R * d + R + 2 * d) * 8 + 16 : (size_t)(R * d + 6 * d) * 8, kExclusiveSmem);
-    auto wkern = d <= 32 ? pg_warp_kernel<1> : d <= 64 ? pg_warp_kernel<2> : d <= 128 ? pg_warp_kernel<4>
-                                                                             : pg_warp_kernel<8>;
-    const void *kern = wv ? (const void *)wkern : (const void *)pg_cluster_kernel;
+    const size_t smem = std::max((size_t)(R + 2 * d) * 8 + 16, kExclusiveSmem);
+    const void *kern = nullptr;
+#define IHS_PGK(KV, UV) \
+  if (K == KV && U == UV) kern = (const void *)pg_warp_kernel<KV, UV>;
+    IHS_PGK(8, 1) IHS_PGK(8, 2) IHS_PGK(8, 4) IHS_PGK(4, 1) IHS_PGK(4, 2) IHS_PGK(4, 4) IHS_PGK(4, 8)
+    IHS_PGK(2, 1) IHS_PGK(2, 2) IHS_PGK(2, 4) IHS_PGK(2, 8) IHS_PGK(1, 1) IHS_PGK(1, 2) IHS_PGK(1, 4) IHS_PGK(1, 8)
+#undef IHS_PGK
+    if (!kern) return cudaErrorInvalidValue;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (cs > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(cs);
-    cfg.blockDim = dim3(wv ? kWT : kCT);
+    cfg.blockDim = dim3(kWT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -709,19 +718,44 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     lc.add();
-    if (!wv) {
-      if (prox || L_out) return cudaErrorNotSupported;
-      return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
-                                x_next, inner_iters, status);
-    }
     // accel bit 0: FISTA with restart; bit 1: warm-started projection threshold
-    constexpr int accel = 3;
+    int accel = 3;
     // warm start (scratch = d doubles holding the last eigenvector estimate):
     // warm_power_iters steps from it instead of power_iters from 1/sqrt(d)
     const bool warm_ok = warm_start && scratch;
-    const int piters = warm_ok ? warm_power_iters : power_iters;
-    return cudaLaunchKernelEx(&cfg, wkern, H, g, (int)d, x, radius, max_inner, piters, tol, safety, x_next,
-                              inner_iters, status, accel, scratch, warm_ok ? 1 : 0, prox, L_in, L_out);
+    int piters = warm_ok ? warm_power_iters : power_iters;
+    int warm = warm_ok ? 1 : 0;
+    void *args[] = {(void *)&H,     (void *)&g,         (void *)&d,        (void *)&x,      (void *)&radius,
+                    (void *)&max_inner, (void *)&piters, (void *)&tol,     (void *)&safety, (void *)&x_next,
+                    (void *)&inner_iters, (void *)&status, (void *)&accel, (void *)&scratch, (void *)&warm,
+                    (void *)&prox,  (void *)&L_in,      (void *)&L_out};
+    int di = (int)d;
+    args[2] = (void *)&di;
+    return cudaLaunchKernelExC(&cfg, kern, args);
+  }
+  int cs = pg_cluster_size(d);
+  if (cs > 0) {
+    if (prox || L_out) return cudaErrorNotSupported;
+    const int64_t R = (d + cs - 1) / cs;
+    const size_t smem = std::max((size_t)(R * d + 6 * d) * 8, kExclusiveSmem);
+    cudaFuncSetAttribute((const void *)pg_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (cs > 8)
+      cudaFuncSetAttribute((const void *)pg_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(kCT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cs;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    lc.add();
+    return cudaLaunchKernelEx(&cfg, pg_cluster_kernel, H, g, (int)d, x, radius, max_inner, power_iters, tol, safety,
+                              x_next, inner_iters, status);
   }
   if (L_out) return cudaErrorNotSupported;  // power-only launches: the warp kernel only
   if (prox) return cudaErrorNotSupported;

@@ -69,9 +69,9 @@ int main(int argc, char **argv) {
 #endif
       const double k = it > 0 ? it : 1;
       printf("%s d=%d cluster=%d: %d inner steps, %.4f ms launch (%.3f us/step incl. launch); cycles/step: "
-             "gemv+send %.0f  wait %.0f  projection %.0f  norms+update %.0f  total %.0f  (%s)\n",
+             "gemv+send %.0f  wait %.0f  projection %.0f  norms+update %.0f [elementwise %.0f, shuffles %.0f]  total %.0f  (%s)\n",
              prox ? "lasso " : "l1ball", d, cl, it, ms, 1e3 * ms / k, z[0] / k - z[1] / k, z[1] / k, z[2] / k,
-             z[3] / k, z[4] / k, cudaGetErrorString(cudaGetLastError()));
+             z[3] / k, z[5] / k, z[6] / k, z[4] / k, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
