@@ -638,7 +638,9 @@ def main():
                           "K consecutive steps between two device events"),
                "config": config_obj(cfg, world, {"per_gpu_rows": n_loc, "schedule": (
                    "one-launch small step per iteration (small_step.cu)" if solve_mode else
-                   "look-ahead Gram (H_{t+1} beside the update of t and the next pass; DESIGN.md section 9)"
+                   ("look-ahead Gram (H_{t+1} after the CG update of t, beside the next pass; DESIGN.md section 9)"
+                    if cfg.constraint == "ols" else
+                    "look-ahead Gram (H_{t+1} beside the update of t; DESIGN.md section 9)")
                    if S.lookahead and S.la_gram_only else
                    "look-ahead (H^-1 of the next sketch beside the pass; DESIGN.md section 9)" if S.lookahead
                    else "plain")}),

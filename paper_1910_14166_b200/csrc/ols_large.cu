@@ -44,23 +44,32 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
                : "d"(a), "d"(b));
 }
 
-// Sense-free generation barrier over all CTAs of a cooperative launch.
+// Grid barrier over all CTAs of a cooperative launch: one ticket counter that
+// only grows (zeroed by the launch's memset); a CTA's ticket t releases when
+// the counter reaches the next multiple of the grid size.  One atomic round
+// trip and a relaxed poll of the same word -- the generation-word version
+// (read the generation, fence, atomic, last arriver resets the count and
+// bumps the generation, the others sleep-poll it) measured ~4650 cycles per
+// CG step (tools/probe/cg_timing.cu).  (`gen` is unused; kept for the
+// scratch layout.)
 __device__ __forceinline__ void grid_barrier(unsigned *count, volatile unsigned *gen, unsigned nblocks) {
+  (void)gen;
   __syncthreads();
   if (threadIdx.x == 0) {
-    const unsigned g0 = *gen;
-    __threadfence();
-    if (atomicAdd(count, 1u) == nblocks - 1) {
-      atomicExch(count, 0u);
-      __threadfence();
-      atomicExch((unsigned *)gen, g0 + 1);
-    } else {
-      while (*gen == g0) __nanosleep(20);
+    unsigned t;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(count) : "memory");
+    const unsigned target = (t / nblocks + 1u) * nblocks;
+    for (;;) {
+      unsigned v;
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+      if (v >= target) break;
     }
-    __threadfence();
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
   __syncthreads();
 }
+// (Tickets spread over 8 counters 128 B apart, polled by 8 lanes, measured
+// slower: 3600 vs 3150 cycles per CG step -- the arrivals were not the cost.)
 
 // CTA-wide sums of two values in a fixed order (every thread gets both).
 __device__ __forceinline__ void cta_sum2(double &a, double &b, double *red) {
@@ -333,6 +342,23 @@ __device__ void chol_grid(const double *H, const double *g, const double *x, dou
   if (blockIdx.x == 0) backsolve(c, x, x_next, sm);
 }
 
+#ifdef IHS_CG_TIMING
+// tools/probe/cg_timing.cu only (never in the library build): per-phase clock
+// sums of the CG loop, measured by thread 0 of CTA 0.
+__device__ long long g_cg_timing[8];
+#define CGT_MARK(v) long long v = clock64()
+#define CGT_ADD(i, a, b) cgt_acc[i] += (b) - (a)
+#else
+#define CGT_MARK(v)
+#define CGT_ADD(i, a, b)
+#endif
+
+// RP > 0 (d <= 1024, at most RP rows a CTA): the CTA's rows of H in
+// registers, thread t holding columns t + 256 k (k < 4) of each -- the product
+// H p is then RP register dot products and one CTA reduction, with no shared-
+// memory pass over H or p (1670 cycles per step with the rows in shared memory).
+// RP = 0: rows in shared memory (or global), one warp per row.
+template <int RP>
 __global__ void __launch_bounds__(kThreads) ols_large_kernel(const double *__restrict__ H,
                                                              const double *__restrict__ g, int d,
                                                              const double *__restrict__ x, double *x_next,
@@ -341,6 +367,7 @@ __global__ void __launch_bounds__(kThreads) ols_large_kernel(const double *__res
                                                              Chol chol, int *status) {
   extern __shared__ double sm[];
   __shared__ double red[2 * kWarps];
+  __shared__ double redq[kWarps * (RP > 0 ? RP : 1)];
   if (mode == 2) {  // Cholesky only
     chol_grid(H, g, x, x_next, chol, status, bar, sm);
     return;
@@ -349,7 +376,19 @@ __global__ void __launch_bounds__(kThreads) ols_large_kernel(const double *__res
   double *Hs = sm + d;   // rows_per x d when smem_rows
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int i0 = blockIdx.x * rows_per, i1 = min(d, i0 + rows_per);
-  if (smem_rows) load_rows(Hs, H + (int64_t)i0 * d, (int64_t)(i1 - i0) * d, tid, kThreads);
+  constexpr int KR = 4;  // (RP > 0: d <= 4 * kThreads)
+  double hreg[RP > 0 ? RP : 1][KR];
+  if (RP > 0) {
+#pragma unroll
+    for (int i = 0; i < (RP > 0 ? RP : 1); ++i)
+#pragma unroll
+      for (int k = 0; k < KR; ++k) {
+        const int c = tid + kThreads * k;
+        hreg[i][k] = (i0 + i < i1 && c < d) ? __ldg(H + (int64_t)(i0 + i) * d + c) : 0.0;
+      }
+  } else if (smem_rows) {
+    load_rows(Hs, H + (int64_t)i0 * d, (int64_t)(i1 - i0) * d, tid, kThreads);
+  }
   // full-length vectors, element c = tid + kThreads * k, in registers
   double u[kMaxPer], r[kMaxPer], z[kMaxPer], p[kMaxPer], dinv[kMaxPer];
   double rz = 0.0, gg = 0.0;
@@ -373,28 +412,59 @@ __global__ void __launch_bounds__(kThreads) ols_large_kernel(const double *__res
   cta_sum2(nonpos, unused, red);
   int it = 0;
   bool not_spd = nonpos > 0.0;
+#ifdef IHS_CG_TIMING
+  long long cgt_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   for (;;) {
     if (not_spd || !(gg > 0.0) || it >= max_iter) break;
-#pragma unroll
-    for (int k = 0; k < kMaxPer; ++k) {
-      const int c = tid + kThreads * k;
-      if (c < d) ps[c] = p[k];
-    }
-    __syncthreads();
+    CGT_MARK(c0);
     double *q = qbuf + (size_t)(it & 1) * d;
-    for (int i = i0 + warp; i < i1; i += kWarps) {
-      const double *row = smem_rows ? Hs + (size_t)(i - i0) * d : H + (int64_t)i * d;
-      double t0 = 0.0, t1 = 0.0;
-      int c = lane;
-      for (; c + 32 < d; c += 64) {
-        t0 = fma(row[c], ps[c], t0);
-        t1 = fma(row[c + 32], ps[c + 32], t1);
+    if (RP > 0) {
+      double part[RP > 0 ? RP : 1];
+#pragma unroll
+      for (int i = 0; i < (RP > 0 ? RP : 1); ++i) {
+        double a = 0.0;
+#pragma unroll
+        for (int k = 0; k < KR; ++k) a = fma(hreg[i][k], p[k], a);
+        part[i] = a;
       }
-      if (c < d) t0 = fma(row[c], ps[c], t0);
-      const double s = warp_sum(t0 + t1);
-      if (lane == 0) q[i] = s;
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < (RP > 0 ? RP : 1); ++i) part[i] += __shfl_xor_sync(0xffffffffu, part[i], o);
+      if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < (RP > 0 ? RP : 1); ++i) redq[warp * (RP > 0 ? RP : 1) + i] = part[i];
+      __syncthreads();
+      if (tid < (RP > 0 ? RP : 1) && i0 + tid < i1) {
+        double sq = 0.0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) sq += redq[w * (RP > 0 ? RP : 1) + tid];
+        q[i0 + tid] = sq;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kMaxPer; ++k) {
+        const int c = tid + kThreads * k;
+        if (c < d) ps[c] = p[k];
+      }
+      __syncthreads();
+      for (int i = i0 + warp; i < i1; i += kWarps) {
+        const double *row = smem_rows ? Hs + (size_t)(i - i0) * d : H + (int64_t)i * d;
+        double t0 = 0.0, t1 = 0.0;
+        int c = lane;
+        for (; c + 32 < d; c += 64) {
+          t0 = fma(row[c], ps[c], t0);
+          t1 = fma(row[c + 32], ps[c + 32], t1);
+        }
+        if (c < d) t0 = fma(row[c], ps[c], t0);
+        const double s = warp_sum(t0 + t1);
+        if (lane == 0) q[i] = s;
+      }
     }
+    CGT_MARK(c1);
     grid_barrier(bar, bar + 1, gridDim.x);
+    CGT_MARK(c2);
     double qv[kMaxPer];
     double pq = 0.0, dummy = 0.0;
 #pragma unroll
@@ -404,6 +474,7 @@ __global__ void __launch_bounds__(kThreads) ols_large_kernel(const double *__res
       pq += p[k] * qv[k];
     }
     cta_sum2(pq, dummy, red);
+    CGT_MARK(c3);
     if (!(pq > 0.0)) {
       not_spd = true;
       break;
@@ -426,7 +497,19 @@ __global__ void __launch_bounds__(kThreads) ols_large_kernel(const double *__res
 #pragma unroll
     for (int k = 0; k < kMaxPer; ++k) p[k] = fma(beta, p[k], z[k]);
     __syncthreads();  // ps is rewritten at the top of the next step
+    CGT_MARK(c4);
+    CGT_ADD(0, c0, c1);
+    CGT_ADD(1, c1, c2);
+    CGT_ADD(2, c2, c3);
+    CGT_ADD(3, c3, c4);
+    CGT_ADD(4, c0, c4);
   }
+#ifdef IHS_CG_TIMING
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int i = 0; i < 5; ++i) g_cg_timing[i] = cgt_acc[i];
+    g_cg_timing[5] = it;
+  }
+#endif
   const bool capped = gg > 0.0 && it >= max_iter && !not_spd;
   if (mode == 1 && (not_spd || capped)) {  // CG did not finish: the Cholesky decides (same launch)
     grid_barrier(bar, bar + 1, gridDim.x);  // every CTA is done with H's rows in shared memory
@@ -456,9 +539,10 @@ size_t chol_smem() {
 
 bool ols_large_supported(int64_t d) { return d >= 1 && d <= (int64_t)kThreads * kMaxPer; }
 
+constexpr int kFlagDoubles = 8;  // the grid-barrier words
 size_t ols_large_scratch_bytes(int64_t d) {
   const int64_t Dp = (d + 1 + PB - 1) / PB * PB;
-  return (size_t)2 * d * 8 + 64 + (size_t)(Dp * Dp + Dp) * 8 + 64;
+  return (size_t)2 * d * 8 + kFlagDoubles * 8 + (size_t)(Dp * Dp + Dp) * 8 + 64;
 }
 
 cudaError_t launch_ols_large(const double *H, const double *g, int64_t d, const double *x, double *x_next,
@@ -476,20 +560,37 @@ cudaError_t launch_ols_large(const double *H, const double *g, int64_t d, const 
   }
   smem = std::max(smem, chol_smem());
   smem = std::max(smem, ((size_t)d + PB * (PB + 1)) * 8);  // back substitution
-  IHS_SMEM_ATTR(ols_large_kernel, smem);
-  if (occ_smem != smem) {
+  // the register-row kernel when d <= 1024 and at most 8 rows a CTA
+  const int rp = (mode != 2 && d <= 4 * kThreads && rows_per <= 8) ? rows_per : 0;
+  const void *kern = nullptr;
+  switch (rp) {
+    case 1: kern = (const void *)ols_large_kernel<1>; break;
+    case 2: kern = (const void *)ols_large_kernel<2>; break;
+    case 3: kern = (const void *)ols_large_kernel<3>; break;
+    case 4: kern = (const void *)ols_large_kernel<4>; break;
+    case 5: kern = (const void *)ols_large_kernel<5>; break;
+    case 6: kern = (const void *)ols_large_kernel<6>; break;
+    case 7: kern = (const void *)ols_large_kernel<7>; break;
+    case 8: kern = (const void *)ols_large_kernel<8>; break;
+    default: kern = (const void *)ols_large_kernel<0>;
+  }
+  if (rp > 0) smem_rows = 0;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static const void *occ_kern = nullptr;
+  if (occ_smem != smem || occ_kern != kern) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ols_large_kernel, kThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, smem);
     max_per_sm = nb;
     occ_smem = smem;
+    occ_kern = kern;
   }
   if (max_per_sm * num_sms < nblk) return cudaErrorCooperativeLaunchTooLarge;
   double *qbuf = scratch;
-  unsigned *bar = reinterpret_cast<unsigned *>(scratch + 2 * d);
+  unsigned *bar = reinterpret_cast<unsigned *>(scratch + 2 * d);  // [2] grid-barrier words
   Chol chol;
   chol.Dp = (int)((d + 1 + PB - 1) / PB * PB);
   chol.d = (int)d;
-  chol.M = scratch + 2 * d + 8;
+  chol.M = scratch + 2 * d + kFlagDoubles;
   chol.rdiag = chol.M + (size_t)chol.Dp * chol.Dp;
   chol.flag = reinterpret_cast<int *>(chol.rdiag + chol.Dp);
   cudaError_t e = cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st);
@@ -499,7 +600,7 @@ cudaError_t launch_ols_large(const double *H, const double *g, int64_t d, const 
   void *args[] = {(void *)&H,    (void *)&g,    (void *)&di,  (void *)&x,    (void *)&x_next,
                   (void *)&qbuf, (void *)&bar,  (void *)&rows_per, (void *)&mi, (void *)&tol2,
                   (void *)&sr,   (void *)&md,   (void *)&chol, (void *)&status};
-  e = cudaLaunchCooperativeKernel((const void *)ols_large_kernel, dim3(nblk), dim3(kThreads), args, smem, st);
+  e = cudaLaunchCooperativeKernel(kern, dim3(nblk), dim3(kThreads), args, smem, st);
   lc.add();
   return e;
 }

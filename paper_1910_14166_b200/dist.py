@@ -182,11 +182,15 @@ class ShardedIHS:
             if self.la_gram_only:  # only the Gram looks ahead
                 self.ops.sketch_grad(self.A, self.spec, t + 1, self.b, x, SAn, gn)
                 self.allreduce(pk)
-                self.ops.gram_lookahead(SAn, self.Hinv[nxt])  # beside this update
                 H = self.Hinv[cur]
                 if self.constraint == "ols":
+                    # the CG update first; the next Gram then runs beside the next pass
                     self.ops.ols(H, gn, x, xn)
-                elif self.constraint == "lasso":
+                    self.ops.gram_lookahead(SAn, self.Hinv[nxt])
+                    self._la_t, self._la_cur = t + 1, nxt
+                    return xn
+                self.ops.gram_lookahead(SAn, self.Hinv[nxt])  # beside this update
+                if self.constraint == "lasso":
                     self.ops.lasso(H, gn, x, self.radius, self.cfg, xn, self.inner)
                 else:
                     self.ops.l1(H, gn, x, self.radius, self.cfg, xn, self.inner)
