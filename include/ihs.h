@@ -123,8 +123,10 @@ int64_t ihs_ctx_kernel_launches(ihs_ctx ctx);
  * value: IHS_ERR_INVALID_ARGUMENT.
  *   "lookahead"    -1 (default) look-ahead schedules of the solve calls by size,
  *                  0 off, 1 whenever supported                    [IHS_LOOKAHEAD]
- *   "sjlt_onepass" 1 (default) dense SJLT in one read of A, 0 as s sorted
- *                  CountSketch passes (bit-identical to the oracle) [IHS_SJLT=passes]
+ *   "sjlt_onepass" 1 (default) dense SJLT in one read of A, the gradient of
+ *                  ihs_sketch_grad riding on the same pass (d <= 128); 2 the same
+ *                  with the gradient in its own pass; 0 as s sorted CountSketch
+ *                  passes (bit-identical to the oracle) [IHS_SJLT=passes|gradpass]
  *   "ols_large"    d > 160 OLS step: 1 (default) conjugate gradients, then the
  *                  blocked Cholesky in the same launch when CG does not finish;
  *                  0 CG only (IHS_ERR_NOT_CONVERGED at its cap); 2 the Cholesky

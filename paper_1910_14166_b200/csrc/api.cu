@@ -74,7 +74,8 @@ struct ihs_ctx_s {
   bool profiling = false;
   // Options (ihs_ctx_set_option; initial values from the IHS_* environment at
   // ihs_ctx_create).  Per context, so alternatives can be compared in one process.
-  int sjlt_onepass = 1;  // dense SJLT: 1 = one read of A (sjlt_onepass.cu), 0 = s sorted CountSketch passes
+  int sjlt_onepass = 1;  // dense SJLT: 1 = one read of A (sjlt_onepass.cu) with the gradient riding on it,
+                         // 2 = the same with the gradient in its own pass, 0 = s sorted CountSketch passes
   int lookahead = -1;    // look-ahead schedules: -1 = by size (use_lookahead), 0 = off, 1 = whenever supported
   int ols_large = 1;     // d > 160 OLS: 0 = CG only, 1 = CG + Cholesky fallback, 2 = Cholesky only
   int fuse_max_d = 64;   // a4 + a6 in one cluster launch up to this d (<= 128)
@@ -314,11 +315,11 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
   SjltOnepassPlan op;
   if (SA && s > 1 && c->sjlt_onepass && n > 0 && sjlt_onepass_plan(n, d, m, s, c->num_sms, A->values, op)) {
     // One read of A for S A (sjlt_onepass.cu): the per-chunk bucket lists
-    // (a1) on the side stream, beside the gradient pass (a5, HBM-bound) on the
-    // ctx stream when asked for; then the column-slice sketch pass.  (The
-    // gradient beside the sketch pass instead, in 4-warp CTAs that fit next to
-    // it, measured slower: both stream through the L1/shared data pipe the
-    // sketch is bound by -- C5 28.2 + 0 vs 21.6 + 4.3 ms.)
+    // (a1), then the column-slice sketch pass with the gradient (a5) riding on
+    // it in extra warps (C5: 21.1 + 4.3 ms in two passes -> 22.9 ms).  (A
+    // separate co-resident gradient kernel could not share the SMs: the
+    // sketch's 17 warps leave an SM sub-partition 1 K registers, and an SM
+    // that started the small kernel first is carved out for L1.)
     join_side(c);
     join_factor(c);
     uint16_t *lists;
@@ -335,18 +336,26 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
     }
     IHS_CUDA(cudaEventRecord(c->ev_side, c->side));
     c->side_pending = true;
-    const int64_t nbg = grad_dense_blocks(n, d, c->num_sms);
+    // The gradient (a5) rides on the sketch pass by default: extra warps of
+    // its CTAs stream A for g (sjlt_onepass.cu), hidden under the sketch's
+    // shared-memory-bound work.  Option sjlt_onepass = 2, or d > 128: the
+    // gradient in its own pass beside the lists instead.
+    const int nfused = (g && c->sjlt_onepass == 1) ? sjlt_onepass_grad_blocks(op) : 0;
+    const int64_t nbg = nfused ? nfused : grad_dense_blocks(n, d, c->num_sms);
     double *gpart = nullptr;
     if (g) {
       if (d > 1024) return IHS_ERR_UNSUPPORTED;
       IHS_TRY(scratch(c, S_GPART, ((size_t)nbg * d + reduce_rows_tmp(nbg, d)) * 8, &gpart));
+    }
+    if (g && !nfused) {
       Prof pr(c, IHS_K_GRAD);
       IHS_CUDA(launch_grad_dense(A->values, n, d, b, x, gpart, nbg, st, lc_of(c)));
     }
     join_side(c);
     {
       Prof pr(c, IHS_K_SJLT);
-      IHS_CUDA(launch_sjlt_onepass(op, A->values, lists, part, SA, spec_scale(spec), st, lc_of(c)));
+      IHS_CUDA(launch_sjlt_onepass(op, A->values, lists, part, SA, spec_scale(spec), st, lc_of(c), nfused ? b : nullptr,
+                                   nfused ? x : nullptr, nfused ? gpart : nullptr));
     }
     if (g) {
       if (ls && ls->Hinv_next) IHS_TRY(ols_factor_impl(c, SA, m, d, 1.0, ls->Hinv_next));
@@ -1104,7 +1113,7 @@ ihs_status ihs_ctx_create(ihs_ctx *out, int device, void *stream) {
   cudaMemset(c->d_status, 0, 4 * sizeof(int));
   // initial option values from the environment (ihs_ctx_set_option changes them per ctx)
   if (const char *e = getenv("IHS_PREFETCH")) c->prefetch = std::strcmp(e, "0") != 0;
-  if (const char *e = getenv("IHS_SJLT")) c->sjlt_onepass = !std::strcmp(e, "passes") ? 0 : 1;
+  if (const char *e = getenv("IHS_SJLT")) c->sjlt_onepass = !std::strcmp(e, "passes") ? 0 : !std::strcmp(e, "gradpass") ? 2 : 1;
   if (const char *e = getenv("IHS_LOOKAHEAD")) c->lookahead = std::strcmp(e, "0") != 0 ? 1 : 0;
   if (const char *e = getenv("IHS_OLS")) c->ols_large = !std::strcmp(e, "chol") ? 2 : !std::strcmp(e, "cg") ? 0 : 1;
   if (const char *e = getenv("IHS_FUSE")) c->fuse_max_d = !std::strcmp(e, "0") ? 0 : 128;
@@ -1176,7 +1185,7 @@ struct OptionDef {
   int lo, hi;
 };
 const OptionDef kOptions[] = {
-    {"lookahead", &ihs_ctx_s::lookahead, -1, 1},   {"sjlt_onepass", &ihs_ctx_s::sjlt_onepass, 0, 1},
+    {"lookahead", &ihs_ctx_s::lookahead, -1, 1},   {"sjlt_onepass", &ihs_ctx_s::sjlt_onepass, 0, 2},
     {"ols_large", &ihs_ctx_s::ols_large, 0, 2},    {"fuse_max_d", &ihs_ctx_s::fuse_max_d, 0, 128},
     {"pg_warm", &ihs_ctx_s::pg_warm, 0, 1},       {"small_step", &ihs_ctx_s::small_step, 0, 1},
     {"pg_cluster", &ihs_ctx_s::pg_cluster, 0, 16},

@@ -236,21 +236,6 @@ cudaError_t launch_grad_dense(const double *A, int64_t n, int64_t d, const doubl
   return cudaGetLastError();
 }
 
-// The same pass as a 4-warp CTA per SM (nblocks = the SM count): small enough
-// (<= ~13 K registers, 3 KiB of shared memory for d = 96) to sit beside a
-// one-CTA-per-SM kernel -- the one-read SJLT sketch -- and stream A from HBM
-// while that kernel is bound by shared memory (api.cu).
-cudaError_t launch_grad_dense_corun(const double *A, int64_t n, int64_t d, const double *bvec, const double *x,
-                                    double *gpart, int64_t nblocks, cudaStream_t st, LaunchCounter lc) {
-  if (d > 1024) return cudaErrorInvalidValue;
-  const int nv = (int)((d + 31) / 32);
-#define CALL(NV, U) launch_grad_t<NV, U, 4>(A, n, (int)d, bvec, x, gpart, nblocks, st)
-  IHS_NV_DISPATCH(nv, CALL)
-#undef CALL
-  lc.add();
-  return cudaGetLastError();
-}
-
 int64_t reduce_rows_tmp(int64_t rows, int64_t d) {
   return ((rows + kReduceRowsPerCta - 1) / kReduceRowsPerCta) * d;
 }

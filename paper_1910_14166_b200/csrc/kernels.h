@@ -87,9 +87,14 @@ struct SjltOnepassPlan {
 bool sjlt_onepass_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, const void *A, SjltOnepassPlan &p);
 cudaError_t launch_sjlt_lists(const SjltOnepassPlan &p, uint64_t key, int64_t row_offset, uint16_t *lists,
                               cudaStream_t st, LaunchCounter lc);
-// SA = scale * S A from the lists (partials: p.partial_bytes of scratch)
+// SA = scale * S A from the lists (partials: p.partial_bytes of scratch).
+// gpart != nullptr: the gradient's partial rows g_k = sum r_i a_i ride on the
+// same launch (extra warps streaming A), sjlt_onepass_grad_blocks(p) rows of d
+// doubles in gpart (0: d too wide, use the separate gradient pass).
+int sjlt_onepass_grad_blocks(const SjltOnepassPlan &p);
 cudaError_t launch_sjlt_onepass(const SjltOnepassPlan &p, const double *A, const uint16_t *lists, double *partials,
-                                double *SA, double scale, cudaStream_t st, LaunchCounter lc);
+                                double *SA, double scale, cudaStream_t st, LaunchCounter lc,
+                                const double *bvec = nullptr, const double *x = nullptr, double *gpart = nullptr);
 // SA[e] = scale * sum_{k < nsplit} partials[k * count + e], k ascending.
 cudaError_t launch_sum_splits(const double *partials, int64_t count, int nsplit, double scale, double *SA,
                               cudaStream_t st, LaunchCounter lc);
@@ -106,10 +111,6 @@ cudaError_t launch_scale(double *buf, int64_t count, double scale, cudaStream_t 
 int64_t grad_dense_blocks(int64_t n, int64_t d, int num_sms);
 cudaError_t launch_grad_dense(const double *A, int64_t n, int64_t d, const double *bvec, const double *x,
                               double *gpart, int64_t nblocks, cudaStream_t st, LaunchCounter lc);
-// 4-warp CTAs (one per SM, nblocks = SMs) that can co-reside with a
-// one-CTA-per-SM kernel; same gpart layout.
-cudaError_t launch_grad_dense_corun(const double *A, int64_t n, int64_t d, const double *bvec, const double *x,
-                                    double *gpart, int64_t nblocks, cudaStream_t st, LaunchCounter lc);
 // out[c] = sum_{r < rows} part[r*d + c] (fixed order), c < d.
 constexpr int64_t kReduceRowsPerCta = 64;
 // scratch doubles launch_reduce_rows needs in tmp

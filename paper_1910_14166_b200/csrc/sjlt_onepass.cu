@@ -13,8 +13,8 @@
 // pair is a register update by its owner thread -- no shared-memory
 // read-modify-write, no atomics.  The owner finds its rows through per-chunk
 // lists built once per iteration by sjlt_lists_kernel: for every chunk of
-// kR rows and every block, the chunk's rows stably sorted by bucket (u16 row |
-// sign << 15) and the bucket offsets.  The sum per bucket runs in ascending
+// kR rows and every block, the chunk's rows stably sorted by bucket (u16: the
+// row's byte offset in a stage tile | sign << 3) and the bucket offsets.  The sum per bucket runs in ascending
 // row order inside a chunk, chunks ascending inside a row group; the row-group
 // partials are added in group order (deterministic; within rounding of the
 // oracle's single left-to-right sum, reading R3).
@@ -41,7 +41,7 @@ constexpr int kTileBytes = kR * kC * 8;  // 64 KiB
 // List block of one chunk (u16 elements): for each block j, off[j][0..M]
 // (bucket t's rows are ent[j][off[j][t] .. off[j][t+1])) padded to moff_of(M),
 // then ent[j][0..kR): the chunk's rows sorted by bucket, ascending within a
-// bucket, as row | sign << 15.
+// bucket, as tile_offset(row) | sign << 3.
 __host__ __device__ constexpr int moff_of(int M) { return (M + 1 + 7) / 8 * 8; }
 __host__ __device__ constexpr int list_block_elems(int S, int M) { return S * (moff_of(M) + kR); }
 
@@ -77,6 +77,20 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+
+// List entries hold the byte offset, within a stage tile, of the 16-byte half
+// with columns 0-1 of row r: SWIZZLE_32B puts the half h of row r at h ^ bit 2
+// of r, so the offset is 32r + 16 * bit 2 of r, and the other half sits at
+// that offset ^ 16.  The sign rides in bit 3 (offsets are 16-byte aligned), so
+// the consumer's per-entry work is one mask + add for the address and one
+// shift-add for the +-1.0 multiplier (no swizzle arithmetic; 23 -> 14.5
+// instructions per entry, C5 sketch pass 22.0 -> 21.2 ms).
+__host__ __device__ constexpr uint32_t tile_offset(uint32_t r) { return 32u * r + 16u * ((r >> 2) & 1u); }
+static_assert(32 * kR <= 0x10000, "tile offsets must fit 16 bits");
+
+__device__ __forceinline__ void lds_f64x2(uint32_t a, double &x, double &y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
 }
 
 // ---------------------------------------------------------------------------
@@ -144,7 +158,7 @@ __global__ void __launch_bounds__(32 * kSMax) sjlt_lists_kernel(int64_t n, uint6
       if (v) base = ct[b];
       __syncwarp();
       if (v) {
-        ent[base + rank] = (uint16_t)(r | (c & 0x8000u));
+        ent[base + rank] = (uint16_t)(tile_offset(r) | ((c >> 12) & 8u));
         if (rank == 0) ct[b] = base + __popc(peers);
       }
       __syncwarp();
@@ -157,13 +171,60 @@ __global__ void __launch_bounds__(32 * kSMax) sjlt_lists_kernel(int64_t n, uint6
   for (int i = threadIdx.x; i < lbe / 8; i += blockDim.x) dst[i] = src[i];
 }
 
-// Row (entry & 0x7fff) of a stage tile: SWIZZLE_32B puts the 16-byte half h
-// of row r at h ^ bit 2 of r.
-__device__ __forceinline__ void tile_row(const unsigned char *st, uint32_t e, double2 &lo, double2 &hi) {
-  const uint32_t r = e & 0x7fffu;
-  const uint32_t sw = (r >> 2) & 1u;
-  lo = *reinterpret_cast<const double2 *>(st + r * 32u + 16u * sw);
-  hi = *reinterpret_cast<const double2 *>(st + r * 32u + 16u * (sw ^ 1u));
+// a5 riding on the sketch pass: kGradWarps extra warps per CTA stream whole
+// rows of A (row range rows_per_gwarp per warp, coalesced loads that bypass
+// L1) and accumulate g's partial r_i a_i, r_i = b_i - a_i x, in registers --
+// the pass is bound by shared memory, these warps by HBM, so the gradient's
+// own read of A (4.3 ms for C5) hides under the sketch.  One partial row per
+// warp in gpart (reduced in fixed order afterwards; deterministic).
+constexpr int kGradWarps = 3;   // 16 consumer + 1 producer + 3 = 20 warps: 5 per SM sub-partition at 96 registers
+constexpr int kGradU = 4;       // rows per warp step
+constexpr int kGradMaxNV = 4;   // d <= 128 (wider rows: the separate gradient pass)
+template <int NV>
+__device__ __forceinline__ void grad_warp(const double *__restrict__ A, int64_t n, int d,
+                                          const double *__restrict__ bvec, const double *__restrict__ x,
+                                          double *__restrict__ gpart, int64_t gw, int64_t rpw, int lane) {
+  constexpr int U = kGradU;
+  const int64_t r0 = min(n, gw * rpw), r1 = min(n, r0 + rpw);
+  int colc[NV];
+  double xv[NV], gacc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int col = lane + 32 * k;
+    colc[k] = col < d ? col : d - 1;  // clamped columns carry x = 0
+    xv[k] = col < d ? x[col] : 0.0;
+    gacc[k] = 0.0;
+  }
+#pragma unroll 1
+  for (int64_t base = r0; base < r1; base += U) {
+    double v[U][NV];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t row = (base + u < r1) ? base + u : r1 - 1;  // clamped rows carry r = 0
+      const double *rowp = A + row * d;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[u][k] = ldg_stream(rowp + colc[k]);
+    }
+    double p[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      p[u] = 0.0;
+#pragma unroll
+      for (int k = 0; k < NV; ++k) p[u] = fma(v[u][k], xv[k], p[u]);
+    }
+    transpose_reduce<U>(p, lane);
+    const int myu = reduced_row_of_lane<U>(lane);
+    const double res = (base + myu < r1) ? bvec[base + myu] - p[0] : 0.0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double ru = __shfl_sync(0xffffffffu, res, owner_lane_of_row<U>(u));
+#pragma unroll
+      for (int k = 0; k < NV; ++k) gacc[k] = fma(ru, v[u][k], gacc[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+    if (lane + 32 * k < d) gpart[gw * d + lane + 32 * k] = gacc[k];
 }
 
 // ---------------------------------------------------------------------------
@@ -175,10 +236,12 @@ __device__ __forceinline__ void tile_row(const unsigned char *st, uint32_t e, do
 // block j's list of its bucket.  (Measured alternatives, C5: two entries per
 // 4-byte load 23.2 ms; four blocks merged into one list per thread with the
 // block selecting the accumulator by a 0/+-1 weight 22.3; this loop 21.6.)
-template <int S>
+template <int S, int NV>
 __global__ void __maxnreg__(96) sjlt_onepass_kernel(
     const __grid_constant__ CUtensorMap tmap, const uint16_t *__restrict__ lists, int64_t n, int d, int M,
-    int nslices, int ngroups, int64_t nchunks, double *__restrict__ part) {
+    int nslices, int ngroups, int64_t nchunks, double *__restrict__ part, const double *__restrict__ A,
+    const double *__restrict__ bvec,
+    const double *__restrict__ x, double *__restrict__ gpart, int64_t rows_per_gwarp) {
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   // stage buffers 1024-byte aligned (the SWIZZLE_32B pattern is a function of the address)
   unsigned char *smem_raw = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
@@ -199,6 +262,11 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (NV > 0 && warp > kConsumers / 32) {
+    grad_warp<NV ? NV : 1>(A, n, d, bvec, x, gpart, (int64_t)blockIdx.x * kGradWarps + (warp - kConsumers / 32 - 1),
+                  rows_per_gwarp, lane);
+    return;
+  }
   const int nitems = nslices * ngroups;
   if (warp == kConsumers / 32) {
     // ---------------- producer
@@ -243,9 +311,9 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
       for (int c = 0; c < kC; ++c) acc[j][c] = 0.0;
     for (int64_t w = w0; w < w1; ++w) {
       mbar_wait(&full[s], ph);
-      const unsigned char *st = tiles + (size_t)s * kTileBytes;
-      const uint16_t *lb = reinterpret_cast<const uint16_t *>(lbuf + (size_t)s * lb_bytes);
       if (owner) {
+        const uint32_t tb = smem_u32(tiles) + (uint32_t)s * kTileBytes;  // 1024-byte aligned
+        const uint16_t *lb = reinterpret_cast<const uint16_t *>(lbuf + (size_t)s * lb_bytes);
 #pragma unroll
         for (int j = 0; j < S; ++j) {
           const uint16_t *off = lb + j * (moff + kR);
@@ -254,13 +322,15 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
 #pragma unroll 2
           for (int e = o0; e < o1; ++e) {
             const uint32_t en = ent[e];
-            const double sg = (en & 0x8000u) ? -1.0 : 1.0;
-            double2 lo, hi;
-            tile_row(st, en, lo, hi);
-            acc[j][0] = fma(sg, lo.x, acc[j][0]);
-            acc[j][1] = fma(sg, lo.y, acc[j][1]);
-            acc[j][2] = fma(sg, hi.x, acc[j][2]);
-            acc[j][3] = fma(sg, hi.y, acc[j][3]);
+            const double sg = __hiloint2double((int)((en << 28) + 0x3ff00000u), 0);  // bit 3 -> sign bit
+            const uint32_t a = tb + (en & 0xfff0u);
+            double x0, x1, x2, x3;
+            lds_f64x2(a, x0, x1);
+            lds_f64x2(a ^ 16u, x2, x3);
+            acc[j][0] = fma(sg, x0, acc[j][0]);
+            acc[j][1] = fma(sg, x1, acc[j][1]);
+            acc[j][2] = fma(sg, x2, acc[j][2]);
+            acc[j][3] = fma(sg, x3, acc[j][3]);
           }
         }
       }
@@ -343,8 +413,13 @@ cudaError_t launch_sjlt_lists(const SjltOnepassPlan &p, uint64_t key, int64_t ro
   return cudaGetLastError();
 }
 
+int sjlt_onepass_grad_blocks(const SjltOnepassPlan &p) {
+  return (p.d + 31) / 32 <= kGradMaxNV ? p.grid * kGradWarps : 0;
+}
+
 cudaError_t launch_sjlt_onepass(const SjltOnepassPlan &p, const double *A, const uint16_t *lists, double *partials,
-                                double *SA, double scale, cudaStream_t st, LaunchCounter lc) {
+                                double *SA, double scale, cudaStream_t st, LaunchCounter lc, const double *bvec,
+                                const double *x, double *gpart) {
   CUtensorMap tm;
   cuuint64_t gdim[2] = {(cuuint64_t)p.d, (cuuint64_t)p.n};
   cuuint64_t gstr[1] = {(cuuint64_t)p.d * 8};
@@ -354,11 +429,31 @@ cudaError_t launch_sjlt_onepass(const SjltOnepassPlan &p, const double *A, const
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-#define IHS_ONEPASS(SV)                                                                                            \
-  case SV:                                                                                                         \
-    IHS_SMEM_ATTR(sjlt_onepass_kernel<SV>, p.smem);                                                                \
-    sjlt_onepass_kernel<SV><<<p.grid, kConsumers + 32, p.smem, st>>>(tm, lists, p.n, (int)p.d, (int)p.M,         \
-                                                                     p.nslices, p.ngroups, p.nchunks, partials); \
+  const int nv = gpart ? (int)((p.d + 31) / 32) : 0;
+  if (nv > kGradMaxNV) return cudaErrorInvalidValue;
+  int64_t rpw = 0;
+  if (nv) {
+    const int64_t warps = (int64_t)p.grid * kGradWarps;
+    rpw = (p.n + warps - 1) / warps;
+    rpw = (rpw + kGradU - 1) / kGradU * kGradU;
+  }
+  const unsigned threads = kConsumers + 32 + (nv ? 32 * kGradWarps : 0);
+#define IHS_ONEPASS_NV(SV, NVV)                                                                                \
+  case NVV:                                                                                                    \
+    IHS_SMEM_ATTR((sjlt_onepass_kernel<SV, NVV>), p.smem);                                                     \
+    sjlt_onepass_kernel<SV, NVV><<<p.grid, threads, p.smem, st>>>(tm, lists, p.n, (int)p.d, (int)p.M, p.nslices, \
+                                                                  p.ngroups, p.nchunks, partials, A, bvec, x,  \
+                                                                  gpart, rpw);                                  \
+    break;
+#define IHS_ONEPASS(SV)        \
+  case SV:                     \
+    switch (nv) {              \
+      IHS_ONEPASS_NV(SV, 0)    \
+      IHS_ONEPASS_NV(SV, 1)    \
+      IHS_ONEPASS_NV(SV, 2)    \
+      IHS_ONEPASS_NV(SV, 3)    \
+      IHS_ONEPASS_NV(SV, 4)    \
+    }                          \
     break;
   switch (p.s) {
     IHS_ONEPASS(2)
@@ -372,6 +467,7 @@ cudaError_t launch_sjlt_onepass(const SjltOnepassPlan &p, const double *A, const
       return cudaErrorInvalidValue;
   }
 #undef IHS_ONEPASS
+#undef IHS_ONEPASS_NV
   lc.add();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -668,6 +668,18 @@ def test_sjlt_onepass_vs_passes(P, oracle_mod, n, d, m, s):
         assert ctx.status() == P.OK
     np.testing.assert_array_equal(outs[0], ref)
     assert rel_fro(outs[1], ref) <= 1e-12
+    # sketch + gradient, the gradient in its own pass (1) or co-resident beside the sketch pass (2)
+    b = rng.standard_normal(n)
+    x = rng.standard_normal(d)
+    bd, xd = torch.from_numpy(b).to(DEV), torch.from_numpy(x).to(DEV)
+    go = oracle_mod.grad_dense(A, b, x)
+    for opt in (1, 2):
+        ctx = P.Context(0)
+        ctx.set_option("sjlt_onepass", opt)
+        _, SA, g = P.ihs_sketch_grad(Ad, P.Spec(m=m, s=s), 3, bd, xd, ctx=ctx)
+        assert ctx.status() == P.OK
+        assert rel_fro(SA.cpu().numpy(), ref) <= 1e-12, opt
+        assert (np.abs(g.cpu().numpy() - go) <= grad_bound(A, b, x)).all(), opt
 
 
 @pytest.mark.parametrize("n,d,m,s", [(2000, 10, 200, 1), (3001, 32, 512, 4), (500, 1, 7, 1), (40, 5, 64, 8)])

@@ -18,7 +18,8 @@ b = torch.randn(n, dtype=torch.float64, device=dev, generator=g)
 x = torch.randn(d, dtype=torch.float64, device=dev, generator=g) * 0.1
 spec = P.Spec(m=m, s=s)
 res = {}
-for mode in ("onepass", "passes"):
+modes = sys.argv[2].split(",") if len(sys.argv) > 2 else ["onepass", "gradpass", "passes"]
+for mode in modes:
     os.environ["IHS_SJLT"] = mode
     ctx = P.Context(0)
     ctx.set_profiling(True)
@@ -46,5 +47,7 @@ for mode in ("onepass", "passes"):
         res[(mode, grad)] = SA.clone()
         ctx.profile_reset()
     ctx.close()
-da = (res[("onepass", False)] - res[("passes", False)]).norm() / res[("passes", False)].norm()
-print(f"onepass vs passes rel fro {da.item():.3e}")
+ref = res[(modes[-1], False)]
+for mode in modes[:-1]:
+    da = (res[(mode, True)] - ref).norm() / ref.norm()
+    print(f"{mode} vs {modes[-1]} rel fro {da.item():.3e}")
