@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-1e-10 solve")
+    ap.add_argument("--allreduce", default="nccl", choices=["nccl", "nvls"],
+                    help="N > 1: the [SA | g] exchange through NCCL (default) or the library's NVLS multimem kernel")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: host-staged all-reduce, for testing the "
@@ -437,7 +439,11 @@ def main():
     del xs
     ctx = P.Context(local)
     spec = P.Spec(m=cfg.m, s=cfg.s, seed=cfg.hash_seed)
-    S = ShardedIHS(Am, b, spec, ops=CudaOps(ctx), constraint=cfg.constraint, radius=radius)
+    exch = None
+    if world > 1 and args.allreduce == "nvls":
+        from paper_1910_14166_b200.dist import NvlsAllreduce
+        exch = NvlsAllreduce(cfg.m * cfg.d + cfg.d, dev, ctx=ctx)
+    S = ShardedIHS(Am, b, spec, ops=CudaOps(ctx), constraint=cfg.constraint, radius=radius, allreduce=exch)
     d = cfg.d
     xa = torch.zeros(d, dtype=torch.float64, device=dev)
     xb = torch.empty_like(xa)
@@ -651,6 +657,8 @@ def main():
         if world > 1:
             out["ranks_bitwise_identical_x"] = ranks_same
             out["dist_backend"] = args.dist_backend
+            out["exchange"] = ("NVLS multimem kernel (ihs_allreduce_multimem)" if args.allreduce == "nvls"
+                               else "NCCL all-reduce")
             out["nccl"] = nccl_summary(nccl_log)
         print(json.dumps(out))
     if world > 1:

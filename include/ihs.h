@@ -170,6 +170,20 @@ ihs_status ihs_nccl_unique_id(void *out128);
 ihs_status ihs_ctx_set_comm(ihs_ctx ctx, int rank, int world, const void *unique_id128);
 /* In-place sum of count doubles across the ctx communicator (a3). */
 ihs_status ihs_allreduce_sum(ihs_ctx ctx, double *buf, int64_t count);
+/* a3 over NVLink SHARP (the sum of the per-rank partial
+ * sketches and gradients, exact by linearity): in-place sum of
+ * count doubles of a symmetric buffer across `world` ranks, in one kernel that
+ * reduces with multimem.ld_reduce.add.f64 on the buffer's multicast address
+ * (`mc_buf`, device) and broadcasts with multimem.st -- rank r handles slice r
+ * -- between two barriers over the ranks' signal pads (`signal_pads`: device
+ * array of `world` unicast pointers, each >= pad_slots u32, zero before first
+ * use and left zero).  The buffer, its multicast mapping and the pads come
+ * from the caller (e.g. torch symmetric memory); every rank calls with the
+ * same count.  IHS_ERR_UNSUPPORTED when the pads are too small (blocks x world
+ * slots, blocks <= SM count).  Not the default exchange (NCCL is): every rank
+ * receives the same broadcast value. */
+ihs_status ihs_allreduce_multimem(ihs_ctx ctx, double *mc_buf, uint32_t *const *signal_pads, int rank, int world,
+                                  int64_t count, int64_t pad_slots);
 
 /* a1: export buckets/signs of global rows [row_begin, row_begin+count), arrays
  * of count*s entries ordered (row, block) -- bit-exact test interface.

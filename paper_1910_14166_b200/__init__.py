@@ -76,6 +76,8 @@ _EXPORTS = {
     "ihs_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "ihs_ctx_set_comm": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "ihs_allreduce_sum": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+    "ihs_allreduce_multimem": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int64,
+                                         C.c_int64]),
     "ihs_hash": (C.c_int, [C.c_void_p, C.POINTER(SketchSpec), C.c_uint64, C.c_int64, C.c_int64, C.c_void_p,
                            C.c_void_p]),
     "ihs_sketch": (C.c_int, [C.c_void_p, C.POINTER(Matrix), C.POINTER(SketchSpec), C.c_uint64, C.c_void_p,
@@ -307,6 +309,16 @@ def _f64(n, device):
 
 
 # ------------------------------------------------------------------ a1
+def ihs_allreduce_multimem(mc_ptr: int, pads: torch.Tensor, rank: int, world: int, count: int, pad_slots: int,
+                           ctx: Context | None = None) -> None:
+    """a3 over NVLS: in-place sum of `count` doubles of a symmetric buffer whose
+    multicast address is mc_ptr; pads = int64 device tensor of the ranks'
+    signal-pad pointers (ihs.h)."""
+    ctx = ctx or default_context(pads.device)
+    _check(lib().ihs_allreduce_multimem(ctx._bind(), C.c_void_p(mc_ptr), _p(pads), rank, world, count, pad_slots),
+           "ihs_allreduce_multimem")
+
+
 def ihs_hash(spec: Spec, it: int, row_begin: int, count: int, ctx: Context | None = None, device=None):
     ctx = ctx or default_context(device)
     dev = torch.device("cuda", ctx.device)

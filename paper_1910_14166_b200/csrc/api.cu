@@ -1284,6 +1284,18 @@ ihs_status ihs_allreduce_sum(ihs_ctx c, double *buf, int64_t count) {
   return allreduce_impl(c, buf, count);
 }
 
+ihs_status ihs_allreduce_multimem(ihs_ctx c, double *mc_buf, uint32_t *const *signal_pads, int rank, int world,
+                                  int64_t count, int64_t pad_slots) {
+  if (!c || count < 0 || world < 1 || rank < 0 || rank >= world) return IHS_ERR_INVALID_ARGUMENT;
+  if (count == 0) return IHS_OK;
+  if (!mc_buf || !signal_pads) return IHS_ERR_INVALID_ARGUMENT;
+  DevGuard g(c->device);
+  const int blocks = nvls_blocks(count, world, c->num_sms);
+  if ((int64_t)blocks * world > pad_slots) return IHS_ERR_UNSUPPORTED;
+  IHS_CUDA(launch_nvls_allreduce(mc_buf, signal_pads, rank, world, count, blocks, c->stream, lc_of(c)));
+  return IHS_OK;
+}
+
 ihs_status ihs_hash(ihs_ctx c, const ihs_sketch_spec *spec, uint64_t iter, int64_t row_begin, int64_t count,
                     int32_t *bucket, int8_t *sign) {
   if (!c) return IHS_ERR_INVALID_ARGUMENT;

@@ -99,6 +99,14 @@ cudaError_t launch_sjlt_onepass(const SjltOnepassPlan &p, const double *A, const
 cudaError_t launch_sum_splits(const double *partials, int64_t count, int nsplit, double scale, double *SA,
                               cudaStream_t st, LaunchCounter lc);
 
+// ---- a3 over NVLS multicast (nvls.cu) ----------------------------------------
+// In-place sum of count doubles of a symmetric buffer across `world` ranks:
+// mc = its multicast address, pads = device array of the world ranks' signal
+// pads (unicast pointers, >= blocks * world u32 each, zero on first use).
+int nvls_blocks(int64_t count, int world, int num_sms);
+cudaError_t launch_nvls_allreduce(double *mc, uint32_t *const *pads, int rank, int world, int64_t count, int blocks,
+                                  cudaStream_t st, LaunchCounter lc);
+
 // ---- CSR sketch and gradient (atomics into L2) ------------------------------
 // SA must be zeroed first when sketching.  g must be zeroed when gradient.
 cudaError_t launch_csr_sketch_grad(int64_t n, int64_t d, const int64_t *row_ptr, const int32_t *col,

@@ -30,6 +30,34 @@ def torch_allreduce(buf: torch.Tensor, group=None) -> None:
         dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
 
 
+class NvlsAllreduce:
+    """a3 through NVLink SHARP: the [SA | g] sum as one library kernel
+    (ihs_allreduce_multimem: multimem.ld_reduce.add.f64 + multimem.st on the
+    multicast address) on a torch symmetric-memory buffer -- torch provides
+    the buffer, its multicast mapping and the signal pads (plumbing).  Use as
+    ShardedIHS(allreduce=NvlsAllreduce(m * d + d, device)).  Raises when the
+    system gives no multicast mapping (then NCCL, the default, stays)."""
+
+    def __init__(self, numel: int, device, group=None, ctx: "P.Context | None" = None):
+        import torch.distributed._symmetric_memory as symm_mem
+        self.ctx = ctx or P.default_context(device)
+        self.buf = symm_mem.empty(numel, dtype=torch.float64, device=device)
+        grp = group if group is not None else dist.group.WORLD
+        self.h = symm_mem.rendezvous(self.buf, grp.group_name)
+        if not self.h.multicast_ptr:
+            raise RuntimeError("no NVLS multicast mapping for this group")
+        self.pads = torch.tensor(list(self.h.signal_pad_ptrs), dtype=torch.int64, device=device)
+        self.pad_slots = int(self.h.signal_pad_size) // 4
+
+    def __call__(self, t: torch.Tensor) -> None:
+        n = t.numel()
+        flat = t.view(-1)
+        self.buf[:n].copy_(flat)
+        P.ihs_allreduce_multimem(int(self.h.multicast_ptr), self.pads, int(self.h.rank), int(self.h.world_size), n,
+                                 self.pad_slots, ctx=self.ctx)
+        flat.copy_(self.buf[:n])
+
+
 class CudaOps:
     """The product backend: every call goes to the C ABI."""
 
