@@ -17,7 +17,7 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = ["DMMA", "HMMA", "UTCHMMA", "UTMALDG", "UTMASTG", "UBLKCP", "REDG", "RED", "ATOMS", "ATOMG", "ATOM", "LDS",
         "STS", "LDG", "STG", "SHFL", "MATCH", "VOTE", "DFMA", "DADD", "DMUL", "MUFU", "SYNCS", "BAR", "UCGABAR",
-        "LDTM", "STTM", "CCTL", "MEMBAR", "ERRBAR"]
+        "LDTM", "STTM", "CCTL", "MEMBAR", "ERRBAR", "LDGMC"]
 
 
 def demangle(name):
