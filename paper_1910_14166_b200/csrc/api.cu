@@ -621,7 +621,7 @@ ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, dou
   // cluster; larger d (OLS with the CG update, e.g. C3): a full plan reading
   // SA evict_first, beside the CG solve and the next pass's L2 reductions
   const bool wide = d > 256;
-  GramPlan p = gram_plan(m, d, wide ? c->num_sms : std::min(16, c->num_sms));
+  GramPlan p = gram_plan(m, d, wide ? c->num_sms : std::min(16, c->num_sms), 2, wide);
   double *part;
   IHS_TRY(scratch(c, S_GRAMF, p.partial_bytes(), &part));  // (before factor_begin: a regrowth joins)
   const bool power = pg_supported(d);

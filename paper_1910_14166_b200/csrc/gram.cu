@@ -282,9 +282,151 @@ __global__ void __launch_bounds__(256) gram_streamk_reduce_kernel(const double *
   H[(int64_t)q * d + p] = s;
 }
 
+// ---------------------------------------------------------------------------
+// Stream-K with 128 x 128 tiles for large d (d >= 512: C3's 36 upper tiles):
+// half the L2 operand reads of the 64 x 64 tiles (each CTA tile reads 2 x 128
+// columns of SA per k-row for 128 x 128 outputs) -- the look-ahead Gram runs
+// beside the CSR pass, which is bound by its L2 reductions -- and twice the
+// DMMAs per shared-memory fragment load.  8 warps, warp (wm, wn) owns rows
+// [32 wm, +32) x columns [64 wn, +64) as 4 x 8 DMMA 8 x 8 tiles (64 fp64
+// accumulators a thread); one CTA per SM; kStages128 stages of KC128 rows.
+constexpr int GT2 = 128;
+constexpr int KC2 = 16;
+constexpr int LDS2 = GT2 + 4;  // == 4 mod 16 doubles: conflict-free fragment loads
+constexpr int kStages2 = 3;
+
+__global__ void __launch_bounds__(256, 1) gram_streamk128_kernel(const double *__restrict__ SA, int64_t m, int d,
+                                                                 int tiles, int ntri, int kch, int ipc,
+                                                                 double *__restrict__ partials,
+                                                                 int *__restrict__ slot_tile, int hint) {
+  extern __shared__ double sm[];
+  double *Xp = sm;                          // [kStages2][KC2][LDS2]
+  double *Xq = sm + kStages2 * KC2 * LDS2;  // [kStages2][KC2][LDS2]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int64_t total = (int64_t)ntri * kch;
+  const int64_t i0 = (int64_t)blockIdx.x * ipc, i1 = min(total, i0 + ipc);
+  if (tid == 0) slot_tile[2 * blockIdx.x] = slot_tile[2 * blockIdx.x + 1] = -1;
+  uint64_t pol = 0;
+  if (hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  double acc[4][8][2];
+  int cur = -1, slot = 0;
+  auto flush = [&]() {
+    double *out = partials + ((int64_t)blockIdx.x * 2 + slot) * (GT2 * GT2);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int r = 32 * wm + 8 * i + (lane >> 2);
+        const int c = 64 * wn + 8 * j + 2 * (lane & 3);
+        *reinterpret_cast<double2 *>(out + r * GT2 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      }
+    if (tid == 0) slot_tile[2 * blockIdx.x + slot] = cur;
+    ++slot;
+  };
+  for (int64_t it = i0; it < i1; ++it) {
+    const int tile = (int)(it / kch), kc = (int)(it % kch);
+    if (tile != cur) {
+      if (cur >= 0) flush();
+      cur = tile;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    int P, Q;
+    tri_decode(tile, tiles, P, Q);
+    const bool diag = (P == Q);
+    const int64_t k0 = m * kc / kch, k1 = m * (kc + 1) / kch;
+    auto load_stage = [&](int buf, int64_t kb) {
+      // KC2 x 128 doubles per matrix in 16-byte pieces: 1024 / 256 threads = 4 each
+#pragma unroll
+      for (int t2 = 0; t2 < (KC2 * GT2 / 2) / 256; ++t2) {
+        const int e = t2 * 256 + tid;
+        const int r = e / (GT2 / 2), c = 2 * (e % (GT2 / 2));
+        const int64_t row = kb + r;
+        const bool rin = row < k1;
+        const int cp = P * GT2 + c, cq = Q * GT2 + c;
+        const double *gp = SA + (rin ? row : 0) * d + (cp < d ? cp : 0);
+        const double *gq = SA + (rin ? row : 0) * d + (cq < d ? cq : 0);
+        if (hint) {
+          cp_async16_hint(&Xp[(buf * KC2 + r) * LDS2 + c], gp, rin && cp < d, pol);
+          if (!diag) cp_async16_hint(&Xq[(buf * KC2 + r) * LDS2 + c], gq, rin && cq < d, pol);
+        } else {
+          cp_async16(&Xp[(buf * KC2 + r) * LDS2 + c], gp, rin && cp < d);
+          if (!diag) cp_async16(&Xq[(buf * KC2 + r) * LDS2 + c], gq, rin && cq < d);
+        }
+      }
+      cp_async_commit();
+    };
+    const int nstages = (int)((k1 - k0 + KC2 - 1) / KC2);
+    // prologue: kStages2 - 1 stages in flight (empty groups keep the count uniform)
+#pragma unroll
+    for (int q = 0; q < kStages2 - 1; ++q) {
+      if (q < nstages)
+        load_stage(q, k0 + (int64_t)q * KC2);
+      else
+        cp_async_commit();
+    }
+    for (int s2 = 0; s2 < nstages; ++s2) {
+      cp_async_wait<kStages2 - 2>();
+      __syncthreads();
+      const int nxt = s2 + kStages2 - 1;
+      if (nxt < nstages)
+        load_stage(nxt % kStages2, k0 + (int64_t)nxt * KC2);
+      else
+        cp_async_commit();
+      const int buf = s2 % kStages2;
+      const double *xp = Xp + buf * KC2 * LDS2;
+      const double *xq = (diag ? Xp : Xq) + buf * KC2 * LDS2;
+#pragma unroll 1
+      for (int kk = 0; kk < KC2; kk += 4) {
+        const int kr = kk + (lane & 3);
+        double a[4], b[8];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = xp[kr * LDS2 + 32 * wm + 8 * i + (lane >> 2)];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) b[j] = xq[kr * LDS2 + 64 * wn + 8 * j + (lane >> 2)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+  }
+  if (cur >= 0) flush();
+}
+
+// Per 128-tile: the partials of the CTAs that covered it, in CTA order; scale^2, mirror.
+// grid: tile x 64 chunks of 256 elements.
+__global__ void __launch_bounds__(256) gram_streamk128_reduce_kernel(const double *__restrict__ partials,
+                                                                     const int *__restrict__ slot_tile, int d,
+                                                                     int tiles, int kch, int ipc, double scale2,
+                                                                     double *__restrict__ H) {
+  const int t = blockIdx.x;
+  int P, Q;
+  tri_decode(t, tiles, P, Q);
+  const int e = blockIdx.y * 256 + threadIdx.x;
+  const int r = e / GT2, c = e % GT2;
+  const int p = P * GT2 + r, q = Q * GT2 + c;
+  if (p >= d || q >= d) return;
+  if (P == Q && q < p) return;
+  const int64_t c0 = ((int64_t)t * kch) / ipc, c1 = ((int64_t)t * kch + kch - 1) / ipc;
+  double s = 0.0;
+  for (int64_t cta = c0; cta <= c1; ++cta) {
+    const int sl = slot_tile[2 * cta] == t ? 0 : 1;
+    s += partials[((int64_t)cta * 2 + sl) * (GT2 * GT2) + e];
+  }
+  s *= scale2;
+  H[(int64_t)p * d + q] = s;
+  H[(int64_t)q * d + p] = s;
+}
+
 }  // namespace
 
-GramPlan gram_plan(int64_t m, int64_t d, int num_sms, int ctas_per_sm) {
+GramPlan gram_plan(int64_t m, int64_t d, int num_sms, int ctas_per_sm, bool beside) {
   GramPlan p;
   p.m = m;
   p.d = d;
@@ -319,12 +461,54 @@ GramPlan gram_plan(int64_t m, int64_t d, int num_sms, int ctas_per_sm) {
     p.ncta = (int)((p.ntri * best + p.ipc - 1) / p.ipc);
     if (p.ipc > p.kch) p.ncta = 0;  // a CTA would span three tiles: keep split-K
   }
+  // 128 x 128 tiles (one CTA per SM) for d >= 512 when the Gram runs BESIDE
+  // another kernel (the look-ahead Gram next to the CSR pass, C3): alone it
+  // is slower than the 64 x 64 stream-K (0.357 vs 0.322 ms: one CTA of 8
+  // warps per SM hides less latency), beside the pass it leaves the pass's
+  // CTAs room and halves the L2 operand reads (C3 step 0.631 -> 0.426 ms)
+  if (beside && p.ncta > 0 && d >= 512 && num_sms >= 64 && m >= 1024) {
+    const int t2 = (int)((d + GT2 - 1) / GT2);
+    const int64_t ntri2 = (int64_t)t2 * (t2 + 1) / 2;
+    const int64_t ncta = num_sms;
+    const int64_t kmin = std::max<int64_t>(1, (2 * ncta + ntri2 - 1) / ntri2);
+    const int64_t kmax = std::max<int64_t>(kmin, m / 64);
+    int64_t best = kmin;
+    double best_waste = 1e30;
+    for (int64_t k = kmin; k <= kmax && k <= 8 * kmin; ++k) {
+      const int64_t tot = ntri2 * k, ipc = (tot + ncta - 1) / ncta;
+      const double waste = (double)(ipc * ncta - tot) / (double)tot;
+      if (waste < best_waste - 1e-9) {
+        best_waste = waste;
+        best = k;
+      }
+    }
+    const int ipc2 = (int)((ntri2 * best + ncta - 1) / ncta);
+    if (ipc2 <= best) {
+      p.gt = GT2;
+      p.tiles = t2;
+      p.ntri = (int)ntri2;
+      p.kch = (int)best;
+      p.ipc = ipc2;
+      p.ncta = (int)((ntri2 * best + ipc2 - 1) / ipc2);
+    }
+  }
   return p;
 }
 
 cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
                         cudaStream_t st, LaunchCounter lc, int hint) {
   const size_t smem = (size_t)4 * KC * LDS * 8;
+  if (p.gt == GT2 && p.ncta > 0 && (reinterpret_cast<uintptr_t>(SA) % 16) == 0) {
+    const size_t smem2 = (size_t)2 * kStages2 * KC2 * LDS2 * 8;
+    IHS_SMEM_ATTR(gram_streamk128_kernel, smem2);
+    int *slot_tile = reinterpret_cast<int *>(partials + (size_t)p.ncta * 2 * GT2 * GT2);
+    gram_streamk128_kernel<<<p.ncta, 256, smem2, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kch, p.ipc, partials,
+                                                       slot_tile, hint);
+    gram_streamk128_reduce_kernel<<<dim3(p.ntri, (GT2 * GT2) / 256), 256, 0, st>>>(
+        partials, slot_tile, (int)p.d, p.tiles, p.kch, p.ipc, scale * scale, H);
+    lc.add(2);
+    return cudaGetLastError();
+  }
   if (p.ncta > 0 && (reinterpret_cast<uintptr_t>(SA) % 16) == 0) {
     const size_t smem_sk = (size_t)2 * kStagesK * KC * LDS * 8;
     IHS_SMEM_ATTR(gram_streamk_kernel, smem_sk);

@@ -133,17 +133,20 @@ cudaError_t launch_reduce_rows(const double *part, int64_t rows, int64_t d, doub
 // ---- a4 Gram on DMMA ---------------------------------------------------------
 struct GramPlan {
   int64_t m = 0, d = 0;
-  int tiles = 0;    // tiles per side (64-wide)
+  int gt = 64;      // tile edge (64, or 128 for the large-d stream-K kernel)
+  int tiles = 0;    // tiles per side (gt-wide)
   int ntri = 0;     // upper-triangular tiles
   int nsplit = 0;   // split-K
   int64_t kchunk = 0;
   int ncta = 0, kch = 0, ipc = 0;  // stream-K (ncta > 0): CTAs, k-chunks per tile, items per CTA
   size_t partial_bytes() const {
-    const size_t sk = (size_t)ncta * 2 * 64 * 64 * 8 + (size_t)ncta * 2 * 4 + 64;
+    const size_t sk = (size_t)ncta * 2 * gt * gt * 8 + (size_t)ncta * 2 * 4 + 64;
     return std::max((size_t)nsplit * ntri * 64 * 64 * 8, sk);
   }
 };
-GramPlan gram_plan(int64_t m, int64_t d, int num_sms, int ctas_per_sm = 2);
+// beside: the Gram shares the GPU with another kernel (the look-ahead Gram);
+// for d >= 512 it then takes 128 x 128 tiles, one CTA per SM.
+GramPlan gram_plan(int64_t m, int64_t d, int num_sms, int ctas_per_sm = 2, bool beside = false);
 // hint = 1: SA is read with an L2 evict_first policy (stream-K plans only)
 cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, double *partials, double *H,
                         cudaStream_t st, LaunchCounter lc, int hint = 0);

@@ -173,6 +173,22 @@ def test_gram(P, oracle_mod, m, d):
     assert rel_fro(H2, 0.25 * Ho) <= 1e-12
 
 
+@pytest.mark.parametrize("m,d", [(8192, 1024), (2048, 1000), (1024, 513), (4096, 640), (1500, 777), (3000, 300)])
+def test_gram_lookahead_tiles(P, oracle_mod, m, d):
+    """The look-ahead Gram (ihs_gram_lookahead, the factor stream): for d >= 512
+    the 128 x 128-tile stream-K kernel (one CTA per SM), ragged last tiles
+    (513, 640, 777, 1000) and uneven k-chunks; d = 300 takes the 64-tile plan."""
+    rng = np.random.default_rng(m + d)
+    SA = torch.from_numpy(rng.standard_normal((m, d))).to(DEV)
+    ctx = P.Context(0)
+    H = P.ihs_gram_lookahead(SA, scale=0.5, ctx=ctx)
+    ctx.synchronize()
+    Ho = oracle_mod.gram(SA.cpu().numpy())
+    Hn = H.cpu().numpy()
+    assert rel_fro(Hn, 0.25 * Ho) <= 1e-12
+    np.testing.assert_array_equal(Hn, Hn.T)
+
+
 # ---------------------------------------------------------------- a6 inner QP
 def spd(rng, d, cond=13.0):
     Q, _ = np.linalg.qr(rng.standard_normal((d, d)))
