@@ -153,6 +153,45 @@ def test_csr_full_size(P, oracle_mod):
     assert oracle_mod.pred_rel_err(xn.cpu().numpy(), xo, csr=(rph, clh, vlh), d=d) <= 1e-9
 
 
+def test_csr_full_size_lookahead(P, oracle_mod):
+    """C3 in the bench's launch configuration: the Gram-only look-ahead (the
+    prologue's and the step's Grams on the factor stream, 128 x 128-tile
+    stream-K beside the pass), the CG update with H_t, and S^{t+1} A."""
+    cfg = synthetic.CONFIGS["C3"]
+    prob = synthetic.problem(cfg, DEV)
+    rp, cl, vl = prob["csr"]
+    n, d, m, t = cfg.n, cfg.d, cfg.m, 4
+    ctx = P.Context(0)
+    from paper_1910_14166_b200.dist import CudaOps, ShardedIHS
+    spec = P.Spec(m=m, s=cfg.s)
+    S = ShardedIHS(P.Csr(rp, cl, vl, d), prob["b"], spec, ops=CudaOps(ctx))
+    assert S.lookahead and S.la_gram_only
+    x = torch.from_numpy(np.random.default_rng(2).standard_normal(d) * 0.1).to(DEV)
+    xn = torch.empty_like(x)
+    S.prime(t)
+    cur = S._la_cur
+    S.step(t, x, xn)
+    ctx.synchronize()
+    assert ctx.status() == P.OK
+    nxt = 1 - cur
+    rph, clh, vlh, bh, xh = rp.cpu().numpy(), cl.cpu().numpy(), vl.cpu().numpy(), prob["b"].cpu().numpy(), x.cpu().numpy()
+    SA_t = S.packs[cur][: m * d].view(m, d).cpu().numpy()
+    assert rel_fro(SA_t, oracle_mod.sketch_csr(rph, clh, vlh, d, 0, t, m, cfg.s)) <= 1e-12
+    H_t = S.Hinv[cur].cpu().numpy()
+    assert rel_fro(H_t, oracle_mod.gram(SA_t)) <= 1e-12
+    np.testing.assert_array_equal(H_t, H_t.T)
+    g_t = S.packs[nxt][m * d:].cpu().numpy()
+    go = oracle_mod.grad_csr(rph, clh, vlh, d, bh, xh)
+    import scipy.sparse as sp
+    M = sp.csr_matrix((vlh, clh, rph), shape=(n, d))
+    assert (np.abs(g_t - go) <= 1e-12 * (abs(M).T @ np.abs(bh - M @ xh))).all()
+    xo = oracle_mod.ols_step(H_t, g_t, xh)
+    assert oracle_mod.pred_rel_err(xn.cpu().numpy(), xo, csr=(rph, clh, vlh), d=d) <= 1e-9
+    SA_1 = S.packs[nxt][: m * d].view(m, d).cpu().numpy()
+    assert rel_fro(SA_1, oracle_mod.sketch_csr(rph, clh, vlh, d, 0, t + 1, m, cfg.s)) <= 1e-12
+    assert rel_fro(S.Hinv[nxt].cpu().numpy(), oracle_mod.gram(SA_1)) <= 1e-12
+
+
 @pytest.mark.parametrize("name", ["C4", "C4P"])
 def test_solve_pg_default_schedule_full_size(P, oracle_mod, name):
     """ihs_solve_l1ball (C4) / ihs_solve_lasso (C4P) at FULL size through the C

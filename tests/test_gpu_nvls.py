@@ -145,3 +145,24 @@ def test_nvls_torch_symmetric_memory_world1():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_nvls_argument_errors():
+    """ihs_allreduce_multimem's synchronous argument checks (nothing enqueued)."""
+    import paper_1910_14166_b200 as P
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    dev = torch.device("cuda", 0)
+    pads = torch.zeros(1, dtype=torch.int64, device=dev)
+    buf = torch.zeros(16, dtype=torch.float64, device=dev)
+    ctx = P.Context(0)
+    L = P.lib()
+    h = ctx._bind()
+    import ctypes as C
+    mc, pp = C.c_void_p(buf.data_ptr()), C.c_void_p(pads.data_ptr())
+    assert L.ihs_allreduce_multimem(h, mc, pp, 1, 1, 16, 1024) == P.ERR_INVALID_ARGUMENT  # rank >= world
+    assert L.ihs_allreduce_multimem(h, mc, pp, 0, 0, 16, 1024) == P.ERR_INVALID_ARGUMENT  # world < 1
+    assert L.ihs_allreduce_multimem(h, mc, pp, 0, 1, -1, 1024) == P.ERR_INVALID_ARGUMENT  # count < 0
+    assert L.ihs_allreduce_multimem(h, None, pp, 0, 1, 16, 1024) == P.ERR_INVALID_ARGUMENT  # no buffer
+    assert L.ihs_allreduce_multimem(h, mc, pp, 0, 2, 1 << 24, 3) == P.ERR_UNSUPPORTED  # pads too small
+    assert L.ihs_allreduce_multimem(h, mc, pp, 0, 1, 0, 0) == P.OK  # nothing to do
