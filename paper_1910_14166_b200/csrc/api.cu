@@ -300,10 +300,9 @@ ihs_status sketch_grad_impl(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
     if (g) IHS_CUDA(cudaMemsetAsync(g, 0, (size_t)d * 8, st));
     {
       Prof pr(c, IHS_K_CSR);
-      IHS_CUDA(launch_csr_sketch_grad(n, d, A->row_ptr, A->col_idx, A->values, A->row_offset, key, m, s, SA, b, x, g,
-                                      st, lc_of(c)));
+      IHS_CUDA(launch_csr_sketch_grad(n, d, A->row_ptr, A->col_idx, A->values, A->row_offset, key, m, s,
+                                      spec_scale(spec), SA, b, x, g, st, lc_of(c)));
     }
-    if (SA && s > 1) IHS_CUDA(launch_scale(SA, m * d, spec_scale(spec), st, lc_of(c)));
     return IHS_OK;
   }
   // dense.  CountSketch (s = 1): a stable counting sort of the rows by bucket

@@ -65,7 +65,7 @@ constexpr int kRowsPerLane = 4;
 template <bool SKETCH, bool GRAD, bool GSMEM, int SC>
 __device__ __forceinline__ void csr_row(int64_t i, int64_t e0, int64_t e1, int d, const int32_t *__restrict__ col,
                                         const double *__restrict__ val, int64_t row_offset, uint64_t key, uint32_t M,
-                                        int s_rt, double *SA, const double *__restrict__ bvec,
+                                        int s_rt, double scale, double *SA, const double *__restrict__ bvec,
                                         const double *__restrict__ x, double *g, double *gs, uint64_t pf,
                                         uint64_t pl) {
   const int s = SC > 0 ? SC : s_rt;
@@ -87,16 +87,19 @@ __device__ __forceinline__ void csr_row(int64_t i, int64_t e0, int64_t e1, int d
     for (int q = 2; q < nn; ++q) atomicAdd(&gt[col[e0 + q]], val[e0 + q] * res);
   }
   if (SKETCH) {
+    // S's entries are +-1/sqrt(s): the scale rides on each
+    // reduced value (exact for s = 1, 4: a power of two) -- no pass over SA
+    const double w0 = v0 * scale, w1 = v1 * scale;
 #pragma unroll
     for (int j = 0; j < (SC > 0 ? SC : 1); ++j) {
       for (int jj = j; jj < s; jj += (SC > 0 ? SC : 1)) {  // SC > 0: exactly once
         bool neg;
         const uint32_t b = hash_bucket(key, (uint64_t)(row_offset + i), (uint32_t)jj, (uint32_t)s, M, neg);
         double *row = SA + (int64_t)b * d;
-        red_keep(row + c0, neg ? -v0 : v0, pl);
-        if (has1) red_keep(row + c1, neg ? -v1 : v1, pl);
+        red_keep(row + c0, neg ? -w0 : w0, pl);
+        if (has1) red_keep(row + c1, neg ? -w1 : w1, pl);
         for (int q = 2; q < nn; ++q) {
-          const double vq = val[e0 + q];
+          const double vq = val[e0 + q] * scale;
           red_keep(row + col[e0 + q], neg ? -vq : vq, pl);
         }
         if (SC > 0) break;
@@ -109,8 +112,8 @@ template <bool SKETCH, bool GRAD, bool GSMEM, int SC>
 __global__ void __launch_bounds__(256, 3) csr_sketch_grad_kernel(int64_t n, int d, const int64_t *__restrict__ row_ptr,
                                                                  const int32_t *__restrict__ col,
                                                                  const double *__restrict__ val, int64_t row_offset,
-                                                                 uint64_t key, uint32_t M, int s, double *SA,
-                                                                 const double *__restrict__ bvec,
+                                                                 uint64_t key, uint32_t M, int s, double scale,
+                                                                 double *SA, const double *__restrict__ bvec,
                                                                  const double *__restrict__ x, double *g) {
   extern __shared__ double gs[];
   if (GRAD && GSMEM) {
@@ -154,8 +157,8 @@ __global__ void __launch_bounds__(256, 3) csr_sketch_grad_kernel(int64_t n, int 
     }
     __syncwarp();
     for (int q = lane; q < total; q += 32)
-      csr_row<SKETCH, GRAD, GSMEM, SC>(base + crow[q], ce0[q], ce1[q], d, col, val, row_offset, key, M, s, SA, bvec,
-                                       x, g, gs, pf, pl);
+      csr_row<SKETCH, GRAD, GSMEM, SC>(base + crow[q], ce0[q], ce1[q], d, col, val, row_offset, key, M, s, scale, SA,
+                                       bvec, x, g, gs, pf, pl);
     __syncwarp();
   }
   if (GRAD && GSMEM) {
@@ -169,44 +172,44 @@ __global__ void __launch_bounds__(256, 3) csr_sketch_grad_kernel(int64_t n, int 
 
 template <bool SKETCH, bool GRAD, int SC>
 void launch_sc(int grid, int64_t n, int d, const int64_t *row_ptr, const int32_t *col, const double *val,
-               int64_t row_offset, uint64_t key, uint32_t M, int s, double *SA, const double *bvec, const double *x,
-               double *g, cudaStream_t st) {
+               int64_t row_offset, uint64_t key, uint32_t M, int s, double scale, double *SA, const double *bvec,
+               const double *x, double *g, cudaStream_t st) {
   const size_t smem = (size_t)d * 8;
   if (GRAD && smem <= 96 * 1024) {
     IHS_SMEM_ATTR((csr_sketch_grad_kernel<SKETCH, GRAD, true, SC>), smem);
     csr_sketch_grad_kernel<SKETCH, GRAD, true, SC><<<grid, 256, smem, st>>>(n, d, row_ptr, col, val, row_offset, key,
-                                                                           M, s, SA, bvec, x, g);
+                                                                           M, s, scale, SA, bvec, x, g);
   } else {
     csr_sketch_grad_kernel<SKETCH, GRAD, false, SC><<<grid, 256, 0, st>>>(n, d, row_ptr, col, val, row_offset, key,
-                                                                         M, s, SA, bvec, x, g);
+                                                                         M, s, scale, SA, bvec, x, g);
   }
 }
 
 template <bool SKETCH, bool GRAD>
 void launch_t(int grid, int64_t n, int d, const int64_t *row_ptr, const int32_t *col, const double *val,
-              int64_t row_offset, uint64_t key, uint32_t M, int s, double *SA, const double *bvec, const double *x,
-              double *g, cudaStream_t st) {
+              int64_t row_offset, uint64_t key, uint32_t M, int s, double scale, double *SA, const double *bvec,
+              const double *x, double *g, cudaStream_t st) {
   switch (SKETCH ? s : 1) {
-    case 1: launch_sc<SKETCH, GRAD, 1>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, SA, bvec, x, g, st); break;
-    case 2: launch_sc<SKETCH, GRAD, 2>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, SA, bvec, x, g, st); break;
-    case 4: launch_sc<SKETCH, GRAD, 4>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, SA, bvec, x, g, st); break;
-    case 8: launch_sc<SKETCH, GRAD, 8>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, SA, bvec, x, g, st); break;
-    default: launch_sc<SKETCH, GRAD, 0>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, SA, bvec, x, g, st);
+    case 1: launch_sc<SKETCH, GRAD, 1>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, scale, SA, bvec, x, g, st); break;
+    case 2: launch_sc<SKETCH, GRAD, 2>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, scale, SA, bvec, x, g, st); break;
+    case 4: launch_sc<SKETCH, GRAD, 4>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, scale, SA, bvec, x, g, st); break;
+    case 8: launch_sc<SKETCH, GRAD, 8>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, scale, SA, bvec, x, g, st); break;
+    default: launch_sc<SKETCH, GRAD, 0>(grid, n, d, row_ptr, col, val, row_offset, key, M, s, scale, SA, bvec, x, g, st);
   }
 }
 }  // namespace
 
 cudaError_t launch_csr_sketch_grad(int64_t n, int64_t d, const int64_t *row_ptr, const int32_t *col,
                                    const double *val, int64_t row_offset, uint64_t key, int64_t m, int s,
-                                   double *SA_unscaled, const double *bvec, const double *x, double *g,
+                                   double scale, double *SA, const double *bvec, const double *x, double *g,
                                    cudaStream_t st, LaunchCounter lc) {
   if (n <= 0) return cudaSuccess;
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   const uint32_t M = (uint32_t)(m / s);
-  const bool sk = SA_unscaled != nullptr, gr = g != nullptr;
-  if (sk && gr) launch_t<true, true>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, SA_unscaled, bvec, x, g, st);
-  else if (sk) launch_t<true, false>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, SA_unscaled, bvec, x, g, st);
-  else if (gr) launch_t<false, true>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, SA_unscaled, bvec, x, g, st);
+  const bool sk = SA != nullptr, gr = g != nullptr;
+  if (sk && gr) launch_t<true, true>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, scale, SA, bvec, x, g, st);
+  else if (sk) launch_t<true, false>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, scale, SA, bvec, x, g, st);
+  else if (gr) launch_t<false, true>(grid, n, (int)d, row_ptr, col, val, row_offset, key, M, s, scale, SA, bvec, x, g, st);
   lc.add();
   return cudaGetLastError();
 }

@@ -108,10 +108,10 @@ cudaError_t launch_nvls_allreduce(double *mc, uint32_t *const *pads, int rank, i
                                   cudaStream_t st, LaunchCounter lc);
 
 // ---- CSR sketch and gradient (atomics into L2) ------------------------------
-// SA must be zeroed first when sketching.  g must be zeroed when gradient.
+// SA must be zeroed first when sketching (it receives scale * S A).  g must be zeroed when gradient.
 cudaError_t launch_csr_sketch_grad(int64_t n, int64_t d, const int64_t *row_ptr, const int32_t *col,
                                    const double *val, int64_t row_offset, uint64_t key, int64_t m, int s,
-                                   double *SA_unscaled, const double *bvec, const double *x, double *g,
+                                   double scale, double *SA, const double *bvec, const double *x, double *g,
                                    cudaStream_t st, LaunchCounter lc);
 cudaError_t launch_scale(double *buf, int64_t count, double scale, cudaStream_t st, LaunchCounter lc);
 

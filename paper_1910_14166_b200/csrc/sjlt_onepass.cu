@@ -96,7 +96,7 @@ __device__ __forceinline__ void lds_f64x2(uint32_t a, double &x, double &y) {
 // ---------------------------------------------------------------------------
 // Lists (a1): one CTA per chunk of kR local rows, warp j sorts the chunk by the
 // bucket of block j (the counter hash of reading R1, global row ids).  Pass 1
-// hashes each row once (codes kept in registers, two per word) and counts per bucket;
+// hashes each row once (codes kept in shared memory) and counts per bucket;
 // the warp scans its M counts; pass 2 places rows 32 at a time in ascending
 // order (rank among equal buckets from ballots), so each bucket's entries
 // ascend.  Out: the chunk's list block.  (Placement by shared-memory atomics
@@ -107,35 +107,24 @@ __global__ void __launch_bounds__(32 * kSMax) sjlt_lists_kernel(int64_t n, uint6
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int moff = moff_of((int)M);
   const int lbe = list_block_elems((int)s, (int)M);
-  uint16_t *blk = reinterpret_cast<uint16_t *>(smem_raw);          // [s][moff + kR]
-  int32_t *cnt = reinterpret_cast<int32_t *>(blk + lbe);           // [s][M]
+  uint16_t *blk = reinterpret_cast<uint16_t *>(smem_raw);              // [s][moff + kR]
+  uint16_t *code = blk + lbe;                                          // [s][kR]: bucket | neg << 15
+  int32_t *cnt = reinterpret_cast<int32_t *>(code + (size_t)s * kR);  // [s][M]
   const int lane = threadIdx.x & 31, j = threadIdx.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * kR;
   const int valid = (int)min((int64_t)kR, n - r0);
   if (j < (int)s) {
     uint16_t *off = blk + (size_t)j * (moff + kR);
     uint16_t *ent = off + moff;
+    uint16_t *cd = code + (size_t)j * kR;
     int32_t *ct = cnt + (size_t)j * M;
     for (uint32_t b = lane; b < M; b += 32) ct[b] = 0;
     __syncwarp();
-    // the bucket codes of this lane's rows (lane + 32 k) stay in registers,
-    // two per word (bucket | neg << 15), for the placement pass
-    constexpr int KR = kR / 32;
-    uint32_t cpk[KR / 2];
-#pragma unroll
-    for (int k = 0; k < KR; ++k) {
-      const int r = k * 32 + lane;
-      uint32_t cd = 0xffffu;  // invalid rows
-      if (r < valid) {
-        bool neg;
-        const uint32_t b = hash_bucket(key, (uint64_t)(row_offset + r0 + r), (uint32_t)j, s, M, neg) - (uint32_t)j * M;
-        cd = b | (neg ? 0x8000u : 0u);
-        atomicAdd(&ct[b], 1);
-      }
-      if (k & 1)
-        cpk[k / 2] |= cd << 16;
-      else
-        cpk[k / 2] = cd;
+    for (int r = lane; r < valid; r += 32) {
+      bool neg;
+      const uint32_t b = hash_bucket(key, (uint64_t)(row_offset + r0 + r), (uint32_t)j, s, M, neg) - (uint32_t)j * M;
+      cd[r] = (uint16_t)(b | (neg ? 0x8000u : 0u));
+      atomicAdd(&ct[b], 1);
     }
     __syncwarp();
     int carry = 0;  // exclusive scan of ct -> off (u16) and the running bases (in ct)
@@ -158,13 +147,11 @@ __global__ void __launch_bounds__(32 * kSMax) sjlt_lists_kernel(int64_t n, uint6
     if (lane == 0) off[M] = (uint16_t)carry;
     for (int b = (int)M + 1 + lane; b < moff; b += 32) off[b] = 0;
     __syncwarp();
-#pragma unroll
-    for (int k = 0; k < KR; ++k) {  // stable placement, 32 rows at a time
-      if (k * 32 >= valid) break;
-      const int r = k * 32 + lane;
+    for (int rb = 0; rb < valid; rb += 32) {  // stable placement, 32 rows at a time
+      const int r = rb + lane;
       const bool v = r < valid;
-      const uint32_t c = (k & 1) ? (cpk[k / 2] >> 16) : (cpk[k / 2] & 0xffffu);
-      const uint32_t b = v ? (c & 0x7fffu) : 0u;
+      const uint32_t c = v ? cd[r] : 0u;
+      const uint32_t b = c & 0x7fffu;
       const unsigned peers = peers_by_ballot(b, nbits, v);
       const int rank = __popc(peers & lanemask_lt());
       int base = 0;

@@ -46,7 +46,7 @@ if has full; then
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:cs_gather_tma -s 3 -c 1 \
     -o $OUT/full_C2 -f $B1 --config C2 > $OUT/ncu_full_C2.log 2>&1
   $B1 --config C3 > $OUT/plain1_C3.log 2>&1 &&
-  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"csr_sketch|gram_streamk_kernel|ols_large" -s 6 -c 3 \
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"csr_sketch|gram_streamk|ols_large" -s 6 -c 3 \
     -o $OUT/full_C3 -f $B1 --config C3 > $OUT/ncu_full_C3.log 2>&1
   $B1 --config C4 > $OUT/plain1_C4.log 2>&1 &&
   timeout 900 $NCU --set full --clock-control none --import-source on -k regex:"pg_warp" -s 6 -c 1 \
