@@ -495,6 +495,24 @@ def test_solve_with_host_buffers(P, oracle_mod):
     assert oracle_mod.pred_rel_err(out["x"].numpy(), xo[-1], A.numpy()) <= 1e-9
 
 
+def test_solve_csr_with_host_buffers(P, oracle_mod):
+    """e2e path for CSR: host row_ptr / cols / values and b, copied inside the
+    call; iterates against the oracle (R8), and the solve's look-ahead Gram
+    schedule (d > 256) runs on the staged copies."""
+    cfg = synthetic.CONFIGS["C3"].scaled(1 << 16)
+    prob = synthetic.problem(cfg, "cpu")
+    rp, cl, vl = (t.pin_memory() for t in prob["csr"])
+    b = prob["b"].pin_memory()
+    T = 4
+    out = P.ihs_solve_ols(P.Csr(rp, cl, vl, cfg.d), b, P.Spec(m=cfg.m, s=cfg.s), T)
+    assert out["x"].device.type == "cpu"
+    csr = (rp.numpy(), cl.numpy(), vl.numpy())
+    xo, _ = oracle_mod.ihs_solve(b=b.numpy(), csr=csr, d=cfg.d, m=cfg.m, s=cfg.s, T=T)
+    xg = out["x_hist"].numpy()
+    par = max(oracle_mod.pred_rel_err(a, c, csr=csr, d=cfg.d) for a, c in zip(xg[1:], xo[1:]))
+    assert par <= 1e-9
+
+
 def test_pred_err2(P, oracle_mod):
     rng = np.random.default_rng(5)
     A = rng.standard_normal((50_000, 128))
