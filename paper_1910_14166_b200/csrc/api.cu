@@ -985,15 +985,19 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
   // CTA (small_step.cu; launch latency dominates the multi-kernel path there)
   const bool small = !lookahead && !la_gram_ols && c->small_step && c->world == 1 && constraint == 0 &&
                      A.layout == IHS_DENSE_ROW_MAJOR && small_step_supported(n, d, m, spec->s);
-  for (int32_t t = 0; small && t < T; ++t) {
+  if (small && !trace && T > 0) {  // all T iterations in one launch (A staged once)
+    Prof pr(c, IHS_K_CHOL);
+    IHS_CUDA(launch_small_step(A.values, n, d, b, xh, spec->seed, iter0, T, A.row_offset, m, spec->s,
+                               spec_scale(spec), xh + d, nullptr, nullptr, nullptr, c->d_status, st, lc_of(c)));
+  }
+  for (int32_t t = 0; small && trace && t < T; ++t) {  // trace: one launch per iteration, timed
     const double *x = xh + (int64_t)t * d;
     double *xn = xh + (int64_t)(t + 1) * d;
-    if (trace) cudaEventRecord(ev[0], st);
+    cudaEventRecord(ev[0], st);
     {
       Prof pr(c, IHS_K_CHOL);
-      IHS_CUDA(launch_small_step(A.values, n, d, b, x, iter_key(spec->seed, iter0 + (uint64_t)t), A.row_offset, m,
-                                 spec->s, spec_scale(spec), xn, nullptr, nullptr, nullptr, c->d_status, st,
-                                 lc_of(c)));
+      IHS_CUDA(launch_small_step(A.values, n, d, b, x, spec->seed, iter0 + (uint64_t)t, 1, A.row_offset, m, spec->s,
+                                 spec_scale(spec), xn, nullptr, nullptr, nullptr, c->d_status, st, lc_of(c)));
     }
     if (trace) {
       cudaEventRecord(ev[1], st);
@@ -1362,9 +1366,8 @@ ihs_status ihs_small_step(ihs_ctx c, const ihs_matrix *A, const double *b, const
     return IHS_ERR_UNSUPPORTED;
   DevGuard g(c->device);
   Prof pr(c, IHS_K_CHOL);
-  IHS_CUDA(launch_small_step(A->values, A->n_rows, A->n_cols, b, x, iter_key(spec->seed, iter), A->row_offset,
-                             spec->m, spec->s, spec_scale(spec), xn, SA_out, g_out, H_out, c->d_status, c->stream,
-                             lc_of(c)));
+  IHS_CUDA(launch_small_step(A->values, A->n_rows, A->n_cols, b, x, spec->seed, iter, 1, A->row_offset, spec->m,
+                             spec->s, spec_scale(spec), xn, SA_out, g_out, H_out, c->d_status, c->stream, lc_of(c)));
   return IHS_OK;
 }
 

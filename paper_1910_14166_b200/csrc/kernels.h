@@ -198,11 +198,14 @@ cudaError_t launch_l1ball_update(const double *H, const double *g, int64_t d, co
 // ---- a1-a6 in one launch for small dense OLS problems (small_step.cu) --------
 size_t small_step_smem(int64_t n, int64_t d, int64_t m, int s);
 bool small_step_supported(int64_t n, int64_t d, int64_t m, int s);
-// x_next = x + H^{-1} g for H = (S A)^T S A, g = A^T (b - A x), S from key;
-// SA_out / g_out / H_out (optional) receive the intermediates.
-cudaError_t launch_small_step(const double *A, int64_t n, int64_t d, const double *b, const double *x, uint64_t key,
-                              int64_t row_offset, int64_t m, int s, double scale, double *x_next, double *SA_out,
-                              double *g_out, double *H_out, int *status, cudaStream_t st, LaunchCounter lc);
+// T iterations in one launch: x^{t+1} = x^t + H_t^{-1} g_t for H_t = (S_t A)^T S_t A,
+// g_t = A^T (b - A x^t), S_t from the key of iteration iter0 + t; x^0 = x;
+// x^{t+1} written to xout + t d.  SA_out / g_out / H_out (optional) receive
+// the last iteration's intermediates.
+cudaError_t launch_small_step(const double *A, int64_t n, int64_t d, const double *b, const double *x, uint64_t seed,
+                              uint64_t iter0, int T, int64_t row_offset, int64_t m, int s, double scale, double *xout,
+                              double *SA_out, double *g_out, double *H_out, int *status, cudaStream_t st,
+                              LaunchCounter lc);
 
 // ---- a7 error norms ----------------------------------------------------------
 cudaError_t launch_pred_err2(int layout, int64_t n, int64_t d, const double *values, const int64_t *row_ptr,

@@ -55,11 +55,15 @@ __host__ __device__ inline SmallLayout small_layout(int n, int d, int M, int s) 
   return L;
 }
 
+// T iterations in one launch: A is staged once; iteration t uses the key of
+// iteration iter0 + t, starts from x^t (x for t = 0) and writes x^{t+1} to
+// xout + t d.  (One launch per iteration re-staged A from L2 and paid the
+// launch gap each time.)
 __global__ void __launch_bounds__(kThreads) small_step_kernel(const double *__restrict__ A, int n, int d,
                                                               const double *__restrict__ bvec,
-                                                              const double *__restrict__ x, uint64_t key,
-                                                              int64_t row_offset, int s, int M, double scale,
-                                                              double *__restrict__ x_next, double *SA_out,
+                                                              const double *__restrict__ x, uint64_t seed,
+                                                              uint64_t iter0, int T, int64_t row_offset, int s, int M,
+                                                              double scale, double *__restrict__ xout, double *SA_out,
                                                               double *g_out, double *H_out, int *status) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int wsum[kWarps];
@@ -93,6 +97,9 @@ __global__ void __launch_bounds__(kThreads) small_step_kernel(const double *__re
     }
   }
   if (tid < 32) xs[tid] = tid < d ? x[tid] : 0.0;
+  for (int t = 0; t < T; ++t) {
+  const uint64_t key = iter_key(seed, iter0 + (uint64_t)t);
+  double *x_next = xout + (size_t)t * d;
   for (int e = tid; e < s * M * kSortWarps; e += kThreads) cnt[e] = 0;
   __syncthreads();
   // 1. residuals and codes (thread per row); counts per sort warp's row range
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(kThreads) small_step_kernel(const double *__re
   if (SA_out)
     for (int e = tid; e < m * d; e += kThreads) SA_out[e] = SA[e];
   __syncthreads();
-  if (warp != 0) return;
+  if (warp == 0) {
   // 6. Cholesky: lane i holds row i of H (lower part) in registers
   double row[32];
 #pragma unroll
@@ -244,11 +251,10 @@ __global__ void __launch_bounds__(kThreads) small_step_kernel(const double *__re
       for (int k = J + 1; k < 32; ++k) row[k] = fma(-lij, colb[(J & 1) * 32 + k], row[k]);
     }
   }
-  if (__any_sync(0xffffffffu, bad)) {
+  if (__any_sync(0xffffffffu, bad)) {  // x^{t+1} = x^t (the oracle's verdict, R13)
     if (lane < d) x_next[lane] = xs[lane];
     if (lane == 0) set_status(status, 3 /* IHS_ERR_NOT_SPD */);
-    return;
-  }
+  } else {
   // forward L y = g (lane k finishes y_k; lanes below use L[lane][k] = row[k]);
   // the pivot reciprocal is the finishing lane's own
   double y = gl;
@@ -272,7 +278,15 @@ __global__ void __launch_bounds__(kThreads) small_step_kernel(const double *__re
     if (lane == k) u = uk;
     if (lane < k) u = fma(-H[k * 33 + lane], uk, u);
   }
-  if (lane < d) x_next[lane] = xs[lane] + u;
+  if (lane < d) {
+    const double xn = xs[lane] + u;
+    x_next[lane] = xn;
+    xs[lane] = xn;  // x^{t+1}: the next iteration's start
+  }
+  }  // pivots ok
+  }  // warp 0
+  __syncthreads();
+  }  // t
 }
 }  // namespace
 
@@ -285,13 +299,15 @@ bool small_step_supported(int64_t n, int64_t d, int64_t m, int s) {
          m / s <= 32768 && (int64_t)s * n <= 65535 && small_step_smem(n, d, m, s) <= 225 * 1024;
 }
 
-cudaError_t launch_small_step(const double *A, int64_t n, int64_t d, const double *b, const double *x, uint64_t key,
-                              int64_t row_offset, int64_t m, int s, double scale, double *x_next, double *SA_out,
-                              double *g_out, double *H_out, int *status, cudaStream_t st, LaunchCounter lc) {
+cudaError_t launch_small_step(const double *A, int64_t n, int64_t d, const double *b, const double *x, uint64_t seed,
+                              uint64_t iter0, int T, int64_t row_offset, int64_t m, int s, double scale, double *xout,
+                              double *SA_out, double *g_out, double *H_out, int *status, cudaStream_t st,
+                              LaunchCounter lc) {
+  if (T < 1) return cudaSuccess;
   const size_t smem = small_step_smem(n, d, m, s);
   IHS_SMEM_ATTR(small_step_kernel, smem);
-  small_step_kernel<<<1, kThreads, smem, st>>>(A, (int)n, (int)d, b, x, key, row_offset, s, (int)(m / s), scale,
-                                               x_next, SA_out, g_out, H_out, status);
+  small_step_kernel<<<1, kThreads, smem, st>>>(A, (int)n, (int)d, b, x, seed, iter0, T, row_offset, s, (int)(m / s),
+                                               scale, xout, SA_out, g_out, H_out, status);
   lc.add();
   return cudaGetLastError();
 }
