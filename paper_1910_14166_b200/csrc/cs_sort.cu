@@ -259,7 +259,7 @@ CsSortPlan cs_sort_plan(int64_t n, int64_t m) {
   return p;
 }
 
-// perm stores carry an L2 evict_last hint (IHS_SCATTER_KEEP=0: none): a sector
+// perm stores carry an L2 evict_last hint: a sector
 // of perm is written by ~2 CTAs in 4-byte pieces; kept in L2 it is completed
 // there (and read there by the next gather) instead of partially written back
 constexpr int keep_env = 1;
