@@ -286,16 +286,17 @@ __global__ void __launch_bounds__(256) gram_streamk_reduce_kernel(const double *
 // Stream-K with 128 x 128 tiles for large d (d >= 512: C3's 36 upper tiles):
 // half the L2 operand reads of the 64 x 64 tiles (each CTA tile reads 2 x 128
 // columns of SA per k-row for 128 x 128 outputs) -- the look-ahead Gram runs
-// beside the CSR pass, which is bound by its L2 reductions -- and twice the
-// DMMAs per shared-memory fragment load.  8 warps, warp (wm, wn) owns rows
-// [32 wm, +32) x columns [64 wn, +64) as 4 x 8 DMMA 8 x 8 tiles (64 fp64
-// accumulators a thread); one CTA per SM; kStages128 stages of KC128 rows.
+// beside the CSR pass, which is bound by its L2 reductions -- and the same
+// DMMAs per shared-memory fragment load as the 64 tiles.  16 warps,
+// warp (wm, wn) owns rows [32 wm, +32) x columns [32 wn, +32) as 4 x 4 DMMA
+// 8 x 8 tiles (32 fp64 accumulators a thread: no spills, unlike a 32 x 64
+// warp tile at 8 warps); one CTA per SM; kStages2 stages of KC2 rows.
 constexpr int GT2 = 128;
 constexpr int KC2 = 16;
 constexpr int LDS2 = GT2 + 4;  // == 4 mod 16 doubles: conflict-free fragment loads
 constexpr int kStages2 = 3;
 
-__global__ void __launch_bounds__(256, 1) gram_streamk128_kernel(const double *__restrict__ SA, int64_t m, int d,
+__global__ void __launch_bounds__(512, 1) gram_streamk128_kernel(const double *__restrict__ SA, int64_t m, int d,
                                                                  int tiles, int ntri, int kch, int ipc,
                                                                  double *__restrict__ partials,
                                                                  int *__restrict__ slot_tile, int hint) {
@@ -303,22 +304,22 @@ __global__ void __launch_bounds__(256, 1) gram_streamk128_kernel(const double *_
   double *Xp = sm;                          // [kStages2][KC2][LDS2]
   double *Xq = sm + kStages2 * KC2 * LDS2;  // [kStages2][KC2][LDS2]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wm = warp >> 2, wn = warp & 3;  // 16 warps: 4 x 4 of 32 x 32
   const int64_t total = (int64_t)ntri * kch;
   const int64_t i0 = (int64_t)blockIdx.x * ipc, i1 = min(total, i0 + ipc);
   if (tid == 0) slot_tile[2 * blockIdx.x] = slot_tile[2 * blockIdx.x + 1] = -1;
   uint64_t pol = 0;
   if (hint) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  double acc[4][8][2];
+  double acc[4][4][2];
   int cur = -1, slot = 0;
   auto flush = [&]() {
     double *out = partials + ((int64_t)blockIdx.x * 2 + slot) * (GT2 * GT2);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < 4; ++j) {
         const int r = 32 * wm + 8 * i + (lane >> 2);
-        const int c = 64 * wn + 8 * j + 2 * (lane & 3);
+        const int c = 32 * wn + 8 * j + 2 * (lane & 3);
         *reinterpret_cast<double2 *>(out + r * GT2 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
       }
     if (tid == 0) slot_tile[2 * blockIdx.x + slot] = cur;
@@ -332,17 +333,17 @@ __global__ void __launch_bounds__(256, 1) gram_streamk128_kernel(const double *_
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
     int P, Q;
     tri_decode(tile, tiles, P, Q);
     const bool diag = (P == Q);
     const int64_t k0 = m * kc / kch, k1 = m * (kc + 1) / kch;
     auto load_stage = [&](int buf, int64_t kb) {
-      // KC2 x 128 doubles per matrix in 16-byte pieces: 1024 / 256 threads = 4 each
+      // KC2 x 128 doubles per matrix in 16-byte pieces: 1024 / 512 threads = 2 each
 #pragma unroll
-      for (int t2 = 0; t2 < (KC2 * GT2 / 2) / 256; ++t2) {
-        const int e = t2 * 256 + tid;
+      for (int t2 = 0; t2 < (KC2 * GT2 / 2) / 512; ++t2) {
+        const int e = t2 * 512 + tid;
         const int r = e / (GT2 / 2), c = 2 * (e % (GT2 / 2));
         const int64_t row = kb + r;
         const bool rin = row < k1;
@@ -379,18 +380,18 @@ __global__ void __launch_bounds__(256, 1) gram_streamk128_kernel(const double *_
       const int buf = s2 % kStages2;
       const double *xp = Xp + buf * KC2 * LDS2;
       const double *xq = (diag ? Xp : Xq) + buf * KC2 * LDS2;
-#pragma unroll 1
+#pragma unroll
       for (int kk = 0; kk < KC2; kk += 4) {
         const int kr = kk + (lane & 3);
-        double a[4], b[8];
+        double a[4], b[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = xp[kr * LDS2 + 32 * wm + 8 * i + (lane >> 2)];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) b[j] = xq[kr * LDS2 + 64 * wn + 8 * j + (lane >> 2)];
+        for (int j = 0; j < 4; ++j) b[j] = xq[kr * LDS2 + 32 * wn + 8 * j + (lane >> 2)];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int j = 0; j < 8; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
       }
     }
     cp_async_wait<0>();
@@ -502,7 +503,7 @@ cudaError_t launch_gram(const GramPlan &p, const double *SA, double scale, doubl
     const size_t smem2 = (size_t)2 * kStages2 * KC2 * LDS2 * 8;
     IHS_SMEM_ATTR(gram_streamk128_kernel, smem2);
     int *slot_tile = reinterpret_cast<int *>(partials + (size_t)p.ncta * 2 * GT2 * GT2);
-    gram_streamk128_kernel<<<p.ncta, 256, smem2, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kch, p.ipc, partials,
+    gram_streamk128_kernel<<<p.ncta, 512, smem2, st>>>(SA, p.m, (int)p.d, p.tiles, p.ntri, p.kch, p.ipc, partials,
                                                        slot_tile, hint);
     gram_streamk128_reduce_kernel<<<dim3(p.ntri, (GT2 * GT2) / 256), 256, 0, st>>>(
         partials, slot_tile, (int)p.d, p.tiles, p.kch, p.ipc, scale * scale, H);
