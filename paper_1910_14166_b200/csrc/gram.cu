@@ -380,6 +380,9 @@ __global__ void __launch_bounds__(512, 1) gram_streamk128_kernel(const double *_
       const int buf = s2 % kStages2;
       const double *xp = Xp + buf * KC2 * LDS2;
       const double *xq = (diag ? Xp : Xq) + buf * KC2 * LDS2;
+      // a diagonal tile's warps wholly below the diagonal skip their DMMAs
+      // (the reduction reads the upper triangle only)
+      if (!(diag && wm > wn))
 #pragma unroll
       for (int kk = 0; kk < KC2; kk += 4) {
         const int kr = kk + (lane & 3);
