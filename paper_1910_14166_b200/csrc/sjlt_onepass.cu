@@ -172,20 +172,31 @@ __global__ void __launch_bounds__(32 * kSMax) sjlt_lists_kernel(int64_t n, uint6
 }
 
 // a5 riding on the sketch pass: kGradWarps extra warps per CTA stream whole
-// rows of A (row range rows_per_gwarp per warp, coalesced loads that bypass
-// L1) and accumulate g's partial r_i a_i, r_i = b_i - a_i x, in registers --
-// the pass is bound by shared memory, these warps by HBM, so the gradient's
-// own read of A (4.3 ms for C5) hides under the sketch.  One partial row per
-// warp in gpart (reduced in fixed order afterwards; deterministic).
+// rows of A (coalesced loads that bypass L1) and accumulate g's partial
+// r_i a_i, r_i = b_i - a_i x, in registers -- the pass is bound by shared
+// memory, these warps by HBM, so the gradient's own read of A (4.3 ms for C5)
+// hides under the sketch.  The rows follow the sketch: for every chunk w of
+// every item (slice q, group g) the CTA takes, its gradient warps read share q
+// of chunk w's rows (rows w kR + [q kR / nslices, (q+1) kR / nslices)), paced
+// to at most kGradAhead chunks ahead of the CTA's producer.  The nslices CTAs
+// of a group walk its chunks together, so the whole rows the gradient reads
+// are, within the L2 window, the lines the slices' TMA boxes fetch (or the
+// other way round).  ncu at C5 (sketch + gradient launch): DRAM reads 81.9 GB
+// (static row ranges, evict_first boxes) -> 48.6 GB (this; A = 25.8 GB), the
+// launch 22.98 -> 22.93 ms (8 rows per warp step: the warps are latency-bound,
+// 4 rows measured 25.7 ms once paced).  Every row has one fixed warp
+// and position in that warp's order: one partial row per warp in gpart,
+// reduced in fixed order afterwards (deterministic).
 constexpr int kGradWarps = 3;   // 16 consumer + 1 producer + 3 = 20 warps: 5 per SM sub-partition at 96 registers
-constexpr int kGradU = 4;       // rows per warp step
+constexpr int kGradU = 8;       // rows per warp step (loads in flight: the warps are latency-bound)
 constexpr int kGradMaxNV = 4;   // d <= 128 (wider rows: the separate gradient pass)
+constexpr int kGradAhead = 4;   // chunks the gradient may read ahead of the producer's TMA issue
 template <int NV>
 __device__ __forceinline__ void grad_warp(const double *__restrict__ A, int64_t n, int d,
                                           const double *__restrict__ bvec, const double *__restrict__ x,
-                                          double *__restrict__ gpart, int64_t gw, int64_t rpw, int lane) {
+                                          double *__restrict__ gpart, int wk, int nslices, int ngroups,
+                                          int64_t nchunks, const volatile int *issued, int lane) {
   constexpr int U = kGradU;
-  const int64_t r0 = min(n, gw * rpw), r1 = min(n, r0 + rpw);
   int colc[NV];
   double xv[NV], gacc[NV];
 #pragma unroll
@@ -195,33 +206,47 @@ __device__ __forceinline__ void grad_warp(const double *__restrict__ A, int64_t 
     xv[k] = col < d ? x[col] : 0.0;
     gacc[k] = 0.0;
   }
+  const int nitems = nslices * ngroups;
+  int64_t kc = 0;  // the CTA's chunk sequence number (the producer's k)
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int g = it / nslices, q = it % nslices;
+    const int64_t w0 = nchunks * g / ngroups, w1 = nchunks * (g + 1) / ngroups;
+    for (int64_t w = w0; w < w1; ++w, ++kc) {
+      if (lane == 0)
+        while ((int64_t)*issued < kc - kGradAhead) __nanosleep(200);
+      __syncwarp();
+      const int64_t r0 = min(n, w * kR + (int64_t)q * kR / nslices);
+      const int64_t r1 = min(n, w * kR + (int64_t)(q + 1) * kR / nslices);
 #pragma unroll 1
-  for (int64_t base = r0; base < r1; base += U) {
-    double v[U][NV];
+      for (int64_t base = r0 + (int64_t)wk * U; base < r1; base += (int64_t)kGradWarps * U) {
+        double v[U][NV];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t row = (base + u < r1) ? base + u : r1 - 1;  // clamped rows carry r = 0
-      const double *rowp = A + row * d;
+        for (int u = 0; u < U; ++u) {
+          const int64_t row = (base + u < r1) ? base + u : r1 - 1;  // clamped rows carry r = 0
+          const double *rowp = A + row * d;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) v[u][k] = ldg_stream(rowp + colc[k]);
-    }
-    double p[U];
+          for (int k = 0; k < NV; ++k) v[u][k] = ldg_stream(rowp + colc[k]);
+        }
+        double p[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      p[u] = 0.0;
+        for (int u = 0; u < U; ++u) {
+          p[u] = 0.0;
 #pragma unroll
-      for (int k = 0; k < NV; ++k) p[u] = fma(v[u][k], xv[k], p[u]);
-    }
-    transpose_reduce<U>(p, lane);
-    const int myu = reduced_row_of_lane<U>(lane);
-    const double res = (base + myu < r1) ? bvec[base + myu] - p[0] : 0.0;
+          for (int k = 0; k < NV; ++k) p[u] = fma(v[u][k], xv[k], p[u]);
+        }
+        transpose_reduce<U>(p, lane);
+        const int myu = reduced_row_of_lane<U>(lane);
+        const double res = (base + myu < r1) ? bvec[base + myu] - p[0] : 0.0;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const double ru = __shfl_sync(0xffffffffu, res, owner_lane_of_row<U>(u));
+        for (int u = 0; u < U; ++u) {
+          const double ru = __shfl_sync(0xffffffffu, res, owner_lane_of_row<U>(u));
 #pragma unroll
-      for (int k = 0; k < NV; ++k) gacc[k] = fma(ru, v[u][k], gacc[k]);
+          for (int k = 0; k < NV; ++k) gacc[k] = fma(ru, v[u][k], gacc[k]);
+        }
+      }
     }
   }
+  const int64_t gw = (int64_t)blockIdx.x * kGradWarps + wk;
 #pragma unroll
   for (int k = 0; k < NV; ++k)
     if (lane + 32 * k < d) gpart[gw * d + lane + 32 * k] = gacc[k];
@@ -241,7 +266,7 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
     const __grid_constant__ CUtensorMap tmap, const uint16_t *__restrict__ lists, int64_t n, int d, int M,
     int nslices, int ngroups, int64_t nchunks, double *__restrict__ part, const double *__restrict__ A,
     const double *__restrict__ bvec,
-    const double *__restrict__ x, double *__restrict__ gpart, int64_t rows_per_gwarp) {
+    const double *__restrict__ x, double *__restrict__ gpart) {
   extern __shared__ __align__(1024) unsigned char smem_dyn[];
   // stage buffers 1024-byte aligned (the SWIZZLE_32B pattern is a function of the address)
   unsigned char *smem_raw = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
@@ -253,18 +278,20 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
   unsigned char *lbuf = smem_raw + kStages * kTileBytes;
   uint64_t *full = reinterpret_cast<uint64_t *>(lbuf + kStages * lb_bytes);
   uint64_t *empty = full + kStages;
+  int *issued = reinterpret_cast<int *>(empty + kStages);  // chunks whose TMA the producer has issued, minus 1
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers / 32);
     }
+    *issued = -1;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   if (NV > 0 && warp > kConsumers / 32) {
-    grad_warp<NV ? NV : 1>(A, n, d, bvec, x, gpart, (int64_t)blockIdx.x * kGradWarps + (warp - kConsumers / 32 - 1),
-                  rows_per_gwarp, lane);
+    grad_warp<NV ? NV : 1>(A, n, d, bvec, x, gpart, warp - kConsumers / 32 - 1, nslices, ngroups, nchunks,
+                           issued, lane);
     return;
   }
   const int nitems = nslices * ngroups;
@@ -272,7 +299,11 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
     // ---------------- producer
     if (lane == 0) {
       uint64_t pol;
-      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+      // evict_normal, not evict_first: the neighbouring slices' CTAs (and the
+      // gradient warps) read the rest of every 256-byte line a box promotes,
+      // so the sketch takes A from HBM once (ncu, C5 sketch only: 33.2 GB with
+      // evict_first, 26.5 GB with evict_normal, A = 25.8 GB; same time)
+      asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
       int s = 0;
       uint32_t ph = 0;
@@ -288,6 +319,7 @@ __global__ void __maxnreg__(96) sjlt_onepass_kernel(
           for (int bx = 0; bx < kR / kBoxRows; ++bx)
             tma_box(st + bx * kBoxRows * kC * 8, &tmap, q * kC, (int)(w * kR + bx * kBoxRows), &full[s], pol);
           bulk_g2s(lbuf + (size_t)s * lb_bytes, lists + (size_t)w * lbe, lb_bytes, &full[s]);
+          *reinterpret_cast<volatile int *>(issued) = (int)k;
           if (++s == kStages) {
             s = 0;
             ph ^= 1u;
@@ -373,7 +405,7 @@ EncodeTiledFn encode_fn() {
 }
 
 size_t onepass_smem(int S, int M) {
-  return kStages * ((size_t)kTileBytes + (size_t)list_block_elems(S, M) * 2) + 2 * kStages * 8 + 1024;
+  return kStages * ((size_t)kTileBytes + (size_t)list_block_elems(S, M) * 2) + 2 * kStages * 8 + 16 + 1024;
 }
 size_t lists_smem(int S, int M) { return (size_t)list_block_elems(S, M) * 2 + (size_t)S * kR * 2 + (size_t)S * M * 4; }
 }  // namespace
@@ -431,19 +463,13 @@ cudaError_t launch_sjlt_onepass(const SjltOnepassPlan &p, const double *A, const
     return cudaErrorInvalidValue;
   const int nv = gpart ? (int)((p.d + 31) / 32) : 0;
   if (nv > kGradMaxNV) return cudaErrorInvalidValue;
-  int64_t rpw = 0;
-  if (nv) {
-    const int64_t warps = (int64_t)p.grid * kGradWarps;
-    rpw = (p.n + warps - 1) / warps;
-    rpw = (rpw + kGradU - 1) / kGradU * kGradU;
-  }
   const unsigned threads = kConsumers + 32 + (nv ? 32 * kGradWarps : 0);
 #define IHS_ONEPASS_NV(SV, NVV)                                                                                \
   case NVV:                                                                                                    \
     IHS_SMEM_ATTR((sjlt_onepass_kernel<SV, NVV>), p.smem);                                                     \
     sjlt_onepass_kernel<SV, NVV><<<p.grid, threads, p.smem, st>>>(tm, lists, p.n, (int)p.d, (int)p.M, p.nslices, \
                                                                   p.ngroups, p.nchunks, partials, A, bvec, x,  \
-                                                                  gpart, rpw);                                  \
+                                                                  gpart);                                        \
     break;
 #define IHS_ONEPASS(SV)        \
   case SV:                     \
