@@ -62,6 +62,22 @@ __device__ __forceinline__ unsigned peers_by_ballot(uint32_t key, int nbits, boo
   return peers;
 }
 
+// peers_by_ballot with the key width fixed at compile time: the ballots
+// unroll into VOTE + select pairs with no per-bit loop or divergence checks
+// (sjlt_lists_kernel's placement pass, M = 512: NB = 9).
+template <int NB>
+__device__ __forceinline__ unsigned peers_by_ballot_c(uint32_t key, bool valid) {
+  const unsigned vm = __ballot_sync(0xffffffffu, valid);
+  unsigned peers = valid ? vm : ~vm;
+#pragma unroll
+  for (int k = 0; k < NB; ++k) {
+    const bool bit = ((key >> k) & 1u) != 0;
+    const unsigned bk = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bk : ~bk;
+  }
+  return peers;
+}
+
 // Transpose-reduce U per-lane partial sums (one per row) across the warp in
 // U-1 + log2(32/U) shuffles instead of U*5.  On return p[0] holds the full sum
 // for row reduced_row_of_lane<U>(lane).

@@ -100,7 +100,10 @@ __device__ __forceinline__ void lds_f64x2(uint32_t a, double &x, double &y) {
 // the warp scans its M counts; pass 2 places rows 32 at a time in ascending
 // order (rank among equal buckets from ballots), so each bucket's entries
 // ascend.  Out: the chunk's list block.  (Placement by shared-memory atomics
-// plus a per-list sort measured slower: 2.3 vs 1.8 ms for C5.)
+// plus a per-list sort measured slower: 2.3 vs 1.8 ms for C5; the ballots at
+// compile-time key width: 1.84 -> 1.64 ms; two warps per block, each sorting
+// half the rows: 1.64, dropped.)
+template <int NB>  // key bits (NB = 0: nbits at run time)
 __global__ void __launch_bounds__(32 * kSMax) sjlt_lists_kernel(int64_t n, uint64_t key, int64_t row_offset,
                                                                uint32_t s, uint32_t M, int nbits,
                                                                uint16_t *__restrict__ lists) {
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(32 * kSMax) sjlt_lists_kernel(int64_t n, uint6
       const bool v = r < valid;
       const uint32_t c = v ? cd[r] : 0u;
       const uint32_t b = c & 0x7fffu;
-      const unsigned peers = peers_by_ballot(b, nbits, v);
+      const unsigned peers = NB > 0 ? peers_by_ballot_c<NB>(b, v) : peers_by_ballot(b, nbits, v);
       const int rank = __popc(peers & lanemask_lt());
       int base = 0;
       if (v) base = ct[b];
@@ -437,10 +440,20 @@ bool sjlt_onepass_plan(int64_t n, int64_t d, int64_t m, int s, int num_sms, cons
 cudaError_t launch_sjlt_lists(const SjltOnepassPlan &p, uint64_t key, int64_t row_offset, uint16_t *lists,
                               cudaStream_t st, LaunchCounter lc) {
   const size_t smem = lists_smem(p.s, (int)p.M);
-  IHS_SMEM_ATTR(sjlt_lists_kernel, smem);
   const int nbits = p.M > 1 ? 32 - __builtin_clz((unsigned)(p.M - 1)) : 1;
-  sjlt_lists_kernel<<<(unsigned)p.nchunks, 32 * p.s, smem, st>>>(p.n, key, row_offset, (uint32_t)p.s, (uint32_t)p.M,
-                                                                  nbits, lists);
+#define IHS_LISTS(NBV)                                                                                        \
+  {                                                                                                           \
+    IHS_SMEM_ATTR(sjlt_lists_kernel<NBV>, smem);                                                              \
+    sjlt_lists_kernel<NBV><<<(unsigned)p.nchunks, 32 * p.s, smem, st>>>(p.n, key, row_offset, (uint32_t)p.s, \
+                                                                        (uint32_t)p.M, nbits, lists);         \
+  }
+  switch (nbits) {
+    case 8: IHS_LISTS(8) break;
+    case 9: IHS_LISTS(9) break;
+    case 10: IHS_LISTS(10) break;
+    default: IHS_LISTS(0) break;
+  }
+#undef IHS_LISTS
   lc.add();
   return cudaGetLastError();
 }
