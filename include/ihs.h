@@ -165,7 +165,13 @@ ihs_status ihs_ctx_profile_reset(ihs_ctx ctx);
 /* Multi-GPU (BASELINE.json north_star: one allreduce of [SA | g] per
  * iteration).  ihs_nccl_unique_id writes NCCL's 128-byte id (call on rank 0,
  * broadcast it); ihs_ctx_set_comm creates this rank's communicator.  NCCL is
- * resolved at run time from the libnccl.so.2 already loaded in the process. */
+ * resolved at run time from the libnccl.so.2 already loaded in the process.
+ * world == 1 with unique_id128 == NULL: no communicator (single-rank
+ * schedules); world == 1 with an id: a one-rank communicator, and the solve
+ * calls take their collective schedules (NCCL all-reduces over one rank --
+ * the multi-rank code path checked on one GPU).  Once per ctx: a second call
+ * on a ctx that holds a communicator is IHS_ERR_INVALID_ARGUMENT;
+ * IHS_ERR_COMM when NCCL cannot be loaded or the init fails. */
 ihs_status ihs_nccl_unique_id(void *out128);
 ihs_status ihs_ctx_set_comm(ihs_ctx ctx, int rank, int world, const void *unique_id128);
 /* In-place sum of count doubles across the ctx communicator (a3). */

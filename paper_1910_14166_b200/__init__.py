@@ -309,6 +309,14 @@ def _f64(n, device):
 
 
 # ------------------------------------------------------------------ a1
+def ihs_allreduce_sum(buf: torch.Tensor, ctx: Context | None = None) -> torch.Tensor:
+    """In-place sum of a float64 device tensor across the context's communicator (a3)."""
+    ctx = ctx or default_context(buf.device)
+    assert buf.dtype == torch.float64 and buf.is_cuda and buf.is_contiguous()
+    _check(lib().ihs_allreduce_sum(ctx._bind(), _p(buf), buf.numel()), "ihs_allreduce_sum")
+    return buf
+
+
 def ihs_allreduce_multimem(mc_ptr: int, pads: torch.Tensor, rank: int, world: int, count: int, pad_slots: int,
                            ctx: Context | None = None) -> None:
     """a3 over NVLS: in-place sum of `count` doubles of a symmetric buffer whose

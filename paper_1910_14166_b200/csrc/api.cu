@@ -159,6 +159,11 @@ ihs_status from_cuda(cudaError_t e) {
 void join_side(ihs_ctx c);
 void join_factor(ihs_ctx c);
 
+// The collective schedules run whenever the ctx holds a communicator -- also a
+// one-rank one (ihs_ctx_set_comm(c, 0, 1, uid)), whose all-reduces are NCCL
+// calls over one rank: the multi-rank plumbing exercised on one GPU.
+inline bool distributed(const ihs_ctx_s *c) { return c->world > 1 || c->comm != nullptr; }
+
 template <typename T>
 ihs_status scratch(ihs_ctx c, Slot s, size_t bytes, T **out) {
   bytes = std::max<size_t>(bytes, 256);
@@ -768,7 +773,7 @@ ihs_status ols_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_s
   IHS_TRY(scratch(c, S_PACK, (size_t)2 * pk * 8, &packs));
   IHS_TRY(scratch(c, S_H, (size_t)2 * d * d * 8, &Hinv));
   auto allreduce = [&](double *buf, int64_t cnt) -> ihs_status {
-    if (c->world > 1) {
+    if (distributed(c)) {
       if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
       if (g_nccl.AllReduce(buf, buf, (size_t)cnt, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
         return IHS_ERR_COMM;
@@ -784,7 +789,7 @@ ihs_status ols_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_s
     double *SAn = packs + nxt * pk, *gn = SAn + m * d;
     const double *x = xh + (int64_t)t * d;
     double *xn = xh + (int64_t)(t + 1) * d;
-    if (c->world == 1) {  // factor, gradient reduction and update inside the pass
+    if (!distributed(c)) {  // factor, gradient reduction and update inside the pass
       const LookStep ls{Hinv + cur * d * d, x, xn, more ? Hinv + nxt * d * d : nullptr};
       IHS_TRY(sketch_grad_impl(c, A, spec, iter0 + (uint64_t)t + 1, b, x, more ? SAn : nullptr, gn, &ls));
       continue;
@@ -809,7 +814,7 @@ ihs_status pg_lookahead_loop(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_sp
   IHS_TRY(scratch(c, S_PACK, (size_t)2 * pk * 8, &packs));
   IHS_TRY(scratch(c, S_H, (size_t)2 * d * d * 8, &H));
   auto allreduce = [&](double *buf, int64_t cnt) -> ihs_status {
-    if (c->world > 1) {
+    if (distributed(c)) {
       if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
       if (g_nccl.AllReduce(buf, buf, (size_t)cnt, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0)
         return IHS_ERR_COMM;
@@ -865,7 +870,7 @@ bool use_lookahead_pg(ihs_ctx c, const ihs_matrix *A, int64_t rows, const ihs_sk
 
 // a3: in-place sum over the ctx communicator (no-op on one rank).
 ihs_status allreduce_impl(ihs_ctx c, double *buf, int64_t count) {
-  if (c->world <= 1 || count == 0) return IHS_OK;
+  if (!distributed(c) || count == 0) return IHS_OK;
   if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
   if (g_nccl.AllReduce(buf, buf, (size_t)count, kNcclFloat64, kNcclSum, c->comm, c->stream) != 0) return IHS_ERR_COMM;
   return IHS_OK;
@@ -887,7 +892,7 @@ bool use_lookahead_gram_ols(ihs_ctx c, const ihs_matrix *A, const ihs_sketch_spe
 // ranks between two schedules with different collectives).
 ihs_status rows_for_schedule(ihs_ctx c, int64_t n_local, int64_t *rows) {
   *rows = n_local;
-  if (c->world <= 1) return IHS_OK;
+  if (!distributed(c)) return IHS_OK;
   if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
   double *buf;
   IHS_TRY(scratch(c, S_ROWS, 8, &buf));
@@ -983,7 +988,7 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
     IHS_TRY(pg_lookahead_loop(c, &A, spec, b, iter0, T, xh, radius, cfg, inner_dev, constraint == 2 ? 1 : 0));
   // a small dense OLS problem on one rank: each iteration is one launch of one
   // CTA (small_step.cu; launch latency dominates the multi-kernel path there)
-  const bool small = !lookahead && !la_gram_ols && c->small_step && c->world == 1 && constraint == 0 &&
+  const bool small = !lookahead && !la_gram_ols && c->small_step && !distributed(c) && constraint == 0 &&
                      A.layout == IHS_DENSE_ROW_MAJOR && small_step_supported(n, d, m, spec->s);
   if (small && !trace && T > 0) {  // all T iterations in one launch (A staged once)
     Prof pr(c, IHS_K_CHOL);
@@ -1023,7 +1028,7 @@ ihs_status solve_impl(ihs_ctx c, int constraint, const ihs_matrix *A_in, const d
     if (trace) cudaEventRecord(ev[0], st);
     IHS_TRY(sketch_grad_impl(c, &A, spec, iter0 + (uint64_t)t, b, x, SA, g));
     if (trace) cudaEventRecord(ev[1], st);
-    if (c->world > 1) {
+    if (distributed(c)) {
       if (!c->comm || !load_nccl()) return IHS_ERR_COMM;
       if (g_nccl.AllReduce(pack, pack, (size_t)(m * d + d), kNcclFloat64, kNcclSum, c->comm, st) != 0)
         return IHS_ERR_COMM;
@@ -1268,10 +1273,10 @@ ihs_status ihs_nccl_unique_id(void *out128) {
 }
 
 ihs_status ihs_ctx_set_comm(ihs_ctx c, int rank, int world, const void *uid) {
-  if (!c || world < 1 || rank < 0 || rank >= world) return IHS_ERR_INVALID_ARGUMENT;
+  if (!c || world < 1 || rank < 0 || rank >= world || c->comm) return IHS_ERR_INVALID_ARGUMENT;
   c->rank = rank;
   c->world = world;
-  if (world == 1) return IHS_OK;
+  if (world == 1 && !uid) return IHS_OK;  // no communicator: the single-rank schedules
   if (!uid) return IHS_ERR_INVALID_ARGUMENT;
   if (!load_nccl()) return IHS_ERR_COMM;
   DevGuard g(c->device);

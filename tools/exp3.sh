@@ -1,2 +1,2 @@
-python -m pytest tests/test_gpu_parity.py -q -x -k "sjlt" 2>&1 | tail -2
-timeout 300 python tools/sjlt_probe.py 25 onepass 2>&1 | grep -v Warn
+timeout 900 python -m pytest tests/test_gpu_comm_one_rank.py -q -x -p no:cacheprovider 2>&1 | tail -15
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "solve or lookahead or reduce" 2>&1 | tail -3
