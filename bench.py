@@ -582,6 +582,13 @@ def main():
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ttt["ms"] = float(tt.item())
             ttt["bitwise_same_as_first_run"] = bool(torch.equal(xh2[tstar], xh[tstar]))
+            if cfg.constraint != "ols":
+                # the PG step bound L comes from a power iteration warm-started from the
+                # context's previous update (ihs_inner_cfg.warm_power_iters, "pg_warm"): the
+                # second run starts from the first run's vector, so its iterates agree to
+                # rounding (same minimiser), not bitwise; "pg_warm" 0 makes them bitwise
+                ttt["rel_diff_vs_first_run"] = float(
+                    (xh2[tstar] - xh[tstar]).norm() / xh[tstar].norm().clamp_min(1e-300))
             del x0
         del xh
     # ---- e2e: the public solve call with HOST (pinned) buffers, copies inside
