@@ -46,6 +46,11 @@ def parse():
     ap.add_argument("--allreduce", default="nccl", choices=["nccl", "nvls"],
                     help="N > 1: the [SA | g] exchange through NCCL (default) or the library's NVLS multimem kernel")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--lookahead", type=int, default=-1, choices=[-1, 0, 1],
+                    help="force the look-ahead schedule off / on (default: the library's rule)")
+    ap.add_argument("--step-sync-flush", action="store_true",
+                    help="L2-flushed configs: time each step alone between a flush and a sync (side-stream work "
+                         "that outlives the step's update is then NOT timed) instead of K consecutive steps")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: host-staged all-reduce, for testing the "
                          "sharded path with IHS_BENCH_SHARE_GPU=1 on one GPU)")
@@ -66,7 +71,7 @@ def config_obj(cfg, world, extra=None):
          "parallelism": f"row-shard x{world} + allreduce[SA|g]" if world > 1 else "single GPU",
          "l2": ("inputs larger than L2 (A = %.2f GiB per step)" % (cfg.a_bytes / 2**30))
          if (cfg.a_bytes >= 2 * (126 << 20) and cfg.layout != "csr")
-         else ("L2 flushed between steps (512 MiB write outside the timed events; A = %.1f MiB)"
+         else ("L2 flushed before every step (512 MiB write; A = %.1f MiB)"
                % (cfg.a_bytes / 2**20))}
     if extra:
         o.update(extra)
@@ -443,7 +448,8 @@ def main():
     if world > 1 and args.allreduce == "nvls":
         from paper_1910_14166_b200.dist import NvlsAllreduce
         exch = NvlsAllreduce(cfg.m * cfg.d + cfg.d, dev, ctx=ctx)
-    S = ShardedIHS(Am, b, spec, ops=CudaOps(ctx), constraint=cfg.constraint, radius=radius, allreduce=exch)
+    S = ShardedIHS(Am, b, spec, ops=CudaOps(ctx), constraint=cfg.constraint, radius=radius, allreduce=exch,
+                   lookahead=None if args.lookahead < 0 else bool(args.lookahead))
     d = cfg.d
     xa = torch.zeros(d, dtype=torch.float64, device=dev)
     xb = torch.empty_like(xa)
@@ -462,6 +468,7 @@ def main():
     flush = cfg.layout == "csr" or cfg.a_bytes < 2 * (126 << 20)
     fbuf = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
     t = 0
+    flush_info = None
     for _ in range(max(args.warmup, 3) if args.warmup >= 0 else 3):
         S.step(t, xa, xb)
         xa, xb = xb, xa
@@ -496,7 +503,7 @@ def main():
         ms_local = statistics.median(reps)
         xa.copy_(xo_dev)
         t += args.steps
-    elif flush:
+    elif flush and args.step_sync_flush:
         ms_local = 0.0
         for _ in range(args.steps):
             fbuf.zero_()
@@ -507,6 +514,29 @@ def main():
             ms_local += e0.elapsed_time(e1)
             xa, xb = xb, xa
             t += 1
+    elif flush:
+        # K consecutive steps with the L2 flush INSIDE the timed region (stream-ordered
+        # between steps), so work a step leaves on the side streams (the look-ahead Gram)
+        # is timed too; the flush's own time (measured alone) is subtracted afterwards
+        fl = []
+        for _ in range(5):
+            e0.record(stream)
+            fbuf.zero_()
+            e1.record(stream)
+            e1.synchronize()
+            fl.append(e0.elapsed_time(e1))
+        flush_ms = statistics.median(fl)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fbuf.zero_()
+            S.step(t, xa, xb)
+            xa, xb = xb, xa
+            t += 1
+        e1.record(stream)
+        e1.synchronize()
+        ms_incl_flush = e0.elapsed_time(e1)
+        ms_local = ms_incl_flush - args.steps * flush_ms
+        flush_info = {"flush_ms": flush_ms, "ms_per_step_incl_flush": ms_incl_flush / args.steps}
     else:
         e0.record(stream)
         for _ in range(args.steps):
@@ -559,8 +589,11 @@ def main():
     breakdown = {name: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for name, v in prof.items() if v[1]}
     # ---- time to 1e-10 (IHS solve from x^0 = 0; errors post hoc, outside the timing)
     ttt = None
-    if not args.no_ttt and cfg.layout == "dense":
-        xopt = S.exact_ols() if cfg.constraint == "ols" else S.exact_constrained()
+    if not args.no_ttt and (cfg.layout == "dense" or cfg.constraint == "ols"):
+        if cfg.constraint != "ols":
+            xopt = S.exact_constrained()
+        else:  # CSR: no dense Gram of A; CG on the normal equations through the gradient kernel
+            xopt = S.exact_ols() if cfg.layout == "dense" else S.exact_ols_normal_cg()
         Tmax = 60 if cfg.constraint == "ols" else 40
         xh = S.solve(Tmax, iter0=1000)
         err = S.pred_errors(xh, xopt).cpu().tolist()
@@ -647,8 +680,11 @@ def main():
                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
                "timing": ("median of 5 public ihs_solve_ols calls of K iterations each (device events around the "
                           "call, L2 flushed before it)") if solve_mode else
-                         ("K steps, device events per step, L2 flushed between steps" if flush else
-                          "K consecutive steps between two device events"),
+                         ("K steps, device events per step (flush, step, sync), L2 flushed between steps"
+                          if flush and args.step_sync_flush else
+                          "K consecutive steps between two device events with an L2 flush (512 MiB write) before "
+                          "every step INSIDE the region; K x the flush's own time (measured alone) subtracted"
+                          if flush else "K consecutive steps between two device events"),
                "config": config_obj(cfg, world, {"per_gpu_rows": n_loc, "schedule": (
                    "one-launch small step per iteration (small_step.cu)" if solve_mode else
                    ("look-ahead Gram (H_{t+1} after the CG update of t, beside the next pass; DESIGN.md section 9)"
@@ -661,6 +697,8 @@ def main():
                "roofline": roof, "breakdown_ms": breakdown, "time_to_1e-10": ttt, "e2e": e2e,
                "cpu_baseline": cpu, "gpu_launches": launches, "clocks": clk,
                "gpu": torch.cuda.get_device_name(dev)}
+        if flush_info:
+            out["l2_flush"] = flush_info
         if world > 1:
             out["ranks_bitwise_identical_x"] = ranks_same
             out["dist_backend"] = args.dist_backend

@@ -276,6 +276,40 @@ class ShardedIHS:
         self.ops.ols(G, c, x, x2)
         return x2
 
+    def exact_ols_normal_cg(self, max_iters: int = 200, tol: float = 1e-15, restarts: int = 2) -> torch.Tensor:
+        """x_OPT of Eq. (1) with C = R^d when A^T A cannot be formed by the dense Gram kernel
+        (CSR A): conjugate gradients on the normal equations A^T A x = A^T b with the a5
+        kernel as the operator (A^T A p = -ihs_grad(A, b = 0, x = p); all-reduced over
+        ranks), restarted from the true residual A^T(b - A x).  Bench / test bookkeeping
+        (the reference point of the time-to-1e-10 run), not a step of the hot path: only
+        the d-vector recurrences run in torch."""
+        d, dev = self.d, self.b.device
+        zb = torch.zeros_like(self.b)
+        x = torch.zeros(d, dtype=torch.float64, device=dev)
+        r = torch.empty(d, dtype=torch.float64, device=dev)
+        Ap = torch.empty(d, dtype=torch.float64, device=dev)
+        r0n = None
+        for _ in range(restarts):
+            self.ops.grad(self.A, self.b, x, r)
+            self.allreduce(r)
+            rs = torch.dot(r, r)
+            if r0n is None:
+                r0n = torch.sqrt(rs)
+            p = r.clone()
+            for _k in range(max_iters):
+                if float(torch.sqrt(rs)) <= tol * float(r0n):
+                    break
+                self.ops.grad(self.A, zb, p, Ap)
+                self.allreduce(Ap)
+                Ap.neg_()
+                alpha = rs / torch.dot(p, Ap)
+                x.add_(p, alpha=float(alpha))
+                r.sub_(Ap, alpha=float(alpha))
+                rs_new = torch.dot(r, r)
+                p.mul_(float(rs_new / rs)).add_(r)
+                rs = rs_new
+        return x
+
     def exact_constrained(self, refine: int = 4) -> torch.Tensor:
         """x_OPT of the l1 ball (constraint "l1ball", radius tau) or the penalised
         LASSO ("lasso", radius = lambda) for dense A, the reference of the
