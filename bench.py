@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--lookahead", type=int, default=-1, choices=[-1, 0, 1],
                     help="force the look-ahead schedule off / on (default: the library's rule)")
+    ap.add_argument("--la-gram-sms", type=int, default=-1,
+                    help="SMs of the wide look-ahead Gram (ctx option la_gram_sms; default: the library's rule)")
+    ap.add_argument("--la-gram-tile", type=int, default=-1, help="ctx option la_gram_tile (64 or 128)")
     ap.add_argument("--step-sync-flush", action="store_true",
                     help="L2-flushed configs: time each step alone between a flush and a sync (side-stream work "
                          "that outlives the step's update is then NOT timed) instead of K consecutive steps")
@@ -443,6 +446,10 @@ def main():
         A = None
     del xs
     ctx = P.Context(local)
+    if args.la_gram_sms >= 0:
+        ctx.set_option("la_gram_sms", args.la_gram_sms)
+    if args.la_gram_tile >= 0:
+        ctx.set_option("la_gram_tile", args.la_gram_tile)
     spec = P.Spec(m=cfg.m, s=cfg.s, seed=cfg.hash_seed)
     exch = None
     if world > 1 and args.allreduce == "nvls":
@@ -587,6 +594,25 @@ def main():
     NUM_SMS[0] = torch.cuda.get_device_properties(dev).multi_processor_count
     roof = roofline(prof, cfg, n_loc, n_loc_nnz, args.steps)
     breakdown = {name: {"ms_per_step": v[0] / args.steps, "launches": v[1]} for name, v in prof.items() if v[1]}
+    if roof and roof.get("kernel_group") == "csr" and S.lookahead:
+        # in the look-ahead schedule the pass shares the SMs with the Gram of the next sketch, so its
+        # in-situ launch time is not the kernel's own: time the same call alone (nothing on the side
+        # streams, L2 flushed before each launch) and rate it next to the in-situ figure
+        torch.cuda.synchronize()
+        al = []
+        for k in range(5):
+            fbuf.zero_()
+            e0.record(stream)
+            S.ops.sketch_grad(S.A, S.spec, t + 100 + k, S.b, xa, S.SA, S.g)
+            e1.record(stream)
+            e1.synchronize()
+            al.append(e0.elapsed_time(e1))
+        torch.cuda.synchronize()
+        alone = statistics.median(al)
+        roof["in_situ"] = "beside the look-ahead Gram of the next sketch (shared SMs)"
+        roof["alone"] = {"avg_launch_ms": alone, "achieved": roof["algorithmic_reds_per_launch"] / (alone / 1e3) / 1e9,
+                         "unit": roof["unit"], "frac": roof["algorithmic_reds_per_launch"] / (alone / 1e3) / 1e9
+                         / roof["peak"], "timing": "median of 5 launches alone, L2 flushed before each"}
     # ---- time to 1e-10 (IHS solve from x^0 = 0; errors post hoc, outside the timing)
     ttt = None
     if not args.no_ttt and (cfg.layout == "dense" or cfg.constraint == "ols"):

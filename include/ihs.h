@@ -136,6 +136,11 @@ int64_t ihs_ctx_kernel_launches(ihs_ctx ctx);
  *   "small_step"   1 (default) ihs_solve_ols on one rank runs each iteration of a small dense
  *                  problem (d <= 32, n <= 32768, its working set in one CTA's shared memory)
  *                  as ONE launch of one CTA; 0 the general multi-kernel path
+ *   "la_gram_tile" the look-ahead Gram of d > 256 (ihs_gram_lookahead, the OLS solve with the
+ *                  CG update): 0 / 64 (default) the 64 x 64-tile stream-K, whose two
+ *                  128-thread CTAs per SM leave the pass's CTAs room on the same SMs;
+ *                  128 the 128 x 128-tile stream-K (one 512-thread CTA holds an SM)
+ *   "la_gram_sms"  SMs that Gram takes (0 default: all; >= 64): the rest stay with the pass
  *   "prefetch"     1 (default) the next iteration's sort on the side stream   [IHS_PREFETCH] */
 ihs_status ihs_ctx_set_option(ihs_ctx ctx, const char *name, int64_t value);
 ihs_status ihs_ctx_get_option(ihs_ctx ctx, const char *name, int64_t *value);

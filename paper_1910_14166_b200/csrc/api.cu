@@ -82,6 +82,9 @@ struct ihs_ctx_s {
   int pg_warm = 1;       // warm-started power iteration across l1 / LASSO updates
   int small_step = 1;    // small dense OLS solves: one launch per iteration (small_step.cu)
   int pg_cluster = 0;    // PG cluster size for d <= 256 (0: the smallest that holds H)
+  int la_gram_sms = 0;   // SMs the wide (d > 256) look-ahead Gram takes (0: by the rule in gram_side_impl)
+  int la_gram_tile = 0;  // its CTA tile: 0 / 64 = the 64 x 64 stream-K (two 128-thread CTAs per SM leave the
+                         // pass's CTAs registers to run beside them), 128 = the 128 x 128 stream-K
   // Speculative sort of the NEXT iteration's buckets on a side stream: the
   // hash (hence the sort) depends only on (seed, iteration, row), not on x, so
   // after the gathers of iteration t the sort for t + 1 runs beside the
@@ -625,7 +628,14 @@ ihs_status gram_side_impl(ihs_ctx c, const double *SA, int64_t m, int64_t d, dou
   // cluster; larger d (OLS with the CG update, e.g. C3): a full plan reading
   // SA evict_first, beside the CG solve and the next pass's L2 reductions
   const bool wide = d > 256;
-  GramPlan p = gram_plan(m, d, wide ? c->num_sms : std::min(16, c->num_sms), 2, wide);
+  // A 128-tile Gram CTA holds a whole SM's register file (512 threads x 128 registers), so
+  // no CTA of the pass runs on that SM while it is there: beside the pass the two merely
+  // queue (C3, K consecutive steps: 0.71 ms/step).  The 64-tile stream-K (2 x 128 threads x
+  // 152 registers per SM) leaves the pass room: 0.63; either tile on a share of the SMs
+  // ("la_gram_sms") measured 0.62-0.64 (profiles/r02/c3_lookahead_gram_sweep.json)
+  const int wide_sms = c->la_gram_sms > 0 ? std::min(c->la_gram_sms, c->num_sms) : c->num_sms;
+  GramPlan p = gram_plan(m, d, wide ? std::max(64, wide_sms) : std::min(16, c->num_sms), 2,
+                         wide && c->la_gram_tile == 128);
   double *part;
   IHS_TRY(scratch(c, S_GRAMF, p.partial_bytes(), &part));  // (before factor_begin: a regrowth joins)
   const bool power = pg_supported(d);
@@ -1196,7 +1206,8 @@ const OptionDef kOptions[] = {
     {"lookahead", &ihs_ctx_s::lookahead, -1, 1},   {"sjlt_onepass", &ihs_ctx_s::sjlt_onepass, 0, 2},
     {"ols_large", &ihs_ctx_s::ols_large, 0, 2},    {"fuse_max_d", &ihs_ctx_s::fuse_max_d, 0, 128},
     {"pg_warm", &ihs_ctx_s::pg_warm, 0, 1},       {"small_step", &ihs_ctx_s::small_step, 0, 1},
-    {"pg_cluster", &ihs_ctx_s::pg_cluster, 0, 16},
+    {"pg_cluster", &ihs_ctx_s::pg_cluster, 0, 16}, {"la_gram_sms", &ihs_ctx_s::la_gram_sms, 0, 1024},
+    {"la_gram_tile", &ihs_ctx_s::la_gram_tile, 0, 128},
 };
 }  // namespace
 

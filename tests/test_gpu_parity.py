@@ -181,11 +181,32 @@ def test_gram_lookahead_tiles(P, oracle_mod, m, d):
     rng = np.random.default_rng(m + d)
     SA = torch.from_numpy(rng.standard_normal((m, d))).to(DEV)
     ctx = P.Context(0)
+    ctx.set_option("la_gram_tile", 128)  # the default for d > 256 is the 64-tile stream-K (next test)
     H = P.ihs_gram_lookahead(SA, scale=0.5, ctx=ctx)
     ctx.synchronize()
     Ho = oracle_mod.gram(SA.cpu().numpy())
     Hn = H.cpu().numpy()
     assert rel_fro(Hn, 0.25 * Ho) <= 1e-12
+    np.testing.assert_array_equal(Hn, Hn.T)
+
+
+@pytest.mark.parametrize("tile,sms", [(0, 0), (64, 100), (64, 70), (128, 84), (128, 148)])
+@pytest.mark.parametrize("m,d", [(2048, 1000), (1500, 777)])
+def test_gram_lookahead_tile_and_sm_share(P, oracle_mod, m, d, tile, sms):
+    """The wide (d > 256) look-ahead Gram by its options: the default (64 x 64-tile
+    stream-K on every SM), and either tile on a share of the SMs ("la_gram_sms":
+    the rest are left to the pass it runs beside)."""
+    rng = np.random.default_rng(m + d + tile + sms)
+    SA = torch.from_numpy(rng.standard_normal((m, d))).to(DEV)
+    ctx = P.Context(0)
+    if tile:
+        ctx.set_option("la_gram_tile", tile)
+    if sms:
+        ctx.set_option("la_gram_sms", sms)
+    H = P.ihs_gram_lookahead(SA, scale=2.0, ctx=ctx)
+    ctx.synchronize()
+    Hn = H.cpu().numpy()
+    assert rel_fro(Hn, 4.0 * oracle_mod.gram(SA.cpu().numpy())) <= 1e-12
     np.testing.assert_array_equal(Hn, Hn.T)
 
 
